@@ -1,0 +1,42 @@
+# SPDX-License-Identifier: Apache-2.0
+# Builds the B200 product library (sm_100a) and the CPU oracle.
+#   make            -> paper_2504_17449_b200/_lib/libhmi_b200.so + oracle/_build/liboracle.so
+#   make ref        -> oracle/_ref/libhmiref.so (needs /root/reference; see oracle/build_ref.sh)
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+            --expt-relaxed-constexpr -Xptxas -v
+CSRC     := paper_2504_17449_b200/csrc
+LIBDIR   := paper_2504_17449_b200/_lib
+OBJDIR   := build/obj
+CU_SRCS  := $(wildcard $(CSRC)/*.cu)
+CPP_SRCS := $(wildcard $(CSRC)/*.cpp)
+OBJS     := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS)) \
+            $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.cpp.o,$(CPP_SRCS))
+HDRS     := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) include/hmi_gpu.h
+
+all: $(LIBDIR)/libhmi_b200.so oracle
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; false)
+
+$(OBJDIR)/%.cpp.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -x cu $(ARCH) -c $< -o $@
+
+$(LIBDIR)/libhmi_b200.so: $(OBJS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+ref:
+	bash oracle/build_ref.sh
+
+clean:
+	rm -rf build $(LIBDIR)
+
+.PHONY: all oracle ref clean

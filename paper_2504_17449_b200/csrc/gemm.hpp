@@ -1,0 +1,63 @@
+// SPDX-License-Identifier: Apache-2.0
+// Host interface of the tcgen05 GEMM (K1/K2). See gemm_tcgen05.cuh for the kernel.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "host_util.hpp"
+
+namespace hmi_b200 {
+
+// Kernel-side arguments (passed by value).
+struct GemmArgs {
+  int M, N, K;                 // N is per-group
+  int num_m_tiles, num_n_tiles;
+  const float* bias;           // [N] (+ group * bias_slot_stride floats)
+  long long bias_slot_stride;  // in floats, 0 when weights are shared
+  const int* tile_slot;        // per M tile group index (nullptr: group 0)
+  const __half* res0;          // optional residual inputs, row-major ld = res_ld (16-bit)
+  const __half* res1;
+  int res_ld;
+  uint32_t idesc;
+};
+
+// Epilogue flags
+constexpr int kEpiRelu = 1;
+constexpr int kEpiRes1 = 2;  // add res0
+constexpr int kEpiRes2 = 4;  // add res0 + res1
+constexpr int kEpiOutF32 = 8;
+
+// Everything needed to bind one GEMM to fixed device buffers.
+struct GemmSpec {
+  const void* a = nullptr;  // [a_rows][a_ld] 16-bit
+  int a_rows = 0, a_ld = 0, K = 0;
+  const void* b = nullptr;  // [groups][N][b_ld] 16-bit
+  int N = 0, groups = 1, b_ld = 0;
+  size_t b_group_stride_bytes = 0;
+  const float* bias = nullptr;       // [groups][bias_group_stride]
+  long long bias_group_stride = 0;   // floats
+  const int* tile_slot = nullptr;    // per 128-row tile group index (device), or null
+  const void* res0 = nullptr;        // 16-bit residuals [rows][res_ld]
+  const void* res1 = nullptr;
+  int res_ld = 0;
+  void* c = nullptr;                 // output [a_rows][c_ld], 16-bit or f32
+  int c_ld = 0;
+  int epi = 0;                       // kEpi* flags
+  int bn = 256;                      // N tile
+  int precision = 0;                 // 0 fp16, 1 bf16
+};
+
+struct GemmPlan {
+  CUtensorMap map_a, map_b, map_c;
+  GemmArgs args;
+  void* fn = nullptr;
+  int smem_bytes = 0;
+  int max_rows = 0;
+};
+
+GemmPlan make_gemm_plan(const GemmSpec& s);
+void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream);
+
+}  // namespace hmi_b200

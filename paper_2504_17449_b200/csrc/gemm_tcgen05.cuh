@@ -1,0 +1,264 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K1/K2 — persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[M x N] = epilogue( A[M x K] . B^T )   A: 16-bit row-major (K-major)
+//                                           B: 16-bit [groups][N][K]   (K-major, 3-D TMA map)
+//
+// Replaces every `gemm_f64` call on the hot path (proj/src/tensor/kernels_scalar.cpp:11-26
+// via matmul_into, proj/src/tensor/ops.cpp:25-36):
+//   * attention Q/K/V and output projections (proj/src/transformer/model.cpp:35-37, :75)
+//   * FFN (model.cpp:78-82) with the bias+ReLU epilogue fused
+//   * the tenant-grouped adapter products (proj/src/adapters/stacked.cpp:44-64) — "grouped"
+//     mode: every 128-row M tile belongs to exactly one request, and the B tile is
+//     gathered from that request's HBM slot (tile_slot[m_tile] selects the group).
+//
+// Roles (192 threads, 1 CTA per SM):
+//   warp 0      : TMA producer (one elected lane)      smem ring of kStages (A,B) tiles
+//   warp 1      : TMEM allocator + MMA issuer (lane 0)  2 TMEM accumulators of BN fp32 cols
+//   warps 2..5  : epilogue, TMEM -> regs -> bias/ReLU/residual -> 16/32-bit -> smem -> TMA store
+#pragma once
+
+#include "gemm.hpp"
+#include "sm100.cuh"
+
+namespace hmi_b200 {
+
+constexpr int kGemmThreads = 192;
+constexpr int kBlockM = 128;
+constexpr int kBlockK = 64;  // 64 x 16-bit = 128 B = one SWIZZLE_128B atom row
+
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
+  static constexpr int kBBytes = BN * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 warps x double buffer x (32 rows x 128 B)
+  static constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 256 /*barriers*/;
+  static constexpr int kStagesRaw = (kBudget - kEpiBytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+  static constexpr int kTotal = 1024 + kStages * kStageBytes + kEpiBytes + 256;
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                 : 2 * BN <= 256 ? 256 : 512;
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_c, const GemmArgs args) {
+  using L = GemmSmem<BN>;
+  constexpr int kStages = L::kStages;
+  static_assert(kStages >= 2, "smem budget too small");
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+  constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
+  constexpr int kCW = kOutF32 ? 32 : 64;  // output columns per 128-byte staging row
+  static_assert(BN % kCW == 0, "BN must be a multiple of the store chunk");
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * L::kABytes;
+  uint8_t* sEpi = smem + kStages * L::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* tempty = bars + 2 * kStages + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int num_tiles = args.num_m_tiles * args.num_n_tiles;
+  const int num_kb = args.K / kBlockK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    tma_prefetch_desc(&map_c);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_first();
+      const uint64_t pol_b = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int mt = t / args.num_n_tiles;
+        const int nt = t - mt * args.num_n_tiles;
+        const int grp = args.tile_slot ? __ldg(&args.tile_slot[mt]) : 0;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          tma_load_2d_hint(sA + stage * L::kABytes, &map_a, &full[stage], kb * kBlockK,
+                           mt * kBlockM, pol_a);
+          tma_load_3d_hint(sB + stage * L::kBBytes, &map_b, &full[stage], kb * kBlockK,
+                           nt * BN, grp, pol_b);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a_desc = sdesc_k_sw128(smem_u32(sA + stage * L::kABytes));
+          const uint64_t b_desc = sdesc_k_sw128(smem_u32(sB + stage * L::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kBlockK / 16; ++k) {
+            // +32 B along K inside the 128 B swizzle atom = +2 in the 16 B address field
+            umma_f16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, args.idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
+    uint32_t sbuf = 0, acc = 0, acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int mt = t / args.num_n_tiles;
+      const int nt = t - mt * args.num_n_tiles;
+      const int grp = args.tile_slot ? __ldg(&args.tile_slot[mt]) : 0;
+      const float* bias = args.bias + grp * args.bias_slot_stride + nt * BN;
+      const int row0 = mt * kBlockM + q * 32;
+      const int row = row0 + lane;
+      const bool row_ok = row < args.M;
+
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((q * 32) << 16) + acc * BN;
+
+#pragma unroll 1
+      for (int c = 0; c < BN; c += kCW) {
+        float v[kCW];
+#pragma unroll
+        for (int j = 0; j < kCW / 32; ++j) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
+        }
+        if (c + kCW >= BN) {
+          // all TMEM reads of this accumulator are done: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+#pragma unroll
+        for (int i = 0; i < kCW; i += 4) {
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
+          v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+        }
+        if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
+          if (row_ok) {
+            const int col = nt * BN + c;
+            const __half* r0 = args.res0 + static_cast<long long>(row) * args.res_ld + col;
+#pragma unroll
+            for (int i = 0; i < kCW; i += 8) {
+              const uint4 u = __ldg(reinterpret_cast<const uint4*>(r0 + i));
+              const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __half22float2(h2[e]);
+                v[i + 2 * e] += f.x;
+                v[i + 2 * e + 1] += f.y;
+              }
+            }
+            if constexpr ((EPI & kEpiRes2) != 0) {
+              const __half* r1 = args.res1 + static_cast<long long>(row) * args.res_ld + col;
+#pragma unroll
+              for (int i = 0; i < kCW; i += 8) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(r1 + i));
+                const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __half22float2(h2[e]);
+                  v[i + 2 * e] += f.x;
+                  v[i + 2 * e + 1] += f.y;
+                }
+              }
+            }
+          }
+        }
+        if constexpr ((EPI & kEpiRelu) != 0) {
+#pragma unroll
+          for (int i = 0; i < kCW; ++i) v[i] = fmaxf(v[i], 0.0f);
+        }
+        // pack one 128-byte row per thread
+        uint32_t packed[32];
+        if constexpr (kOutF32) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) packed[i] = __float_as_uint(v[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+            packed[i] = *reinterpret_cast<const uint32_t*>(&h);
+          }
+        }
+        // staging buffer reuse: the store issued two chunks ago must have read it
+        if (lane == 0) tma_store_wait_read<1>();
+        __syncwarp();
+        uint8_t* buf = stg + sbuf * 4096;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int phys = i ^ (lane & 7);  // SWIZZLE_128B: 16 B chunk ^= row % 8
+          *reinterpret_cast<uint4*>(buf + lane * 128 + phys * 16) =
+              make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_c, buf, nt * BN + c, row0);
+          tma_store_commit();
+        }
+        sbuf ^= 1;
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<L::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace hmi_b200
