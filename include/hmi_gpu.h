@@ -48,6 +48,155 @@ extern "C" {
 /* Thread-local text of the last failing call on this thread. */
 const char* hmi_gpu_last_error(void);
 
+/* ---- configuration ------------------------------------------------------ */
+/* ModelConfig (proj/include/hmi/transformer/config.hpp:10-24), HMI1 header order. */
+typedef struct hmi_model_config {
+  uint32_t hidden_size, heads, lower_layers, higher_layers, ffn_size, vocab_size;
+  uint32_t mode; /* 0 encoder, 1 causal (AttentionMode) */
+  uint32_t max_fragment;
+  uint32_t seed;
+} hmi_model_config;
+
+/* Device-side options (not part of the reference; SURVEY.md §5 "device config"). */
+typedef struct hmi_gpu_options {
+  uint32_t precision;     /* GEMM/attention operand type: 0 fp16 (default), 1 bf16      */
+  uint32_t max_batch;     /* max requests per batch (BatchQueue max_batch_size)          */
+  uint32_t max_seq;       /* max request length; rows are padded to a multiple of 128    */
+  uint32_t bottleneck;    /* adapter r shared by all tasks (stack() requires uniform r)  */
+  uint32_t max_labels;    /* widest cls / token_tag / lm head                             */
+  uint32_t pipeline_mode; /* 0 sync, 1 coarse, 2 fine                  */
+  uint64_t pool_bytes;    /* DeviceSlotPool capacity in the reference's f32 byte
+                             accounting (device_pool.hpp:40, adapter_set.hpp:24-27);
+                             0 = room for every task (max_tasks)                          */
+  uint32_t max_tasks, max_instances, max_heads, max_versions;
+} hmi_gpu_options;
+
+typedef struct hmi_gpu_ctx hmi_gpu_ctx;
+
+/* Creates a context on `device` and uploads the shared higher-stack weights.
+ * higher_f32: higher_layers blocks of the HMI1 per-layer payload, f32, in
+ * declaration order wq,bq,wk,bk,wv,bv,wo,bo,w1,b1,w2,b2,ln1_gain,ln1_shift,
+ * ln2_gain,ln2_shift (model_io.cpp:19-36; weights.hpp:15-21, matrices [in x out]).
+ * Replaces: the numeric Backend's model artefacts.            */
+int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_options* opts,
+                   const float* higher_f32, hmi_gpu_ctx** out);
+int hmi_gpu_destroy(hmi_gpu_ctx* ctx);
+
+/* ---- domain knowledge: PLOT version tree -------------------------------- */
+/* Uploads one PLOT table version (PlotTable, plot/table.hpp:26-40; PLT1 body
+ * plot_io.cpp:26-31). parent_id = 0xffffffff for the root. Entry e has key
+ * key_len[e] tokens in keys[e*max_fragment ...] and key_len[e] rep rows in
+ * reps (rows concatenated in entry order, hidden_size f32 each).
+ * Errors mirror VersionTree::add_branch (version_tree.cpp:17-30) and PLT1 load
+ * (plot_io.cpp:36-73): unknown parent -> ROUTING, duplicate version -> CONFLICT,
+ * bad key length / duplicate key -> FORMAT, token >= vocab -> VOCABULARY.     */
+int hmi_gpu_upload_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t parent_id,
+                         uint32_t n_entries, const uint32_t* key_len, const uint32_t* keys,
+                         const float* reps);
+
+/* ---- task knowledge ------------------------------------------------------ */
+/* Registers a task's adapter set (AdapterStore::register_set, store.cpp:9-18)
+ * into pinned host memory; nothing is copied to HBM until a batch needs it.
+ * adapter_f32: higher_layers blocks of w_down[d x r], b_down[r], w_up[r x d],
+ * b_up[d] (the ADP1 body, adapter_set.cpp:38-43). Duplicate -> CONFLICT.    */
+int hmi_gpu_register_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapter_f32);
+/* AdapterStore::replace (store.cpp:20-27): swaps the host copy; a resident
+ * device copy is evicted so the next batch reloads it. Unknown -> ROUTING.   */
+int hmi_gpu_replace_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapter_f32);
+/* AdapterStore::erase + DeviceSlotPool::evict (SPEC.md:527 delete_instance). */
+int hmi_gpu_unregister_task(hmi_gpu_ctx* ctx, uint32_t task_idx);
+
+/* OutputHead (weights.hpp:45-53): kind 0 cls_classify, 1 token_tag,
+ * 2 lm_logits; w [hidden x labels] f32, b [labels] f32.                      */
+int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, uint32_t labels,
+                          const float* w, const float* b);
+
+/* InstanceBinding (scheduler/request.hpp:30-36) / VersionTree::bind_instance
+ * (version_tree.cpp:81-93): instance -> (version, task, head).
+ * Already bound -> CONFLICT; unknown version/task/head -> ROUTING.            */
+int hmi_gpu_bind_instance(hmi_gpu_ctx* ctx, uint32_t instance_idx, uint32_t version_id,
+                          uint32_t task_idx, uint32_t head_idx);
+int hmi_gpu_unbind_instance(hmi_gpu_ctx* ctx, uint32_t instance_idx);
+
+/* ---- serving ------------------------------------------------------------- */
+/* One adapter load / hit of a batch, the LoadRecord of device_pool.hpp:27-33
+ * (evicted task indices are written to the separate `evicted` array).        */
+typedef struct hmi_load_record {
+  uint32_t task;
+  int32_t layer;          /* -1: all layers (ensure_resident), else the prefetched layer */
+  int32_t hit;
+  uint32_t n_evicted;
+  uint64_t bytes;         /* reference f32 accounting */
+  uint32_t evicted_offset;
+  uint32_t pad;
+} hmi_load_record;
+
+/* Runs one mixed-tenant batch end to end (stage_compute for every higher layer,
+ * SPEC.md:461-469, with on-device retrieval, routing, swap and head):
+ *   instance_idx[n_req], tokens[n_req x stride] (request i uses lens[i] ids),
+ *   scores[n_req x max_labels] f32 (cls / lm logits), labels[n_req] (argmax,
+ *   -1 for token_tag), tags[n_req x stride] (token_tag only; nullable).
+ * trace/evicted (nullable): up to trace_cap records / evicted_cap ids;
+ * *n_trace receives the record count.                                           */
+int hmi_gpu_infer_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                        const uint32_t* tokens, uint32_t stride, const uint32_t* lens,
+                        float* scores, int32_t* labels, int32_t* tags, hmi_load_record* trace,
+                        uint32_t trace_cap, uint32_t* evicted, uint32_t evicted_cap,
+                        uint32_t* n_trace);
+
+/* Same batch with device-resident tokens/lens and device outputs; enqueued on
+ * the context's compute stream without a host synchronisation (the routing
+ * of instance_idx for the slot pool is host-side). d_tokens is [n_req x stride]. */
+int hmi_gpu_infer_batch_device(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                               const uint32_t* d_tokens, uint32_t stride,
+                               const uint32_t* d_lens, uint32_t max_len, float* d_scores,
+                               int32_t* d_labels);
+/* Waits for every enqueued batch; returns the first device-side error. */
+int hmi_gpu_synchronize(hmi_gpu_ctx* ctx);
+/* cudaStream_t of the compute stream (for event timing by the caller). */
+void* hmi_gpu_stream(hmi_gpu_ctx* ctx);
+
+/* ---- introspection ------------------------------------------------------- */
+/* Routing of the last batch: per request version/task/head, and the HBM slot
+ * of each (request, layer) in slots[layer * n_req + i].                       */
+int hmi_gpu_debug_routing(hmi_gpu_ctx* ctx, int32_t* version, int32_t* task, int32_t* head,
+                          int32_t* slots);
+/* Gather indices of the last batch: for row (i, p) and its k-th covering
+ * window (ascending window order), the global PLOT rep row (upload order) and
+ * the sub-gram level; -1 / 0 where unused. Arrays are [n_req x S x max_fragment]
+ * with S = the batch's padded length (returned in *S).                        */
+int hmi_gpu_debug_gather(hmi_gpu_ctx* ctx, int32_t* rows, int32_t* levels, uint32_t* S);
+/* flags bit0: capture the f64 retrieval output h0 of the next batches.        */
+int hmi_gpu_set_debug(hmi_gpu_ctx* ctx, uint32_t flags);
+int hmi_gpu_debug_h0(hmi_gpu_ctx* ctx, double* out);           /* [n_req x S x d] */
+int hmi_gpu_debug_hidden(hmi_gpu_ctx* ctx, float* out);        /* final f32 rows */
+/* DeviceSlotPool counters (device_pool.cpp:190-217):
+ * out[0] hits, [1] loads, [2] resident_bytes, [3] max_resident_bytes_seen,
+ * [4] resident_task_count, [5] capacity_bytes, [6] physical slots,
+ * [7] bytes actually copied host->device (16-bit device layout).            */
+int hmi_gpu_pool_stats(hmi_gpu_ctx* ctx, uint64_t* out);
+int hmi_gpu_pool_slot(hmi_gpu_ctx* ctx, uint32_t task_idx, uint32_t layer, int32_t* slot);
+
+/* Per-kernel-class device time (CUDA events around every launch while enabled). */
+#define HMI_PROF_CLASSES 16
+int hmi_gpu_profile(hmi_gpu_ctx* ctx, int enable);
+/* ms[c], count[c] accumulated since enable; names in hmi_gpu_profile_name(c). */
+int hmi_gpu_profile_read(hmi_gpu_ctx* ctx, double* ms, uint64_t* count);
+const char* hmi_gpu_profile_name(int cls);
+
+/* ---- standalone slot-pool policy (host only; trace parity tests) ---------- */
+typedef struct hmi_pool hmi_pool;
+int hmi_pool_create(uint64_t capacity_bytes, hmi_pool** out);
+int hmi_pool_destroy(hmi_pool* pool);
+int hmi_pool_register(hmi_pool* pool, uint32_t task, uint32_t layers, uint64_t layer_bytes);
+/* op 0 ensure_resident, 1 try_ensure_layer_resident(layer), 2 pin, 3 unpin, 4 touch,
+ * 5 evict(tasks[0]). Returns records like hmi_gpu_infer_batch; *n_trace = -1
+ * encodes try_ensure's nullopt. Errors as the reference (CAPACITY, ROUTING...). */
+int hmi_pool_op(hmi_pool* pool, int op, uint32_t n, const uint32_t* tasks, uint32_t layer,
+                hmi_load_record* trace, uint32_t trace_cap, uint32_t* evicted,
+                uint32_t evicted_cap, int32_t* n_trace);
+int hmi_pool_stats(hmi_pool* pool, uint64_t* out);
+
 /* ---- standalone kernel probe (K1/K2 GEMM) ------------------------------ */
 /* C[M x N] = epi(A[M x K] . B[g]^T + bias[g]) for a device-side tcgen05 GEMM,
  * host buffers in/out, used by the parity tests of the GEMM kernel alone.

@@ -1,9 +1,9 @@
 # SPDX-License-Identifier: Apache-2.0
-"""ctypes loader for the in-tree C-ABI library ``_lib/libhmi_b200.so``.
+"""ctypes binding of the in-tree C-ABI library ``_lib/libhmi_b200.so``.
 
-The product path has no CPU fallback: if the shared library is missing or does
-not export the symbols declared in ``include/hmi_gpu.h`` this module raises at
-import time of :func:`lib`.
+The product path has no CPU fallback: if the shared library is missing this
+module raises on first use (:func:`lib`). Status codes become the Python
+mirrors of the reference's exception classes (proj/include/hmi/errors.hpp).
 """
 from __future__ import annotations
 
@@ -17,19 +17,78 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "hmi_gpu.h")
 
 _lib = None
 
-STATUS_NAMES = {
-    0: "OK",
-    1: "DimensionError",
-    2: "VocabularyError",
-    3: "ConflictError",
-    4: "CapacityError",
-    5: "RoutingError",
-    6: "ConfigError",
-    7: "BuildError",
-    8: "SchedulingBugError",
-    9: "FormatError",
-    100: "CudaError",
-}
+
+class HmiError(RuntimeError):
+    code = -1
+
+
+class DimensionError(HmiError, ValueError):
+    code = 1
+
+
+class VocabularyError(HmiError, IndexError):
+    code = 2
+
+
+class ConflictError(HmiError):
+    code = 3
+
+
+class CapacityError(HmiError):
+    code = 4
+
+
+class RoutingError(HmiError):
+    code = 5
+
+
+class ConfigError(HmiError):
+    code = 6
+
+
+class BuildError(HmiError):
+    code = 7
+
+
+class SchedulingBugError(HmiError):
+    code = 8
+
+
+class FormatError(HmiError):
+    code = 9
+
+
+class CudaError(HmiError):
+    code = 100
+
+
+ERRORS = {c.code: c for c in (DimensionError, VocabularyError, ConflictError, CapacityError,
+                              RoutingError, ConfigError, BuildError, SchedulingBugError,
+                              FormatError, CudaError)}
+STATUS_NAMES = {0: "OK", **{k: v.__name__ for k, v in ERRORS.items()}}
+
+
+class ModelConfig(ctypes.Structure):
+    """hmi_model_config == ModelConfig (proj/include/hmi/transformer/config.hpp:10-24)."""
+
+    _fields_ = [(n, ctypes.c_uint32) for n in (
+        "hidden_size", "heads", "lower_layers", "higher_layers", "ffn_size", "vocab_size",
+        "mode", "max_fragment", "seed")]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("precision", ctypes.c_uint32), ("max_batch", ctypes.c_uint32),
+                ("max_seq", ctypes.c_uint32), ("bottleneck", ctypes.c_uint32),
+                ("max_labels", ctypes.c_uint32), ("pipeline_mode", ctypes.c_uint32),
+                ("pool_bytes", ctypes.c_uint64), ("max_tasks", ctypes.c_uint32),
+                ("max_instances", ctypes.c_uint32), ("max_heads", ctypes.c_uint32),
+                ("max_versions", ctypes.c_uint32)]
+
+
+class LoadRecord(ctypes.Structure):
+    _fields_ = [("task", ctypes.c_uint32), ("layer", ctypes.c_int32), ("hit", ctypes.c_int32),
+                ("n_evicted", ctypes.c_uint32), ("bytes", ctypes.c_uint64),
+                ("evicted_offset", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
 
 
 def declared_symbols(header: str = HEADER_PATH) -> list[str]:
@@ -39,6 +98,46 @@ def declared_symbols(header: str = HEADER_PATH) -> list[str]:
     return sorted(set(re.findall(r"\b(hmi_[a-z0-9_]+)\s*\(", text)))
 
 
+def _sig(L):
+    vp, u32, i32, u64 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int32, ctypes.c_uint64
+    P = ctypes.POINTER
+    f32p, f64p = P(ctypes.c_float), P(ctypes.c_double)
+    u32p, i32p, u64p = P(u32), P(i32), P(u64)
+    L.hmi_gpu_last_error.restype = ctypes.c_char_p
+    L.hmi_gpu_create.argtypes = [ctypes.c_int, P(ModelConfig), P(Options), f32p, P(vp)]
+    L.hmi_gpu_destroy.argtypes = [vp]
+    L.hmi_gpu_upload_table.argtypes = [vp, u32, u32, u32, u32p, u32p, f32p]
+    L.hmi_gpu_register_task.argtypes = [vp, u32, f32p]
+    L.hmi_gpu_replace_task.argtypes = [vp, u32, f32p]
+    L.hmi_gpu_unregister_task.argtypes = [vp, u32]
+    L.hmi_gpu_register_head.argtypes = [vp, u32, u32, u32, f32p, f32p]
+    L.hmi_gpu_bind_instance.argtypes = [vp, u32, u32, u32, u32]
+    L.hmi_gpu_unbind_instance.argtypes = [vp, u32]
+    L.hmi_gpu_infer_batch.argtypes = [vp, u32, u32p, u32p, u32, u32p, f32p, i32p, i32p,
+                                      P(LoadRecord), u32, u32p, u32, u32p]
+    L.hmi_gpu_infer_batch_device.argtypes = [vp, u32, u32p, vp, u32, vp, u32, vp, vp]
+    L.hmi_gpu_synchronize.argtypes = [vp]
+    L.hmi_gpu_stream.argtypes = [vp]
+    L.hmi_gpu_stream.restype = vp
+    L.hmi_gpu_debug_routing.argtypes = [vp, i32p, i32p, i32p, i32p]
+    L.hmi_gpu_debug_gather.argtypes = [vp, i32p, i32p, u32p]
+    L.hmi_gpu_set_debug.argtypes = [vp, u32]
+    L.hmi_gpu_debug_h0.argtypes = [vp, f64p]
+    L.hmi_gpu_debug_hidden.argtypes = [vp, f32p]
+    L.hmi_gpu_pool_stats.argtypes = [vp, u64p]
+    L.hmi_gpu_pool_slot.argtypes = [vp, u32, u32, i32p]
+    L.hmi_gpu_profile.argtypes = [vp, ctypes.c_int]
+    L.hmi_gpu_profile_read.argtypes = [vp, f64p, u64p]
+    L.hmi_gpu_profile_name.argtypes = [ctypes.c_int]
+    L.hmi_gpu_profile_name.restype = ctypes.c_char_p
+    L.hmi_pool_create.argtypes = [u64, P(vp)]
+    L.hmi_pool_destroy.argtypes = [vp]
+    L.hmi_pool_register.argtypes = [vp, u32, u32, u64]
+    L.hmi_pool_op.argtypes = [vp, ctypes.c_int, u32, u32p, u32, P(LoadRecord), u32, u32p, u32,
+                              P(i32)]
+    L.hmi_pool_stats.argtypes = [vp, u64p]
+
+
 def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
@@ -46,11 +145,18 @@ def lib() -> ctypes.CDLL:
             raise RuntimeError(
                 f"B200 extension not built: {LIB_PATH} is missing (run __graft_entry__.build())"
             )
-        _lib = ctypes.CDLL(LIB_PATH)
-        _lib.hmi_gpu_last_error.restype = ctypes.c_char_p
+        L = ctypes.CDLL(LIB_PATH)
+        _sig(L)
+        _lib = L
     return _lib
 
 
 def last_error() -> str:
     msg = lib().hmi_gpu_last_error()
     return msg.decode() if msg else ""
+
+
+def check(status: int) -> None:
+    if status != 0:
+        cls = ERRORS.get(status, HmiError)
+        raise cls(f"[{STATUS_NAMES.get(status, status)}] {last_error()}")

@@ -1,0 +1,1351 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// The CUDA backend of the hPLM scheduler: one context per GPU.
+//
+// Restates, for a device, the SPEC's numeric Backend + stage_compute / run
+// and the reference's per-request path it must equal
+// (retrieve_sequence + higher_stack_forward):
+//
+//   host                     | copy stream               | compute stream
+//   -------------------------+---------------------------+-------------------------------
+//   route tasks (host mirror)|                           |
+//   SlotPool decisions       | H2D adapter (task,layer)  | H2D tokens/lens/ids, slot deltas
+//     (LRU/pin law of        |   -> HBM slot, per layer  | K6 route  (instance -> version,
+//      DeviceSlotPool)       |   event ev_layer[l]       |            task, head, slots)
+//                            |                           | K5 PLOT retrieval (Eq. 2/3)
+//                            |                           | per layer l:
+//                            |                           |   K1 QKV, K3 attention, K1 O
+//                            |                           |   wait ev_layer[l]
+//                            |                           |   K2 adapter down/up (+skip+res)
+//                            |                           |   K4 LN1, K1 FFN1, K1 FFN2(+res)
+//                            |                           |   K4 LN2
+//                            |                           | K7 head + argmax, D2H
+//
+// Pipeline modes: sync waits for the previous batch and for
+// every adapter copy before retrieval; coarse lets the next batch's copies run
+// while the current batch computes (one event for all layers); fine waits per
+// layer, so layer l+1's copies overlap layer l's compute.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "gemm.hpp"
+#include "kernels.hpp"
+#include "slot_pool.hpp"
+
+namespace hmi_b200 {
+
+void launch_apply_deltas(int32_t* table, const int32_t* pairs, int n, cudaStream_t stream);
+
+namespace {
+
+constexpr int kStaging = 4;
+
+enum ProfClass {
+  P_H2D = 0, P_ROUTE, P_RETRIEVE, P_QKV, P_ATTN, P_OPROJ, P_AD_DOWN, P_AD_UP, P_LN1, P_FFN1,
+  P_FFN2, P_LN2, P_HEAD, P_D2H, P_COPY, P_STEP
+};
+const char* kProfNames[HMI_PROF_CLASSES] = {
+    "h2d_inputs", "route",  "retrieve", "gemm_qkv", "attention", "gemm_oproj",
+    "adapter_down", "adapter_up", "layernorm1", "gemm_ffn1", "gemm_ffn2", "layernorm2",
+    "head", "d2h_outputs", "adapter_copy", "step"};
+
+uint16_t f2h(float x, int precision) {
+  if (precision == 1) {
+    __nv_bfloat16 b = __float2bfloat16_rn(x);
+    return *reinterpret_cast<uint16_t*>(&b);
+  }
+  __half h = __float2half_rn(x);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    free();
+    if (count) HMI_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct LayerDev {
+  void* mem = nullptr;  // one allocation per layer
+  uint16_t *wqkv, *wo, *w1, *w2;  // [N][K] 16-bit (transposed from [in x out])
+  float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
+  GemmPlan qkv, oproj, ad_down, ad_up, ffn1, ffn2;
+};
+
+struct Staging {
+  uint32_t* inst = nullptr;
+  uint32_t* tokens = nullptr;
+  int32_t* lens = nullptr;
+  int32_t* delta = nullptr;  // (index, value) pairs
+  float* scores = nullptr;
+  int32_t* labels = nullptr;
+  int32_t* tags = nullptr;
+  int32_t* err = nullptr;
+  cudaEvent_t done = nullptr;
+  bool busy = false;
+};
+
+struct Inflight {
+  cudaEvent_t done;
+  int staging;
+  std::vector<uint32_t> tasks;
+};
+
+int pick_bn(int N, int m_tiles, int sms) {
+  int best = -1;
+  double best_eff = -1;
+  for (int bn : {256, 192, 128, 64}) {
+    if (N % bn) continue;
+    const long tiles = static_cast<long>(N / bn) * m_tiles;
+    const long waves = (tiles + sms - 1) / sms;
+    const double eff = static_cast<double>(tiles) / (waves * sms);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+}  // namespace
+
+struct Ctx {
+  int device = 0;
+  hmi_model_config cfg{};
+  hmi_gpu_options opt{};
+  int d = 0, f = 0, L = 0, heads = 0, ngram = 3, r = 0, r_pad = 0;
+  int S_max = 0, max_rows = 0, tile_stride = 0;
+  size_t slot_bytes = 0;         // device bytes per (task, layer)
+  uint64_t ref_layer_bytes = 0;  // reference f32 accounting per layer
+  cudaStream_t compute = nullptr, copy = nullptr;
+  std::mutex mu;
+
+  std::vector<LayerDev> layers;
+  // activations
+  DevBuf<uint16_t> h16, qkv16, ctx16, a16, mid16, x16, ffn16;
+  DevBuf<float> y32, h32;
+  DevBuf<double> h64;
+  // per-batch device inputs / routing
+  DevBuf<uint32_t> d_inst, d_tokens;
+  DevBuf<int32_t> d_lens, d_delta, d_req_version, d_req_task, d_req_head, d_tile_slot, d_err;
+  DevBuf<int32_t> d_gather, d_levels;
+  DevBuf<float> d_scores;
+  DevBuf<int32_t> d_labels, d_tags;
+  // tables
+  DevBuf<int32_t> d_inst_version, d_inst_task, d_inst_head, d_slot_of;
+  std::vector<int32_t> h_inst_version, h_inst_task, h_inst_head;
+  // PLOT
+  std::vector<PlotSlot> h_slots;
+  uint64_t n_keys = 0;
+  std::vector<int32_t> h_parent;  // -2 = absent
+  DevBuf<PlotSlot> d_slots;
+  DevBuf<int32_t> d_parent;
+  DevBuf<float> d_reps;
+  uint64_t rep_rows = 0;
+  // heads
+  DevBuf<float> d_head_arena;
+  uint64_t head_floats = 0;
+  DevBuf<int64_t> d_head_off;
+  DevBuf<int32_t> d_head_labels, d_head_kind;
+  std::vector<int64_t> h_head_off;
+  std::vector<int32_t> h_head_labels, h_head_kind;
+  // adapters: pinned host store + HBM slot arena
+  std::unique_ptr<SlotPool> pool;
+  DevBuf<uint8_t> arena;
+  std::vector<uint8_t*> store;  // per task, L * slot_bytes pinned, or null
+  std::vector<uint8_t*> pinned_chunks;
+  std::vector<uint8_t*> free_blocks;
+  uint8_t* chunk_cur = nullptr;
+  size_t chunk_left = 0;
+  uint64_t bytes_copied = 0;
+  std::vector<cudaEvent_t> ev_layer;
+  // staging / in-flight batches
+  Staging stg[kStaging];
+  int stg_next = 0;
+  std::deque<Inflight> inflight;
+  // last batch (introspection)
+  uint32_t last_n = 0, last_S = 0;
+  uint32_t debug_flags = 0;
+  // profiling
+  bool prof = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+  std::vector<cudaEvent_t> prof_free;
+  double prof_ms[HMI_PROF_CLASSES] = {};
+  uint64_t prof_cnt[HMI_PROF_CLASSES] = {};
+
+  ~Ctx();
+
+  cudaEvent_t ev() {
+    cudaEvent_t e;
+    if (!prof_free.empty()) {
+      e = prof_free.back();
+      prof_free.pop_back();
+    } else {
+      HMI_CUDA(cudaEventCreate(&e));
+    }
+    return e;
+  }
+  template <typename F>
+  void timed(int cls, cudaStream_t s, F&& fn) {
+    if (!prof) {
+      fn();
+      return;
+    }
+    cudaEvent_t a = ev(), b = ev();
+    HMI_CUDA(cudaEventRecord(a, s));
+    fn();
+    HMI_CUDA(cudaEventRecord(b, s));
+    prof_pending.push_back({cls, {a, b}});
+  }
+  void prof_collect() {
+    for (auto& [cls, e] : prof_pending) {
+      HMI_CUDA(cudaEventSynchronize(e.second));
+      float ms = 0;
+      HMI_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+      prof_ms[cls] += ms;
+      prof_cnt[cls] += 1;
+      prof_free.push_back(e.first);
+      prof_free.push_back(e.second);
+    }
+    prof_pending.clear();
+  }
+
+  uint8_t* store_alloc() {
+    if (!free_blocks.empty()) {
+      uint8_t* p = free_blocks.back();
+      free_blocks.pop_back();
+      return p;
+    }
+    const size_t need = static_cast<size_t>(L) * slot_bytes;
+    if (chunk_left < need) {
+      const size_t chunk = std::max<size_t>(need, size_t(256) << 20);
+      uint8_t* p = nullptr;
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), chunk, cudaHostAllocPortable));
+      pinned_chunks.push_back(p);
+      chunk_cur = p;
+      chunk_left = chunk;
+    }
+    uint8_t* p = chunk_cur;
+    chunk_cur += need;
+    chunk_left -= need;
+    return p;
+  }
+
+  void reap(bool all);
+  void build_plans();
+  void upload_plot_hash();
+  void convert_adapter(const float* src, uint8_t* dst) const;
+  int submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_host,
+             const uint32_t* tokens_dev, uint32_t stride, const uint32_t* lens_host,
+             const uint32_t* lens_dev, uint32_t max_len, float* d_scores_out,
+             int32_t* d_labels_out, std::vector<PoolRecord>* records,
+             std::vector<int32_t>* record_layer);
+};
+
+Ctx::~Ctx() {
+  if (compute) cudaStreamSynchronize(compute);
+  if (copy) cudaStreamSynchronize(copy);
+  for (auto& l : layers)
+    if (l.mem) cudaFree(l.mem);
+  for (auto& s : stg) {
+    for (void* p : {static_cast<void*>(s.inst), static_cast<void*>(s.tokens),
+                    static_cast<void*>(s.lens), static_cast<void*>(s.delta),
+                    static_cast<void*>(s.scores), static_cast<void*>(s.labels),
+                    static_cast<void*>(s.tags), static_cast<void*>(s.err)})
+      if (p) cudaFreeHost(p);
+    if (s.done) cudaEventDestroy(s.done);
+  }
+  for (auto* p : pinned_chunks) cudaFreeHost(p);
+  for (auto e : ev_layer) cudaEventDestroy(e);
+  for (auto& [c, e] : prof_pending) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (auto e : prof_free) cudaEventDestroy(e);
+  h16.free(); qkv16.free(); ctx16.free(); a16.free(); mid16.free(); x16.free(); ffn16.free();
+  y32.free(); h32.free(); h64.free();
+  d_inst.free(); d_tokens.free(); d_lens.free(); d_delta.free(); d_req_version.free();
+  d_req_task.free(); d_req_head.free(); d_tile_slot.free(); d_err.free(); d_gather.free();
+  d_levels.free(); d_scores.free(); d_labels.free(); d_tags.free();
+  d_inst_version.free(); d_inst_task.free(); d_inst_head.free(); d_slot_of.free();
+  d_slots.free(); d_parent.free(); d_reps.free(); d_head_arena.free(); d_head_off.free();
+  d_head_labels.free(); d_head_kind.free(); arena.free();
+  if (compute) cudaStreamDestroy(compute);
+  if (copy) cudaStreamDestroy(copy);
+}
+
+// Device layout of one (task, layer) adapter slot:
+//   [Wd^T: r_pad x d 16-bit][Wu^T: d x r_pad 16-bit][bd: r_pad f32][bu: d f32]
+// rows beyond r are zero, so the padded GEMMs add exact zeros.
+void Ctx::convert_adapter(const float* src, uint8_t* dst) const {
+  const int prec = static_cast<int>(opt.precision);
+  for (int l = 0; l < L; ++l) {
+    const float* wd = src;
+    const float* bd = wd + static_cast<size_t>(d) * r;
+    const float* wu = bd + r;
+    const float* bu = wu + static_cast<size_t>(r) * d;
+    src = bu + d;
+    uint8_t* slot = dst + static_cast<size_t>(l) * slot_bytes;
+    uint16_t* wdt = reinterpret_cast<uint16_t*>(slot);
+    uint16_t* wut = wdt + static_cast<size_t>(r_pad) * d;
+    float* bdd = reinterpret_cast<float*>(wut + static_cast<size_t>(d) * r_pad);
+    float* bud = bdd + r_pad;
+    std::memset(slot, 0, slot_bytes);
+    for (int j = 0; j < r; ++j)
+      for (int i = 0; i < d; ++i) wdt[static_cast<size_t>(j) * d + i] = f2h(wd[static_cast<size_t>(i) * r + j], prec);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < r; ++j) wut[static_cast<size_t>(i) * r_pad + j] = f2h(wu[static_cast<size_t>(j) * d + i], prec);
+    for (int j = 0; j < r; ++j) bdd[j] = bd[j];
+    for (int i = 0; i < d; ++i) bud[i] = bu[i];
+  }
+}
+
+void Ctx::build_plans() {
+  const int sms = device_sm_count();
+  const int m_tiles = max_rows / 128;
+  const int prec = static_cast<int>(opt.precision);
+  const size_t off_wu = static_cast<size_t>(r_pad) * d * 2;
+  const size_t off_bd = off_wu + static_cast<size_t>(d) * r_pad * 2;
+  const size_t off_bu = off_bd + static_cast<size_t>(r_pad) * 4;
+  const uint32_t n_slots = pool->physical_slots();
+  for (int l = 0; l < L; ++l) {
+    LayerDev& w = layers[l];
+    GemmSpec s;
+    s.precision = prec;
+    s.a_rows = max_rows;
+    // QKV
+    s.a = h16.p; s.a_ld = d; s.K = d;
+    s.b = w.wqkv; s.N = 3 * d; s.groups = 1; s.b_ld = d; s.b_group_stride_bytes = size_t(3) * d * d * 2;
+    s.bias = w.bqkv; s.bias_group_stride = 0; s.tile_slot = nullptr;
+    s.res0 = s.res1 = nullptr; s.res_ld = 0;
+    s.c = qkv16.p; s.c_ld = 3 * d; s.epi = 0; s.bn = pick_bn(3 * d, m_tiles, sms);
+    w.qkv = make_gemm_plan(s);
+    // O projection
+    s.a = ctx16.p; s.a_ld = d; s.K = d;
+    s.b = w.wo; s.N = d; s.b_ld = d; s.b_group_stride_bytes = size_t(d) * d * 2;
+    s.bias = w.bo; s.c = a16.p; s.c_ld = d; s.epi = 0; s.bn = pick_bn(d, m_tiles, sms);
+    w.oproj = make_gemm_plan(s);
+    // adapter down (grouped): mid = relu(a . Wd + bd)
+    s.a = a16.p; s.a_ld = d; s.K = d;
+    s.b = arena.p; s.N = r_pad; s.groups = static_cast<int>(n_slots); s.b_ld = d;
+    s.b_group_stride_bytes = slot_bytes;
+    s.bias = reinterpret_cast<const float*>(arena.p + off_bd);
+    s.bias_group_stride = static_cast<long long>(slot_bytes / 4);
+    s.tile_slot = d_tile_slot.p + static_cast<size_t>(l) * tile_stride;
+    s.c = mid16.p; s.c_ld = r_pad; s.epi = kEpiRelu; s.bn = r_pad;
+    w.ad_down = make_gemm_plan(s);
+    // adapter up (grouped) + skip (a) + residual (h): y = mid . Wu + bu + a + h
+    s.a = mid16.p; s.a_ld = r_pad; s.K = r_pad;
+    s.b = arena.p + off_wu; s.N = d; s.b_ld = r_pad;
+    s.bias = reinterpret_cast<const float*>(arena.p + off_bu);
+    s.res0 = a16.p; s.res1 = h16.p; s.res_ld = d;
+    s.c = y32.p; s.c_ld = d; s.epi = kEpiRes2 | kEpiOutF32; s.bn = pick_bn(d, m_tiles, sms);
+    w.ad_up = make_gemm_plan(s);
+    // FFN1: relu(x . W1 + b1)
+    s.a = x16.p; s.a_ld = d; s.K = d;
+    s.b = w.w1; s.N = f; s.groups = 1; s.b_ld = d; s.b_group_stride_bytes = size_t(f) * d * 2;
+    s.bias = w.b1; s.bias_group_stride = 0; s.tile_slot = nullptr;
+    s.res0 = s.res1 = nullptr;
+    s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.bn = pick_bn(f, m_tiles, sms);
+    w.ffn1 = make_gemm_plan(s);
+    // FFN2 + residual: y = ffn . W2 + b2 + x
+    s.a = ffn16.p; s.a_ld = f; s.K = f;
+    s.b = w.w2; s.N = d; s.b_ld = f; s.b_group_stride_bytes = size_t(d) * f * 2;
+    s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
+    s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, m_tiles, sms);
+    w.ffn2 = make_gemm_plan(s);
+  }
+}
+
+void Ctx::upload_plot_hash() {
+  HMI_CUDA(cudaStreamSynchronize(compute));
+  if (d_slots.n != h_slots.size()) d_slots.alloc(h_slots.size());
+  HMI_CUDA(cudaMemcpy(d_slots.p, h_slots.data(), h_slots.size() * sizeof(PlotSlot),
+                      cudaMemcpyHostToDevice));
+  HMI_CUDA(cudaMemcpy(d_parent.p, h_parent.data(), h_parent.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice));
+}
+
+void Ctx::reap(bool all) {
+  while (!inflight.empty()) {
+    Inflight& f = inflight.front();
+    if (all) {
+      HMI_CUDA(cudaEventSynchronize(f.done));
+    } else if (cudaEventQuery(f.done) != cudaSuccess) {
+      break;
+    }
+    pool->unpin(f.tasks);
+    stg[f.staging].busy = false;
+    inflight.pop_front();
+  }
+}
+
+int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_host,
+                const uint32_t* tokens_dev, uint32_t stride, const uint32_t* lens_host,
+                const uint32_t* lens_dev, uint32_t max_len, float* d_scores_out,
+                int32_t* d_labels_out, std::vector<PoolRecord>* records,
+                std::vector<int32_t>* record_layer) {
+  HMI_CHECK(n_req >= 1 && n_req <= opt.max_batch, HMI_DIMENSION_ERROR,
+            "batch size must be in [1, max_batch]");
+  const bool sync_mode = opt.pipeline_mode == 0;
+  const bool fine = opt.pipeline_mode == 2;
+  reap(sync_mode);
+
+  // ---- host routing mirror (InstanceTable) and request validation
+  std::vector<uint32_t> tasks(n_req);
+  for (uint32_t i = 0; i < n_req; ++i) {
+    const uint32_t k = inst[i];
+    if (k >= h_inst_task.size() || h_inst_task[k] < 0) {
+      throw HmiError(HMI_ROUTING_ERROR, "instance " + std::to_string(k) + " is not bound");
+    }
+    tasks[i] = static_cast<uint32_t>(h_inst_task[k]);
+  }
+  if (lens_host) {
+    max_len = 0;
+    for (uint32_t i = 0; i < n_req; ++i) {
+      HMI_CHECK(lens_host[i] >= 1 && lens_host[i] <= stride, HMI_DIMENSION_ERROR,
+                "request length must be in [1, stride]");
+      max_len = std::max(max_len, lens_host[i]);
+      for (uint32_t p = 0; p < lens_host[i]; ++p) {
+        if (tokens_host[static_cast<size_t>(i) * stride + p] >= cfg.vocab_size) {
+          throw HmiError(HMI_VOCABULARY_ERROR, "token id outside vocabulary");
+        }
+      }
+    }
+  }
+  HMI_CHECK(max_len >= 1 && max_len <= static_cast<uint32_t>(S_max), HMI_DIMENSION_ERROR,
+            "request length exceeds max_seq");
+  const int S = static_cast<int>((max_len + 127) / 128 * 128);
+  const int rows = static_cast<int>(n_req) * S;
+  const int tiles_per_req = S / 128;
+
+  // ---- residency decisions (stage_prefetch)
+  std::vector<uint32_t> uniq;
+  {
+    std::set<uint32_t> seen;
+    for (uint32_t t : tasks)
+      if (seen.insert(t).second) uniq.push_back(t);
+  }
+  std::vector<std::vector<std::pair<uint32_t, int32_t>>> loads(L);  // per layer (task, slot)
+  std::vector<int32_t> delta;
+  auto absorb = [&](std::vector<PoolRecord>& recs, int layer_tag) {
+    for (auto& rec : recs) {
+      for (const PoolFree& fr : rec.freed) {
+        delta.push_back(static_cast<int32_t>(fr.task * L + fr.layer));
+        delta.push_back(-1);
+      }
+      for (const PoolLoad& ld : rec.loads) {
+        loads[ld.layer].push_back({rec.task, ld.slot});
+        delta.push_back(static_cast<int32_t>(rec.task * L + ld.layer));
+        delta.push_back(ld.slot);
+      }
+      if (records) {
+        records->push_back(rec);
+        record_layer->push_back(layer_tag);
+      }
+    }
+  };
+  auto absorb_pending = [&]() {
+    for (const PoolFree& fr : pool->take_pending_freed()) {
+      delta.push_back(static_cast<int32_t>(fr.task * L + fr.layer));
+      delta.push_back(-1);
+    }
+  };
+  if (!fine) {
+    for (;;) {
+      try {
+        auto recs = pool->ensure_resident(uniq);
+        absorb(recs, -1);
+        break;
+      } catch (const HmiError& e) {
+        // a pinned in-flight working set blocks the load: retire the oldest batch and retry
+        if (e.code != HMI_CAPACITY_ERROR || inflight.empty()) throw;
+        HMI_CUDA(cudaEventSynchronize(inflight.front().done));
+        reap(false);
+      }
+    }
+  } else {
+    for (int l = 0; l < L; ++l) {
+      for (;;) {
+        auto recs = pool->try_ensure_layer_resident(uniq, static_cast<uint32_t>(l));
+        absorb_pending();
+        if (recs) {
+          absorb(*recs, l);
+          break;
+        }
+        if (inflight.empty()) {
+          throw HmiError(HMI_CAPACITY_ERROR, "pinned working set blocks adapter load");
+        }
+        HMI_CUDA(cudaEventSynchronize(inflight.front().done));
+        reap(false);
+      }
+    }
+  }
+  pool->pin(uniq);
+
+  // ---- staging buffer for this batch
+  const int si = stg_next;
+  stg_next = (stg_next + 1) % kStaging;
+  Staging& st = stg[si];
+  if (st.busy) {
+    while (stg[si].busy) {
+      HMI_CUDA(cudaEventSynchronize(inflight.front().done));
+      reap(false);
+    }
+  }
+  HMI_CHECK(delta.size() / 2 <= d_delta.n / 2, HMI_SCHEDULING_BUG, "slot delta overflow");
+  std::memcpy(st.inst, inst, n_req * sizeof(uint32_t));
+  if (!delta.empty()) std::memcpy(st.delta, delta.data(), delta.size() * sizeof(int32_t));
+  if (tokens_host) {
+    for (uint32_t i = 0; i < n_req; ++i) {
+      std::memcpy(st.tokens + static_cast<size_t>(i) * S, tokens_host + static_cast<size_t>(i) * stride,
+                  std::min<uint32_t>(stride, S) * sizeof(uint32_t));
+      st.lens[i] = static_cast<int32_t>(lens_host[i]);
+    }
+  }
+
+  // ---- copy stream: adapter H2D into HBM slots, one event per layer
+  for (int l = 0; l < L; ++l) {
+    for (const auto& [task, slot] : loads[l]) {
+      HMI_CUDA(cudaMemcpyAsync(arena.p + static_cast<size_t>(slot) * slot_bytes,
+                               store[task] + static_cast<size_t>(l) * slot_bytes, slot_bytes,
+                               cudaMemcpyHostToDevice, copy));
+      bytes_copied += slot_bytes;
+    }
+    HMI_CUDA(cudaEventRecord(ev_layer[l], copy));
+  }
+
+  // ---- compute stream
+  cudaStream_t s = compute;
+  if (sync_mode || !fine) {
+    // sync / coarse: every layer's adapters resident before this batch computes
+    HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[L - 1], 0));
+  }
+  timed(P_H2D, s, [&] {
+    HMI_CUDA(cudaMemcpyAsync(d_inst.p, st.inst, n_req * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    if (tokens_host) {
+      HMI_CUDA(cudaMemcpyAsync(d_tokens.p, st.tokens, static_cast<size_t>(n_req) * S * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, s));
+      HMI_CUDA(cudaMemcpyAsync(d_lens.p, st.lens, n_req * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    } else {
+      HMI_CUDA(cudaMemcpy2DAsync(d_tokens.p, static_cast<size_t>(S) * sizeof(uint32_t), tokens_dev,
+                                 static_cast<size_t>(stride) * sizeof(uint32_t),
+                                 std::min<uint32_t>(stride, S) * sizeof(uint32_t), n_req,
+                                 cudaMemcpyDeviceToDevice, s));
+      HMI_CUDA(cudaMemcpyAsync(d_lens.p, lens_dev, n_req * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    }
+    if (!delta.empty()) {
+      HMI_CUDA(cudaMemcpyAsync(d_delta.p, st.delta, delta.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+    HMI_CUDA(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), s));
+  });
+  timed(P_ROUTE, s, [&] {
+    if (!delta.empty()) launch_apply_deltas(d_slot_of.p, d_delta.p, static_cast<int>(delta.size() / 2), s);
+    launch_route(d_inst.p, static_cast<int>(n_req), d_inst_version.p, d_inst_task.p, d_inst_head.p,
+                 static_cast<int>(h_inst_task.size()), d_slot_of.p, L, tiles_per_req, tile_stride,
+                 d_req_version.p,
+                 d_req_task.p, d_req_head.p, d_tile_slot.p, d_err.p, s);
+  });
+  PlotDev P;
+  P.slots = d_slots.p;
+  P.mask = h_slots.empty() ? 0 : h_slots.size() - 1;
+  P.parent = d_parent.p;
+  P.max_versions = static_cast<int>(h_parent.size());
+  P.reps = d_reps.p;
+  P.ngram = ngram;
+  P.d = d;
+  const int causal = cfg.mode == 1 ? 1 : 0;
+  const int prec = static_cast<int>(opt.precision);
+  timed(P_RETRIEVE, s, [&] {
+    launch_retrieve(P, d_tokens.p, d_lens.p, d_req_version.p, static_cast<int>(n_req), S, causal,
+                    h16.p, prec, (debug_flags & 1) ? h64.p : nullptr, d_gather.p, d_levels.p,
+                    d_err.p, s);
+  });
+  for (int l = 0; l < L; ++l) {
+    LayerDev& w = layers[l];
+    const bool last = l == L - 1;
+    timed(P_QKV, s, [&] { launch_gemm(w.qkv, rows, s); });
+    timed(P_ATTN, s, [&] {
+      launch_attention(qkv16.p, ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal, prec, s);
+    });
+    timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
+    if (fine) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
+    timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
+    timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
+    timed(P_LN1, s, [&] { launch_layernorm(y32.p, w.ln1g, w.ln1b, x16.p, nullptr, rows, d, prec, s); });
+    timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
+    timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
+    timed(P_LN2, s, [&] {
+      launch_layernorm(y32.p, w.ln2g, w.ln2b, h16.p, last ? h32.p : nullptr, rows, d, prec, s);
+    });
+  }
+  HeadDev H;
+  H.arena = d_head_arena.p;
+  H.offset = d_head_off.p;
+  H.labels = d_head_labels.p;
+  H.kind = d_head_kind.p;
+  timed(P_HEAD, s, [&] {
+    launch_head(H, h32.p, d_req_head.p, d_lens.p, static_cast<int>(n_req), S, d,
+                static_cast<int>(opt.max_labels), d_scores_out ? d_scores_out : d_scores.p,
+                d_labels_out ? d_labels_out : d_labels.p, d_tags.p, s);
+  });
+  if (!d_scores_out) {
+    timed(P_D2H, s, [&] {
+      HMI_CUDA(cudaMemcpyAsync(st.scores, d_scores.p, static_cast<size_t>(n_req) * opt.max_labels * sizeof(float),
+                               cudaMemcpyDeviceToHost, s));
+      HMI_CUDA(cudaMemcpyAsync(st.labels, d_labels.p, n_req * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    });
+  }
+  HMI_CUDA(cudaMemcpyAsync(st.err, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  HMI_CUDA(cudaEventRecord(st.done, s));
+  st.busy = true;
+  inflight.push_back(Inflight{st.done, si, uniq});
+  last_n = n_req;
+  last_S = static_cast<uint32_t>(S);
+  return si;
+}
+
+}  // namespace hmi_b200
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using hmi_b200::Ctx;
+using hmi_b200::HmiError;
+
+struct hmi_gpu_ctx {
+  Ctx impl;
+};
+
+namespace {
+
+template <typename F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return HMI_OK;
+  } catch (const HmiError& e) {
+    hmi_b200::set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    hmi_b200::set_last_error(std::string("host allocation failed: ") + e.what());
+    return HMI_CAPACITY_ERROR;
+  } catch (const std::exception& e) {
+    hmi_b200::set_last_error(e.what());
+    return HMI_CUDA_ERROR;
+  }
+}
+
+// ModelConfig::validate (weights.cpp:56-70) plus the device constraints.
+void validate(const hmi_model_config& c, const hmi_gpu_options& o) {
+  if (c.hidden_size == 0 || c.heads == 0 || c.hidden_size % c.heads != 0)
+    throw HmiError(HMI_CONFIG_ERROR, "hidden_size must be a positive multiple of heads");
+  if (c.lower_layers < 1 || c.higher_layers < 1)
+    throw HmiError(HMI_CONFIG_ERROR, "lower_layers and higher_layers must both be >= 1");
+  if (c.ffn_size == 0 || c.vocab_size == 0)
+    throw HmiError(HMI_CONFIG_ERROR, "ffn_size and vocab_size must be positive");
+  if (c.max_fragment != 1 && c.max_fragment != 2 && c.max_fragment != 3 && c.max_fragment != 5)
+    throw HmiError(HMI_CONFIG_ERROR, "max_fragment must be one of {1, 2, 3, 5}");
+  if (c.hidden_size / c.heads != 64)
+    throw HmiError(HMI_CONFIG_ERROR, "device path requires hidden_size / heads == 64");
+  if (c.hidden_size % 128 != 0 || c.ffn_size % 64 != 0)
+    throw HmiError(HMI_CONFIG_ERROR, "device path requires hidden_size % 128 == 0 and ffn % 64 == 0");
+  if (o.bottleneck == 0 || o.bottleneck >= c.hidden_size || o.bottleneck > 256)
+    throw HmiError(HMI_CONFIG_ERROR, "adapter bottleneck must be in [1, min(hidden_size, 257))");
+  if (o.max_batch == 0 || o.max_seq == 0 || o.max_labels == 0)
+    throw HmiError(HMI_CONFIG_ERROR, "max_batch, max_seq and max_labels must be positive");
+  if (o.precision > 1) throw HmiError(HMI_CONFIG_ERROR, "precision must be 0 (fp16) or 1 (bf16)");
+  if (o.pipeline_mode > 2) throw HmiError(HMI_CONFIG_ERROR, "pipeline_mode must be 0, 1 or 2");
+  if (c.vocab_size >= (1u << 31)) throw HmiError(HMI_CONFIG_ERROR, "vocab too large");
+}
+
+}  // namespace
+
+extern "C" {
+
+int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_options* opts,
+                   const float* higher_f32, hmi_gpu_ctx** out) {
+  using namespace hmi_b200;
+  *out = nullptr;
+  auto holder = std::make_unique<hmi_gpu_ctx>();
+  int rc = guarded([&] {
+    HMI_CHECK(cfg && opts && higher_f32, HMI_CONFIG_ERROR, "null argument");
+    validate(*cfg, *opts);
+    Ctx& c = holder->impl;
+    c.device = device;
+    c.cfg = *cfg;
+    c.opt = *opts;
+    if (c.opt.max_tasks == 0) c.opt.max_tasks = 1024;
+    if (c.opt.max_instances == 0) c.opt.max_instances = c.opt.max_tasks;
+    if (c.opt.max_heads == 0) c.opt.max_heads = c.opt.max_tasks;
+    if (c.opt.max_versions == 0) c.opt.max_versions = 64;
+    HMI_CUDA(cudaSetDevice(device));
+    c.d = static_cast<int>(cfg->hidden_size);
+    c.f = static_cast<int>(cfg->ffn_size);
+    c.L = static_cast<int>(cfg->higher_layers);
+    c.heads = static_cast<int>(cfg->heads);
+    c.ngram = static_cast<int>(cfg->max_fragment);
+    c.r = static_cast<int>(opts->bottleneck);
+    c.r_pad = (c.r + 63) / 64 * 64;
+    c.S_max = static_cast<int>((opts->max_seq + 127) / 128 * 128);
+    c.max_rows = static_cast<int>(c.opt.max_batch) * c.S_max;
+    c.tile_stride = c.max_rows / 128;
+    c.slot_bytes = (static_cast<size_t>(c.r_pad) * c.d * 2 * 2 + (c.r_pad + c.d) * 4 + 1023) / 1024 * 1024;
+    c.ref_layer_bytes = (static_cast<uint64_t>(c.d) * c.r * 2 + c.r + c.d) * 4;
+    HMI_CUDA(cudaStreamCreateWithFlags(&c.compute, cudaStreamNonBlocking));
+    HMI_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+    c.ev_layer.resize(c.L);
+    for (auto& e : c.ev_layer) HMI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+    // ---- shared weights: [in x out] f32 -> [out][in] 16-bit, biases / LN f32
+    const size_t d = c.d, f = c.f;
+    const size_t lf = 4 * (d * d + d) + (d * f + f) + (f * d + d) + 4 * d;
+    const int prec = static_cast<int>(c.opt.precision);
+    c.layers.resize(c.L);
+    std::vector<uint16_t> tmp;
+    for (int l = 0; l < c.L; ++l) {
+      const float* w = higher_f32 + l * lf;
+      const float *wq = w, *bq = wq + d * d, *wk = bq + d, *bk = wk + d * d, *wv = bk + d,
+                  *bv = wv + d * d, *wo = bv + d, *bo = wo + d * d, *w1 = bo + d, *b1 = w1 + d * f,
+                  *w2 = b1 + f, *b2 = w2 + f * d, *g1 = b2 + d, *s1 = g1 + d, *g2 = s1 + d,
+                  *s2 = g2 + d;
+      const size_t n16 = 3 * d * d + d * d + f * d + d * f;
+      const size_t n32 = 3 * d + d + f + d + 4 * d;
+      LayerDev& L = c.layers[l];
+      HMI_CUDA(cudaMalloc(&L.mem, n16 * 2 + n32 * 4 + 1024));
+      uint16_t* p16 = static_cast<uint16_t*>(L.mem);
+      L.wqkv = p16; L.wo = L.wqkv + 3 * d * d; L.w1 = L.wo + d * d; L.w2 = L.w1 + f * d;
+      float* p32 = reinterpret_cast<float*>(L.w2 + d * f);
+      L.bqkv = p32; L.bo = L.bqkv + 3 * d; L.b1 = L.bo + d; L.b2 = L.b1 + f;
+      L.ln1g = L.b2 + d; L.ln1b = L.ln1g + d; L.ln2g = L.ln1b + d; L.ln2b = L.ln2g + d;
+      tmp.assign(n16, 0);
+      auto transpose = [&](const float* src, size_t in, size_t outn, uint16_t* dst) {
+        for (size_t o = 0; o < outn; ++o)
+          for (size_t i = 0; i < in; ++i) dst[o * in + i] = f2h(src[i * outn + o], prec);
+      };
+      transpose(wq, d, d, tmp.data());
+      transpose(wk, d, d, tmp.data() + d * d);
+      transpose(wv, d, d, tmp.data() + 2 * d * d);
+      transpose(wo, d, d, tmp.data() + 3 * d * d);
+      transpose(w1, d, f, tmp.data() + 4 * d * d);
+      transpose(w2, f, d, tmp.data() + 4 * d * d + f * d);
+      HMI_CUDA(cudaMemcpy(p16, tmp.data(), n16 * 2, cudaMemcpyHostToDevice));
+      std::vector<float> v32;
+      v32.insert(v32.end(), bq, bq + d);
+      v32.insert(v32.end(), bk, bk + d);
+      v32.insert(v32.end(), bv, bv + d);
+      v32.insert(v32.end(), bo, bo + d);
+      v32.insert(v32.end(), b1, b1 + f);
+      v32.insert(v32.end(), b2, b2 + d);
+      v32.insert(v32.end(), g1, g1 + d);
+      v32.insert(v32.end(), s1, s1 + d);
+      v32.insert(v32.end(), g2, g2 + d);
+      v32.insert(v32.end(), s2, s2 + d);
+      HMI_CUDA(cudaMemcpy(p32, v32.data(), v32.size() * 4, cudaMemcpyHostToDevice));
+    }
+
+    // ---- activations
+    const size_t R = c.max_rows;
+    c.h16.alloc(R * d); c.qkv16.alloc(R * 3 * d); c.ctx16.alloc(R * d); c.a16.alloc(R * d);
+    c.mid16.alloc(R * c.r_pad); c.x16.alloc(R * d); c.ffn16.alloc(R * f);
+    c.y32.alloc(R * d); c.h32.alloc(R * d);
+    const size_t B = c.opt.max_batch;
+    c.d_inst.alloc(B); c.d_tokens.alloc(B * c.S_max); c.d_lens.alloc(B);
+    c.d_req_version.alloc(B); c.d_req_task.alloc(B); c.d_req_head.alloc(B);
+    c.d_tile_slot.alloc(static_cast<size_t>(c.L) * c.tile_stride);
+    HMI_CUDA(cudaMemset(c.d_tile_slot.p, 0, c.d_tile_slot.n * 4));
+    c.d_err.alloc(1);
+    c.d_gather.alloc(R * c.ngram); c.d_levels.alloc(R * c.ngram);
+    c.d_scores.alloc(B * c.opt.max_labels); c.d_labels.alloc(B); c.d_tags.alloc(R);
+    const size_t max_delta = B * c.L * (c.L + 2) + 64;
+    c.d_delta.alloc(2 * max_delta);
+    for (auto& s : c.stg) {
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.inst), B * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.tokens), B * c.S_max * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.lens), B * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.delta), 2 * max_delta * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.scores), B * c.opt.max_labels * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.labels), B * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.tags), R * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.err), 4, 0));
+      HMI_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    }
+
+    // ---- routing tables
+    c.h_inst_version.assign(c.opt.max_instances, -1);
+    c.h_inst_task.assign(c.opt.max_instances, -1);
+    c.h_inst_head.assign(c.opt.max_instances, -1);
+    c.d_inst_version.alloc(c.opt.max_instances);
+    c.d_inst_task.alloc(c.opt.max_instances);
+    c.d_inst_head.alloc(c.opt.max_instances);
+    HMI_CUDA(cudaMemset(c.d_inst_version.p, 0xff, c.opt.max_instances * 4));
+    HMI_CUDA(cudaMemset(c.d_inst_task.p, 0xff, c.opt.max_instances * 4));
+    HMI_CUDA(cudaMemset(c.d_inst_head.p, 0xff, c.opt.max_instances * 4));
+    c.d_slot_of.alloc(static_cast<size_t>(c.opt.max_tasks) * c.L);
+    HMI_CUDA(cudaMemset(c.d_slot_of.p, 0xff, c.d_slot_of.n * 4));
+    c.store.assign(c.opt.max_tasks, nullptr);
+
+    // ---- heads
+    c.h_head_off.assign(c.opt.max_heads, -1);
+    c.h_head_labels.assign(c.opt.max_heads, 0);
+    c.h_head_kind.assign(c.opt.max_heads, -1);
+    c.d_head_off.alloc(c.opt.max_heads);
+    c.d_head_labels.alloc(c.opt.max_heads);
+    c.d_head_kind.alloc(c.opt.max_heads);
+    HMI_CUDA(cudaMemset(c.d_head_off.p, 0, c.opt.max_heads * 8));
+    HMI_CUDA(cudaMemset(c.d_head_labels.p, 0, c.opt.max_heads * 4));
+    HMI_CUDA(cudaMemset(c.d_head_kind.p, 0, c.opt.max_heads * 4));
+
+    // ---- PLOT
+    c.h_parent.assign(c.opt.max_versions, -2);
+    c.d_parent.alloc(c.opt.max_versions);
+    c.h_slots.assign(1024, PlotSlot{kEmptyKey, 0, {0, 0, 0, 0, 0}, 0});
+
+    // ---- adapter slot pool: HBM arena sized by the byte budget
+    uint64_t pool_bytes = c.opt.pool_bytes;
+    if (pool_bytes == 0) pool_bytes = static_cast<uint64_t>(c.opt.max_tasks) * c.L * c.ref_layer_bytes;
+    const uint64_t n_slots64 = pool_bytes / c.ref_layer_bytes;
+    HMI_CHECK(n_slots64 >= 1 && n_slots64 < (1ull << 31), HMI_CONFIG_ERROR,
+              "pool_bytes must hold at least one adapter layer");
+    c.pool = std::make_unique<SlotPool>(pool_bytes, static_cast<uint32_t>(n_slots64));
+    c.arena.alloc(static_cast<size_t>(n_slots64) * c.slot_bytes);
+    HMI_CUDA(cudaMemset(c.arena.p, 0, c.arena.n));
+    c.build_plans();
+    HMI_CUDA(cudaDeviceSynchronize());
+  });
+  if (rc == HMI_OK) *out = holder.release();
+  return rc;
+}
+
+int hmi_gpu_destroy(hmi_gpu_ctx* ctx) {
+  if (!ctx) return HMI_OK;
+  cudaSetDevice(ctx->impl.device);
+  delete ctx;
+  return HMI_OK;
+}
+
+int hmi_gpu_upload_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t parent_id,
+                         uint32_t n_entries, const uint32_t* key_len, const uint32_t* keys,
+                         const float* reps) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    HMI_CHECK(version_id < c.h_parent.size(), HMI_CONFIG_ERROR, "version id exceeds max_versions");
+    if (c.h_parent[version_id] != -2) throw HmiError(HMI_CONFLICT_ERROR, "version already exists");
+    if (parent_id != kNoParent) {
+      if (parent_id >= c.h_parent.size() || c.h_parent[parent_id] == -2)
+        throw HmiError(HMI_ROUTING_ERROR, "branch parent version " + std::to_string(parent_id) +
+                                              " does not exist");
+    } else {
+      for (int32_t p : c.h_parent)
+        if (p == -1) throw HmiError(HMI_CONFLICT_ERROR, "a root table is already registered");
+    }
+    const uint32_t n = static_cast<uint32_t>(c.ngram);
+    uint64_t rows = 0;
+    for (uint32_t e = 0; e < n_entries; ++e) {
+      if (key_len[e] == 0 || key_len[e] > n)
+        throw HmiError(HMI_FORMAT_ERROR, "entry key length outside [1, n]");
+      for (uint32_t j = 0; j < key_len[e]; ++j)
+        if (keys[static_cast<size_t>(e) * n + j] >= c.cfg.vocab_size)
+          throw HmiError(HMI_VOCABULARY_ERROR, "key token outside vocabulary");
+      rows += key_len[e];
+    }
+    // grow the hash to keep load <= 0.5, then insert
+    uint64_t need = c.n_keys + n_entries;
+    if (need * 2 > c.h_slots.size()) {
+      uint64_t cap = c.h_slots.size();
+      while (need * 2 > cap) cap <<= 1;
+      std::vector<PlotSlot> old;
+      old.swap(c.h_slots);
+      c.h_slots.assign(cap, PlotSlot{kEmptyKey, 0, {0, 0, 0, 0, 0}, 0});
+      for (const PlotSlot& s : old) {
+        if (s.version == kEmptyKey) continue;
+        uint64_t i = plot_hash(s.version, s.len, s.tok) & (cap - 1);
+        while (c.h_slots[i].version != kEmptyKey) i = (i + 1) & (cap - 1);
+        c.h_slots[i] = s;
+      }
+    }
+    std::vector<PlotSlot> staged(c.h_slots);  // insert into a copy: fail-closed on duplicates
+    const uint64_t mask = staged.size() - 1;
+    uint64_t row = c.rep_rows;
+    for (uint32_t e = 0; e < n_entries; ++e) {
+      PlotSlot s{version_id, key_len[e], {0, 0, 0, 0, 0}, static_cast<uint32_t>(row)};
+      for (uint32_t j = 0; j < key_len[e]; ++j) s.tok[j] = keys[static_cast<size_t>(e) * n + j];
+      uint64_t i = plot_hash(s.version, s.len, s.tok) & mask;
+      for (;; i = (i + 1) & mask) {
+        const PlotSlot& o = staged[i];
+        if (o.version == kEmptyKey) break;
+        if (o.version == s.version && o.len == s.len &&
+            std::memcmp(o.tok, s.tok, sizeof(uint32_t) * s.len) == 0)
+          throw HmiError(HMI_FORMAT_ERROR, "duplicate entry key");
+      }
+      staged[i] = s;
+      row += key_len[e];
+    }
+    HMI_CHECK(row < (1ull << 31), HMI_CAPACITY_ERROR, "PLOT row count exceeds 2^31");
+    // reps arena (append, growing geometrically)
+    const size_t need_f = static_cast<size_t>(row) * c.d;
+    if (need_f > c.d_reps.n) {
+      DevBuf<float> grown;
+      grown.alloc(std::max(need_f, c.d_reps.n * 3 / 2 + 1));
+      if (c.rep_rows) HMI_CUDA(cudaMemcpy(grown.p, c.d_reps.p, c.rep_rows * c.d * 4, cudaMemcpyDeviceToDevice));
+      c.d_reps.free();
+      c.d_reps = grown;
+      grown.p = nullptr;
+    }
+    if (rows)
+      HMI_CUDA(cudaMemcpy(c.d_reps.p + c.rep_rows * c.d, reps, rows * c.d * 4, cudaMemcpyHostToDevice));
+    c.h_slots.swap(staged);
+    c.n_keys += n_entries;
+    c.rep_rows = row;
+    c.h_parent[version_id] = parent_id == kNoParent ? -1 : static_cast<int32_t>(parent_id);
+    c.upload_plot_hash();
+  });
+}
+
+int hmi_gpu_register_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapter_f32) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CHECK(task_idx < c.store.size(), HMI_CONFIG_ERROR, "task index exceeds max_tasks");
+    if (c.store[task_idx]) throw HmiError(HMI_CONFLICT_ERROR, "adapter set for task already registered");
+    uint8_t* p = c.store_alloc();
+    c.convert_adapter(adapter_f32, p);
+    c.store[task_idx] = p;
+    c.pool->set_task(task_idx, static_cast<uint32_t>(c.L), c.ref_layer_bytes);
+  });
+}
+
+static void evict_task_slots(Ctx& c, uint32_t task, bool remove) {
+  using namespace hmi_b200;
+  std::vector<PoolFree> freed;
+  if (remove) {
+    c.pool->remove_task(task, &freed);
+  } else {
+    c.pool->evict(task, &freed);
+  }
+  for (const PoolFree& fr : freed) {
+    const int32_t minus1 = -1;
+    HMI_CUDA(cudaMemcpy(c.d_slot_of.p + static_cast<size_t>(fr.task) * c.L + fr.layer, &minus1, 4,
+                        cudaMemcpyHostToDevice));
+  }
+}
+
+int hmi_gpu_replace_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapter_f32) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    if (task_idx >= c.store.size() || !c.store[task_idx])
+      throw HmiError(HMI_ROUTING_ERROR, "no adapter set registered for task");
+    c.convert_adapter(adapter_f32, c.store[task_idx]);
+    evict_task_slots(c, task_idx, false);
+  });
+}
+
+int hmi_gpu_unregister_task(hmi_gpu_ctx* ctx, uint32_t task_idx) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    if (task_idx >= c.store.size() || !c.store[task_idx]) return;  // AdapterStore::erase is a no-op
+    evict_task_slots(c, task_idx, true);
+    c.free_blocks.push_back(c.store[task_idx]);
+    c.store[task_idx] = nullptr;
+  });
+}
+
+int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, uint32_t labels,
+                          const float* w, const float* b) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    HMI_CHECK(head_idx < c.h_head_off.size(), HMI_CONFIG_ERROR, "head index exceeds max_heads");
+    HMI_CHECK(kind <= 2, HMI_CONFIG_ERROR, "head kind must be 0, 1 or 2");
+    HMI_CHECK(labels >= 1, HMI_CONFIG_ERROR, "output head needs at least one label");
+    HMI_CHECK(labels <= c.opt.max_labels, HMI_CONFIG_ERROR, "head labels exceed max_labels");
+    if (c.h_head_kind[head_idx] >= 0) throw HmiError(HMI_CONFLICT_ERROR, "head already registered");
+    const size_t n = static_cast<size_t>(c.d) * labels + labels;
+    if (c.head_floats + n > c.d_head_arena.n) {
+      DevBuf<float> grown;
+      grown.alloc(std::max(c.head_floats + n, c.d_head_arena.n * 3 / 2 + 1024));
+      if (c.head_floats)
+        HMI_CUDA(cudaMemcpy(grown.p, c.d_head_arena.p, c.head_floats * 4, cudaMemcpyDeviceToDevice));
+      c.d_head_arena.free();
+      c.d_head_arena = grown;
+      grown.p = nullptr;
+    }
+    HMI_CUDA(cudaMemcpy(c.d_head_arena.p + c.head_floats, w, static_cast<size_t>(c.d) * labels * 4,
+                        cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(c.d_head_arena.p + c.head_floats + static_cast<size_t>(c.d) * labels, b,
+                        labels * 4, cudaMemcpyHostToDevice));
+    c.h_head_off[head_idx] = static_cast<int64_t>(c.head_floats);
+    c.h_head_labels[head_idx] = static_cast<int32_t>(labels);
+    c.h_head_kind[head_idx] = static_cast<int32_t>(kind);
+    c.head_floats += n;
+    HMI_CUDA(cudaMemcpy(c.d_head_off.p + head_idx, &c.h_head_off[head_idx], 8, cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(c.d_head_labels.p + head_idx, &c.h_head_labels[head_idx], 4, cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(c.d_head_kind.p + head_idx, &c.h_head_kind[head_idx], 4, cudaMemcpyHostToDevice));
+  });
+}
+
+int hmi_gpu_bind_instance(hmi_gpu_ctx* ctx, uint32_t instance_idx, uint32_t version_id,
+                          uint32_t task_idx, uint32_t head_idx) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    HMI_CHECK(instance_idx < c.h_inst_task.size(), HMI_CONFIG_ERROR, "instance index exceeds max_instances");
+    if (c.h_inst_task[instance_idx] >= 0) throw HmiError(HMI_CONFLICT_ERROR, "instance already bound");
+    if (version_id >= c.h_parent.size() || c.h_parent[version_id] == -2)
+      throw HmiError(HMI_ROUTING_ERROR, "version " + std::to_string(version_id) + " does not exist");
+    if (task_idx >= c.store.size() || !c.store[task_idx])
+      throw HmiError(HMI_ROUTING_ERROR, "no adapter set registered for task");
+    if (head_idx >= c.h_head_kind.size() || c.h_head_kind[head_idx] < 0)
+      throw HmiError(HMI_ROUTING_ERROR, "no output head registered");
+    c.h_inst_version[instance_idx] = static_cast<int32_t>(version_id);
+    c.h_inst_task[instance_idx] = static_cast<int32_t>(task_idx);
+    c.h_inst_head[instance_idx] = static_cast<int32_t>(head_idx);
+    HMI_CUDA(cudaMemcpy(c.d_inst_version.p + instance_idx, &c.h_inst_version[instance_idx], 4, cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(c.d_inst_task.p + instance_idx, &c.h_inst_task[instance_idx], 4, cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(c.d_inst_head.p + instance_idx, &c.h_inst_head[instance_idx], 4, cudaMemcpyHostToDevice));
+  });
+}
+
+int hmi_gpu_unbind_instance(hmi_gpu_ctx* ctx, uint32_t instance_idx) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    if (instance_idx >= c.h_inst_task.size()) return;
+    c.h_inst_version[instance_idx] = c.h_inst_task[instance_idx] = c.h_inst_head[instance_idx] = -1;
+    const int32_t m1 = -1;
+    HMI_CUDA(cudaMemcpy(c.d_inst_version.p + instance_idx, &m1, 4, cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(c.d_inst_task.p + instance_idx, &m1, 4, cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(c.d_inst_head.p + instance_idx, &m1, 4, cudaMemcpyHostToDevice));
+  });
+}
+
+static void fill_trace(const std::vector<hmi_b200::PoolRecord>& recs, const std::vector<int32_t>& layer_tag,
+                       hmi_load_record* trace, uint32_t trace_cap, uint32_t* evicted,
+                       uint32_t evicted_cap, uint32_t* n_trace) {
+  uint32_t ev = 0;
+  for (size_t i = 0; i < recs.size() && i < trace_cap; ++i) {
+    hmi_load_record& t = trace[i];
+    t.task = recs[i].task;
+    t.layer = layer_tag[i];
+    t.hit = recs[i].hit ? 1 : 0;
+    t.bytes = recs[i].bytes;
+    t.n_evicted = static_cast<uint32_t>(recs[i].evicted.size());
+    t.evicted_offset = ev;
+    t.pad = 0;
+    for (uint32_t e : recs[i].evicted) {
+      if (evicted && ev < evicted_cap) evicted[ev] = e;
+      ++ev;
+    }
+  }
+  if (n_trace) *n_trace = static_cast<uint32_t>(recs.size());
+}
+
+int hmi_gpu_infer_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                        const uint32_t* tokens, uint32_t stride, const uint32_t* lens,
+                        float* scores, int32_t* labels, int32_t* tags, hmi_load_record* trace,
+                        uint32_t trace_cap, uint32_t* evicted, uint32_t evicted_cap,
+                        uint32_t* n_trace) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    std::vector<PoolRecord> recs;
+    std::vector<int32_t> tag;
+    const bool want = trace || n_trace;
+    const int si = c.submit(n_req, instance_idx, tokens, nullptr, stride, lens, nullptr, 0, nullptr,
+                            nullptr, want ? &recs : nullptr, want ? &tag : nullptr);
+    Staging& st = c.stg[si];
+    HMI_CUDA(cudaEventSynchronize(st.done));
+    if (tags) {
+      HMI_CUDA(cudaMemcpy(st.tags, c.d_tags.p, static_cast<size_t>(n_req) * c.last_S * 4, cudaMemcpyDeviceToHost));
+      for (uint32_t i = 0; i < n_req; ++i) {
+        for (uint32_t p = 0; p < stride; ++p)
+          tags[static_cast<size_t>(i) * stride + p] = p < lens[i] ? st.tags[static_cast<size_t>(i) * c.last_S + p] : -1;
+      }
+    }
+    const int err = *st.err;
+    std::memcpy(scores, st.scores, static_cast<size_t>(n_req) * c.opt.max_labels * 4);
+    std::memcpy(labels, st.labels, n_req * 4);
+    if (c.prof) c.prof_collect();
+    c.reap(false);
+    if (want) fill_trace(recs, tag, trace, trace_cap, evicted, evicted_cap, n_trace);
+    if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
+  });
+}
+
+int hmi_gpu_infer_batch_device(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                               const uint32_t* d_tokens, uint32_t stride,
+                               const uint32_t* d_lens, uint32_t max_len, float* d_scores,
+                               int32_t* d_labels) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.submit(n_req, instance_idx, nullptr, d_tokens, stride, nullptr, d_lens, max_len, d_scores,
+             d_labels, nullptr, nullptr);
+  });
+}
+
+int hmi_gpu_synchronize(hmi_gpu_ctx* ctx) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    int err = 0;
+    for (auto& f : c.inflight) {
+      HMI_CUDA(cudaEventSynchronize(f.done));
+      if (!err) err = *c.stg[f.staging].err;
+    }
+    c.reap(true);
+    HMI_CUDA(cudaStreamSynchronize(c.compute));
+    if (c.prof) c.prof_collect();
+    if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
+  });
+}
+
+void* hmi_gpu_stream(hmi_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->impl.compute) : nullptr; }
+
+int hmi_gpu_debug_routing(hmi_gpu_ctx* ctx, int32_t* version, int32_t* task, int32_t* head,
+                          int32_t* slots) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    HMI_CUDA(cudaStreamSynchronize(c.compute));
+    const uint32_t n = c.last_n;
+    if (version) HMI_CUDA(cudaMemcpy(version, c.d_req_version.p, n * 4, cudaMemcpyDeviceToHost));
+    if (task) HMI_CUDA(cudaMemcpy(task, c.d_req_task.p, n * 4, cudaMemcpyDeviceToHost));
+    if (head) HMI_CUDA(cudaMemcpy(head, c.d_req_head.p, n * 4, cudaMemcpyDeviceToHost));
+    if (slots) {
+      const uint32_t tpr = c.last_S / 128;
+      std::vector<int32_t> t(static_cast<size_t>(c.L) * c.tile_stride);
+      HMI_CUDA(cudaMemcpy(t.data(), c.d_tile_slot.p, t.size() * 4, cudaMemcpyDeviceToHost));
+      for (int l = 0; l < c.L; ++l)
+        for (uint32_t i = 0; i < n; ++i) slots[static_cast<size_t>(l) * n + i] = t[static_cast<size_t>(l) * c.tile_stride + i * tpr];
+    }
+  });
+}
+
+int hmi_gpu_debug_gather(hmi_gpu_ctx* ctx, int32_t* rows, int32_t* levels, uint32_t* S) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    HMI_CUDA(cudaStreamSynchronize(c.compute));
+    const size_t n = static_cast<size_t>(c.last_n) * c.last_S * c.ngram;
+    if (rows) HMI_CUDA(cudaMemcpy(rows, c.d_gather.p, n * 4, cudaMemcpyDeviceToHost));
+    if (levels) HMI_CUDA(cudaMemcpy(levels, c.d_levels.p, n * 4, cudaMemcpyDeviceToHost));
+    if (S) *S = c.last_S;
+  });
+}
+
+int hmi_gpu_set_debug(hmi_gpu_ctx* ctx, uint32_t flags) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.debug_flags = flags;
+    if ((flags & 1) && !c.h64.p) c.h64.alloc(static_cast<size_t>(c.max_rows) * c.d);
+  });
+}
+
+int hmi_gpu_debug_h0(hmi_gpu_ctx* ctx, double* out) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CHECK(c.h64.p, HMI_CONFIG_ERROR, "enable debug flag 1 before the batch");
+    HMI_CUDA(cudaStreamSynchronize(c.compute));
+    HMI_CUDA(cudaMemcpy(out, c.h64.p, static_cast<size_t>(c.last_n) * c.last_S * c.d * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int hmi_gpu_debug_hidden(hmi_gpu_ctx* ctx, float* out) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaStreamSynchronize(c.compute));
+    HMI_CUDA(cudaMemcpy(out, c.h32.p, static_cast<size_t>(c.last_n) * c.last_S * c.d * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int hmi_gpu_pool_stats(hmi_gpu_ctx* ctx, uint64_t* out) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    out[0] = c.pool->hits();
+    out[1] = c.pool->loads();
+    out[2] = c.pool->resident_bytes();
+    out[3] = c.pool->max_resident_bytes_seen();
+    out[4] = c.pool->resident_task_count();
+    out[5] = c.pool->capacity_bytes();
+    out[6] = c.pool->physical_slots();
+    out[7] = c.bytes_copied;
+  });
+}
+
+int hmi_gpu_pool_slot(hmi_gpu_ctx* ctx, uint32_t task_idx, uint32_t layer, int32_t* slot) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    *slot = c.pool->slot_of(task_idx, layer);
+  });
+}
+
+int hmi_gpu_profile(hmi_gpu_ctx* ctx, int enable) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.prof_collect();
+    c.prof = enable != 0;
+    for (int i = 0; i < HMI_PROF_CLASSES; ++i) {
+      c.prof_ms[i] = 0;
+      c.prof_cnt[i] = 0;
+    }
+  });
+}
+
+int hmi_gpu_profile_read(hmi_gpu_ctx* ctx, double* ms, uint64_t* count) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.prof_collect();
+    for (int i = 0; i < HMI_PROF_CLASSES; ++i) {
+      if (ms) ms[i] = c.prof_ms[i];
+      if (count) count[i] = c.prof_cnt[i];
+    }
+  });
+}
+
+const char* hmi_gpu_profile_name(int cls) {
+  return cls >= 0 && cls < HMI_PROF_CLASSES ? hmi_b200::kProfNames[cls] : "";
+}
+
+// ---- standalone pool ---------------------------------------------------------
+struct hmi_pool {
+  std::unique_ptr<hmi_b200::SlotPool> p;
+};
+
+int hmi_pool_create(uint64_t capacity_bytes, hmi_pool** out) {
+  return guarded([&] {
+    auto* h = new hmi_pool;
+    h->p = std::make_unique<hmi_b200::SlotPool>(capacity_bytes, 0);
+    *out = h;
+  });
+}
+
+int hmi_pool_destroy(hmi_pool* pool) {
+  delete pool;
+  return HMI_OK;
+}
+
+int hmi_pool_register(hmi_pool* pool, uint32_t task, uint32_t layers, uint64_t layer_bytes) {
+  return guarded([&] {
+    if (pool->p->has_task(task)) throw HmiError(HMI_CONFLICT_ERROR, "task already registered");
+    pool->p->set_task(task, layers, layer_bytes);
+  });
+}
+
+int hmi_pool_op(hmi_pool* pool, int op, uint32_t n, const uint32_t* tasks, uint32_t layer,
+                hmi_load_record* trace, uint32_t trace_cap, uint32_t* evicted,
+                uint32_t evicted_cap, int32_t* n_trace) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    std::vector<uint32_t> v(tasks, tasks + n);
+    std::vector<PoolRecord> recs;
+    if (n_trace) *n_trace = 0;
+    switch (op) {
+      case 0: recs = pool->p->ensure_resident(v); break;
+      case 1: {
+        auto r = pool->p->try_ensure_layer_resident(v, layer);
+        pool->p->take_pending_freed();
+        if (!r) {
+          if (n_trace) *n_trace = -1;
+          return;
+        }
+        recs = std::move(*r);
+        break;
+      }
+      case 2: pool->p->pin(v); return;
+      case 3: pool->p->unpin(v); return;
+      case 4: pool->p->touch(v); return;
+      case 5:
+        if (n_trace) *n_trace = pool->p->evict(v.at(0), nullptr) ? 1 : 0;
+        return;
+      default: throw HmiError(HMI_CONFIG_ERROR, "unknown pool op");
+    }
+    std::vector<int32_t> tag(recs.size(), op == 1 ? static_cast<int32_t>(layer) : -1);
+    uint32_t cnt = 0;
+    fill_trace(recs, tag, trace, trace_cap, evicted, evicted_cap, &cnt);
+    if (n_trace) *n_trace = static_cast<int32_t>(cnt);
+  });
+}
+
+int hmi_pool_stats(hmi_pool* pool, uint64_t* out) {
+  return guarded([&] {
+    out[0] = pool->p->hits();
+    out[1] = pool->p->loads();
+    out[2] = pool->p->resident_bytes();
+    out[3] = pool->p->max_resident_bytes_seen();
+    out[4] = pool->p->resident_task_count();
+    out[5] = pool->p->capacity_bytes();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// SPDX-License-Identifier: Apache-2.0
+// Launchers of the non-GEMM hot-path kernels (K3-K7).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "host_util.hpp"
+
+namespace hmi_b200 {
+
+constexpr uint32_t kNoParent = 0xffffffffu;
+constexpr int kMaxNgram = 5;
+constexpr uint32_t kEmptyKey = 0xffffffffu;
+
+// One open-addressing slot of the device PLOT hash (32 B):
+//   {version, key_len, t0..t4, row_base}; version == kEmptyKey marks an empty slot.
+struct PlotSlot {
+  uint32_t version, len, tok[kMaxNgram], row_base;
+};
+
+__host__ __device__ inline uint64_t plot_hash(uint32_t version, uint32_t len, const uint32_t* t) {
+  uint64_t h = 0x9e3779b97f4a7c15ULL ^ (static_cast<uint64_t>(version) << 32 | len);
+  for (uint32_t i = 0; i < len; ++i) {
+    h ^= t[i] + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);
+    h *= 0xbf58476d1ce4e5b9ULL;
+  }
+  h ^= h >> 31;
+  h *= 0x94d049bb133111ebULL;
+  h ^= h >> 29;
+  return h;
+}
+
+struct PlotDev {
+  const PlotSlot* slots = nullptr;
+  uint64_t mask = 0;               // capacity - 1 (power of two)
+  const int32_t* parent = nullptr; // [max_versions], -1 = root / none, -2 = not a version
+  int max_versions = 0;
+  const float* reps = nullptr;     // [rows][d] f32, float32-exact PLOT values
+  int ngram = 3;
+  int d = 0;
+};
+
+// K5: on-device PLOT retrieval (retrieve_sequence, proj/src/plot/retrieval.cpp:82-124).
+void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* lens,
+                     const int* req_version, int n_req, int S, int causal, void* h16,
+                     int precision, double* h64_debug, int32_t* gather, int32_t* levels,
+                     int32_t* err, cudaStream_t stream);
+
+// K6: routing instance -> (version, task, head) and task -> per-layer HBM slot.
+void launch_route(const uint32_t* instance_idx, int n_req, const int32_t* inst_version,
+                  const int32_t* inst_task, const int32_t* inst_head, int n_instances,
+                  const int32_t* slot_of, int layers, int tiles_per_req, int tile_stride,
+                  int32_t* req_version, int32_t* req_task, int32_t* req_head,
+                  int32_t* tile_slot, int32_t* err, cudaStream_t stream);
+
+// K3: attention core.
+void launch_attention(const void* qkv, void* ctx, const int* lens, int n_req, int S, int d,
+                      int heads, int causal, int precision, cudaStream_t stream);
+
+// K4: LayerNorm over f32 rows (the residual sum is produced by the GEMM epilogue).
+void launch_layernorm(const float* y, const float* gamma, const float* beta, void* out16,
+                      float* out32, int rows, int d, int precision, cudaStream_t stream);
+
+// K7: per-request task head + first-max argmax (apply_head, model.cpp:120-171).
+struct HeadDev {
+  const float* arena = nullptr;     // all heads, f32
+  const int64_t* offset = nullptr;  // [heads] float offset of W (d x labels) ; b follows
+  const int32_t* labels = nullptr;  // [heads]
+  const int32_t* kind = nullptr;    // [heads] 0 cls, 1 token_tag, 2 lm
+};
+void launch_head(const HeadDev& heads, const float* h32, const int32_t* req_head,
+                 const int* lens, int n_req, int S, int d, int max_labels, float* scores,
+                 int32_t* labels_out, int32_t* tags, cudaStream_t stream);
+
+}  // namespace hmi_b200

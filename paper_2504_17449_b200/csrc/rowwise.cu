@@ -1,0 +1,436 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// HBM-bound row-wise kernels of the hot path:
+//   K4 LayerNorm            layer_norm (proj/src/tensor/ops.cpp:92-116)
+//   K5 PLOT retrieval       retrieve_sequence / resolve_window / VersionTree::lookup
+//                           (proj/src/plot/retrieval.cpp:23-124, version_tree.cpp:47-79)
+//   K6 routing              InstanceTable (scheduler/request.hpp:30-36) + slot mapping
+//   K7 task head            apply_head / argmax (proj/src/transformer/model.cpp:120-171)
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace hmi_b200 {
+
+namespace {
+
+template <bool kBf16>
+__device__ __forceinline__ uint32_t pack16x2(float a, float b) {
+  if constexpr (kBf16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: one warp per row; d = 128 * V (V float4 per lane).
+// ---------------------------------------------------------------------------
+template <int V, bool kBf16>
+__global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict__ y,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta,
+                                                        uint16_t* __restrict__ out16,
+                                                        float* __restrict__ out32, int rows) {
+  constexpr int d = 128 * V;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float4* src = reinterpret_cast<const float4*>(y + static_cast<long long>(warp) * d);
+  float4 v[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) v[i] = __ldcs(src + lane + 32 * i);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s * (1.0f / d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+    q += (a * a + b * b) + (c * c + e * e);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float inv = 1.0f / sqrtf(q * (1.0f / d) + 1e-5f);
+  const float4* g4 = reinterpret_cast<const float4*>(gamma);
+  const float4* b4 = reinterpret_cast<const float4*>(beta);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c4 = lane + 32 * i;
+    const float4 g = __ldg(g4 + c4), b = __ldg(b4 + c4);
+    float4 r;
+    r.x = (v[i].x - mean) * inv * g.x + b.x;
+    r.y = (v[i].y - mean) * inv * g.y + b.y;
+    r.z = (v[i].z - mean) * inv * g.z + b.z;
+    r.w = (v[i].w - mean) * inv * g.w + b.w;
+    uint2 p;
+    p.x = pack16x2<kBf16>(r.x, r.y);
+    p.y = pack16x2<kBf16>(r.z, r.w);
+    reinterpret_cast<uint2*>(out16 + static_cast<long long>(warp) * d)[c4] = p;
+    if (out32) reinterpret_cast<float4*>(out32 + static_cast<long long>(warp) * d)[c4] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: PLOT retrieval, one CTA per request.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t plot_find(const PlotDev& P, uint32_t version,
+                                             const uint32_t* key, uint32_t len) {
+  uint64_t i = plot_hash(version, len, key) & P.mask;
+  for (;;) {
+    const PlotSlot& s = P.slots[i];
+    const uint32_t v = __ldg(&s.version);
+    if (v == kEmptyKey) return -1;
+    if (v == version && __ldg(&s.len) == len) {
+      bool eq = true;
+      for (uint32_t j = 0; j < len; ++j) eq &= (__ldg(&s.tok[j]) == key[j]);
+      if (eq) return static_cast<int32_t>(__ldg(&s.row_base));
+    }
+    i = (i + 1) & P.mask;
+  }
+}
+
+// VersionTree::lookup: the version's own table, then its parent chain to the root.
+__device__ __forceinline__ int32_t plot_lookup(const PlotDev& P, int32_t version,
+                                               const uint32_t* key, uint32_t len) {
+  for (int depth = 0; version >= 0 && depth < 64; ++depth) {
+    const int32_t r = plot_find(P, static_cast<uint32_t>(version), key, len);
+    if (r >= 0) return r;
+    version = __ldg(&P.parent[version]);
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t* __restrict__ tokens,
+                                                       const int* __restrict__ lens,
+                                                       const int* __restrict__ req_version,
+                                                       int S, int causal, void* __restrict__ h16,
+                                                       int bf16, double* __restrict__ h64,
+                                                       int32_t* __restrict__ gather,
+                                                       int32_t* __restrict__ levels,
+                                                       int32_t* __restrict__ err) {
+  extern __shared__ int32_t sm[];
+  const int n = P.ngram;
+  int32_t* wrow = sm;              // [S][n] rep row per (window, offset)
+  int32_t* wlev = sm + S * n;      // [S][n] sub-gram length
+  const int b = blockIdx.x;
+  const int len = lens[b];
+  const int version = req_version[b];
+  const uint32_t* tok = tokens + static_cast<long long>(b) * S;
+  const int hl = (n - 1) / 2, hr = n - 1 - hl;
+
+  // ---- phase 1: resolve every window (resolve_window, retrieval.cpp:23-69)
+  for (int c = threadIdx.x; c < len; c += blockDim.x) {
+    int start, end;
+    if (causal) {
+      start = c + 1 >= n ? c + 1 - n : 0;
+      end = c;
+    } else {
+      start = c >= hl ? c - hl : 0;
+      end = c + hr < len - 1 ? c + hr : len - 1;
+    }
+    const int wl = end - start + 1;
+    uint32_t w[kMaxNgram];
+    for (int j = 0; j < wl; ++j) w[j] = tok[start + j];
+    int32_t memo[kMaxNgram][kMaxNgram + 1];
+    uint32_t done = 0;  // bit (o * 6 + k)
+    for (int p = 0; p < wl; ++p) {
+      int32_t row = -1, lev = 0;
+      for (int k = wl; k >= 1 && row < 0; --k) {
+        const int o_lo = p + 1 >= k ? p + 1 - k : 0;
+        const int o_hi = p < wl - k ? p : wl - k;
+        for (int o = o_lo; o <= o_hi; ++o) {
+          const uint32_t bit = 1u << (o * 6 + k);
+          if (!(done & bit)) {
+            memo[o][k] = plot_lookup(P, version, w + o, static_cast<uint32_t>(k));
+            done |= bit;
+          }
+          if (memo[o][k] >= 0) {
+            row = memo[o][k] + (p - o);
+            lev = k;
+            break;
+          }
+        }
+      }
+      if (row < 0) atomicExch(err, HMI_BUILD_ERROR);  // uni-gram backstop missing
+      wrow[c * n + p] = row;
+      wlev[c * n + p] = lev;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: Eq. 2 aggregation, one warp per position
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int d = P.d;
+  const int V = d / 128;  // float4 per lane
+  for (int p = warp; p < S; p += nwarps) {
+    const long long orow = static_cast<long long>(b) * S + p;
+    int32_t rows[kMaxNgram];
+    int32_t levs[kMaxNgram];
+    int cnt = 0;
+    if (p < len) {
+      if (causal) {
+        const int start = p + 1 >= n ? p + 1 - n : 0;
+        rows[0] = wrow[p * n + (p - start)];
+        levs[0] = wlev[p * n + (p - start)];
+        cnt = 1;
+      } else {
+        const int c_lo = p - hr > 0 ? p - hr : 0;
+        const int c_hi = p + hl < len - 1 ? p + hl : len - 1;
+        for (int c = c_lo; c <= c_hi; ++c) {
+          const int start = c >= hl ? c - hl : 0;
+          rows[cnt] = wrow[c * n + (p - start)];
+          levs[cnt] = wlev[c * n + (p - start)];
+          ++cnt;
+        }
+      }
+    }
+    if (gather && lane < n) {
+      int32_t gr = -1, gl = 0;
+      for (int k = 0; k < cnt; ++k) {
+        if (k == lane) { gr = rows[k]; gl = levs[k]; }
+      }
+      gather[orow * n + lane] = gr;
+      levels[orow * n + lane] = gl;
+    }
+    const double inv = cnt > 0 ? 1.0 / static_cast<double>(cnt) : 0.0;
+    for (int i = 0; i < V; ++i) {
+      const int col = (lane + 32 * i) * 4;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (int k = 0; k < cnt; ++k) {
+        const int32_t r = rows[k] < 0 ? 0 : rows[k];
+        const float4 x = __ldg(reinterpret_cast<const float4*>(P.reps + static_cast<long long>(r) * d + col));
+        a0 = a0 + static_cast<double>(x.x);
+        a1 = a1 + static_cast<double>(x.y);
+        a2 = a2 + static_cast<double>(x.z);
+        a3 = a3 + static_cast<double>(x.w);
+      }
+      a0 *= inv; a1 *= inv; a2 *= inv; a3 *= inv;
+      if (h64) {
+        double* o = h64 + orow * d + col;
+        o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+      }
+      uint2 pk;
+      if (bf16) {
+        __nv_bfloat162 x = __halves2bfloat162(__double2bfloat16(a0), __double2bfloat16(a1));
+        __nv_bfloat162 y = __halves2bfloat162(__double2bfloat16(a2), __double2bfloat16(a3));
+        pk.x = *reinterpret_cast<uint32_t*>(&x);
+        pk.y = *reinterpret_cast<uint32_t*>(&y);
+      } else {
+        __half2 x = __halves2half2(__double2half(a0), __double2half(a1));
+        __half2 y = __halves2half2(__double2half(a2), __double2half(a3));
+        pk.x = *reinterpret_cast<uint32_t*>(&x);
+        pk.y = *reinterpret_cast<uint32_t*>(&y);
+      }
+      *reinterpret_cast<uint2*>(static_cast<uint16_t*>(h16) + orow * d + col) = pk;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: routing
+// ---------------------------------------------------------------------------
+__global__ void route_kernel(const uint32_t* __restrict__ instance_idx, int n_req,
+                             const int32_t* __restrict__ inst_version,
+                             const int32_t* __restrict__ inst_task,
+                             const int32_t* __restrict__ inst_head, int n_instances,
+                             const int32_t* __restrict__ slot_of, int layers, int tiles_per_req,
+                             int tile_stride,
+                             int32_t* __restrict__ req_version, int32_t* __restrict__ req_task,
+                             int32_t* __restrict__ req_head, int32_t* __restrict__ tile_slot,
+                             int32_t* __restrict__ err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req) return;
+  const uint32_t inst = instance_idx[i];
+  int32_t v = -1, t = -1, h = -1;
+  if (inst < static_cast<uint32_t>(n_instances)) {
+    v = inst_version[inst];
+    t = inst_task[inst];
+    h = inst_head[inst];
+  }
+  if (v < 0 || t < 0 || h < 0) {
+    atomicExch(err, HMI_ROUTING_ERROR);
+    v = 0; t = -1; h = 0;
+  }
+  req_version[i] = v;
+  req_task[i] = t;
+  req_head[i] = h;
+  for (int l = 0; l < layers; ++l) {
+    int32_t s = t >= 0 ? slot_of[static_cast<long long>(t) * layers + l] : -1;
+    if (s < 0) {
+      atomicExch(err, HMI_SCHEDULING_BUG);  // compute reached a non-resident adapter
+      s = 0;
+    }
+    for (int k = 0; k < tiles_per_req; ++k) tile_slot[static_cast<long long>(l) * tile_stride + i * tiles_per_req + k] = s;
+  }
+}
+
+// Slot-table maintenance: table[pairs[2k]] = pairs[2k+1], applied in order.
+__global__ void apply_deltas_kernel(int32_t* __restrict__ table, const int32_t* __restrict__ pairs,
+                                    int n) {
+  // order matters only for repeated indices; one thread keeps the host's order
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int k = 0; k < n; ++k) table[pairs[2 * k]] = pairs[2 * k + 1];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7: heads. cls/lm: one CTA per request over the selected row; token_tag: one
+// warp per valid row. f64 accumulation of an f32 row against f32 weights.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) head_kernel(HeadDev H, const float* __restrict__ h32,
+                                                   const int32_t* __restrict__ req_head,
+                                                   const int* __restrict__ lens, int S, int d,
+                                                   int max_labels, float* __restrict__ scores,
+                                                   int32_t* __restrict__ labels_out,
+                                                   int32_t* __restrict__ tags) {
+  extern __shared__ double shd[];
+  const int b = blockIdx.x;
+  const int hid = req_head[b];
+  const int kind = H.kind[hid];
+  const int nl = H.labels[hid];
+  const float* W = H.arena + H.offset[hid];
+  const float* B = W + static_cast<long long>(d) * nl;
+  const int len = lens[b];
+  if (kind == 1) {
+    // token_tag: rows < valid_len, argmax per row
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < len; r += blockDim.x >> 5) {
+      const float* x = h32 + (static_cast<long long>(b) * S + r) * d;
+      double best = -INFINITY;
+      int besti = 0;
+      for (int l0 = 0; l0 < nl; l0 += 32) {
+        const int l = l0 + lane;
+        double acc = 0.0;
+        if (l < nl) {
+          for (int j = 0; j < d; ++j) acc += static_cast<double>(x[j]) * W[static_cast<long long>(j) * nl + l];
+          acc += B[l];
+        }
+        // serial first-max scan over this chunk in label order (model.cpp:122-128)
+        for (int k = 0; k < 32 && l0 + k < nl; ++k) {
+          const double v = __shfl_sync(0xffffffffu, acc, k);
+          if (v > best) { best = v; besti = l0 + k; }
+        }
+      }
+      if (lane == 0) tags[static_cast<long long>(b) * S + r] = besti;
+    }
+    if (threadIdx.x == 0) labels_out[b] = -1;
+    return;
+  }
+  const int row = kind == 0 ? 0 : len - 1;
+  const float* x = h32 + (static_cast<long long>(b) * S + row) * d;
+  double* xs = shd;                       // d
+  double* rv = shd + d;                   // blockDim reduction values
+  int* ri = reinterpret_cast<int*>(rv + blockDim.x);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) xs[j] = x[j];
+  __syncthreads();
+  double best = -INFINITY;
+  int besti = 0x7fffffff;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) acc += xs[j] * static_cast<double>(W[static_cast<long long>(j) * nl + l]);
+    acc += static_cast<double>(B[l]);
+    if (l < max_labels) scores[static_cast<long long>(b) * max_labels + l] = static_cast<float>(acc);
+    if (acc > best) { best = acc; besti = l; }  // labels visited in ascending order
+  }
+  rv[threadIdx.x] = best;
+  ri[threadIdx.x] = besti;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      const double ov = rv[threadIdx.x + off];
+      const int oi = ri[threadIdx.x + off];
+      // first max (model.cpp:122-128): larger value wins, ties go to the lower index
+      if (ov > rv[threadIdx.x] || (ov == rv[threadIdx.x] && oi < ri[threadIdx.x])) {
+        rv[threadIdx.x] = ov;
+        ri[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) labels_out[b] = ri[0] == 0x7fffffff ? 0 : ri[0];
+}
+
+}  // namespace
+
+void launch_layernorm(const float* y, const float* gamma, const float* beta, void* out16,
+                      float* out32, int rows, int d, int precision, cudaStream_t stream) {
+  if (rows <= 0) return;
+  HMI_CHECK(d % 128 == 0 && d <= 2048, HMI_CONFIG_ERROR, "layernorm: d must be a multiple of 128");
+  const int blocks = (rows + 7) / 8;
+  auto* o16 = static_cast<uint16_t*>(out16);
+#define HMI_LN_CASE(VV)                                                                       \
+  case VV:                                                                                    \
+    if (precision == 1)                                                                       \
+      layernorm_kernel<VV, true><<<blocks, 256, 0, stream>>>(y, gamma, beta, o16, out32, rows); \
+    else                                                                                      \
+      layernorm_kernel<VV, false><<<blocks, 256, 0, stream>>>(y, gamma, beta, o16, out32, rows); \
+    break;
+  switch (d / 128) {
+    HMI_LN_CASE(1) HMI_LN_CASE(2) HMI_LN_CASE(3) HMI_LN_CASE(4) HMI_LN_CASE(5) HMI_LN_CASE(6)
+    HMI_LN_CASE(7) HMI_LN_CASE(8) HMI_LN_CASE(9) HMI_LN_CASE(10) HMI_LN_CASE(11)
+    HMI_LN_CASE(12) HMI_LN_CASE(13) HMI_LN_CASE(14) HMI_LN_CASE(15) HMI_LN_CASE(16)
+    default: break;
+  }
+#undef HMI_LN_CASE
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* lens,
+                     const int* req_version, int n_req, int S, int causal, void* h16,
+                     int precision, double* h64_debug, int32_t* gather, int32_t* levels,
+                     int32_t* err, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  HMI_CHECK(plot.d % 128 == 0, HMI_CONFIG_ERROR, "retrieve: d must be a multiple of 128");
+  const size_t smem = static_cast<size_t>(S) * plot.ngram * 2 * sizeof(int32_t);
+  if (smem > 48 * 1024) {
+    HMI_CUDA(cudaFuncSetAttribute(retrieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  }
+  retrieve_kernel<<<n_req, 256, smem, stream>>>(plot, tokens, lens, req_version, S, causal, h16,
+                                                precision, h64_debug, gather, levels, err);
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_route(const uint32_t* instance_idx, int n_req, const int32_t* inst_version,
+                  const int32_t* inst_task, const int32_t* inst_head, int n_instances,
+                  const int32_t* slot_of, int layers, int tiles_per_req, int tile_stride,
+                  int32_t* req_version, int32_t* req_task, int32_t* req_head,
+                  int32_t* tile_slot, int32_t* err, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  route_kernel<<<(n_req + 127) / 128, 128, 0, stream>>>(
+      instance_idx, n_req, inst_version, inst_task, inst_head, n_instances, slot_of, layers,
+      tiles_per_req, tile_stride, req_version, req_task, req_head, tile_slot, err);
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_apply_deltas(int32_t* table, const int32_t* pairs, int n, cudaStream_t stream) {
+  if (n <= 0) return;
+  apply_deltas_kernel<<<1, 32, 0, stream>>>(table, pairs, n);
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_head(const HeadDev& heads, const float* h32, const int32_t* req_head,
+                 const int* lens, int n_req, int S, int d, int max_labels, float* scores,
+                 int32_t* labels_out, int32_t* tags, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  const size_t smem = static_cast<size_t>(d + 256) * sizeof(double) + 256 * sizeof(int);
+  if (smem > 48 * 1024) {
+    HMI_CUDA(cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  }
+  head_kernel<<<n_req, 256, smem, stream>>>(heads, h32, req_head, lens, S, d, max_labels, scores,
+                                            labels_out, tags);
+  HMI_CUDA(cudaGetLastError());
+}
+
+}  // namespace hmi_b200

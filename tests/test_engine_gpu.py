@@ -1,0 +1,170 @@
+# SPDX-License-Identifier: Apache-2.0
+"""End-to-end parity of the CUDA backend against the CPU oracle.
+
+Bar (BASELINE.json north_star): routing and gather indices bit-exact; logits
+within max_i ||d_i||_inf / ||ref_i||_inf <= 2e-2; argmax agreement >= 99.9%.
+The retrieval output h0 is additionally compared bit-exactly in f64.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2504_17449_b200 import engine as E
+from paper_2504_17449_b200._native import RoutingError, VocabularyError
+from tests.world import World, logit_error
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def c1():
+    # C1 tiny hBERT: d=256, 4 heads, 2 PLOT + 2 higher layers, ffn 1024, vocab 1024, r=16
+    return World(oracle.TINY, n_tasks=16, r=16, labels=8, max_batch=32)
+
+
+def test_c1_parity(c1):
+    inst, toks, lens = c1.requests(7, 32, 128, min_len=1)
+    lens[:4] = [1, 2, 3, 128]
+    c1.eng.set_debug(1)
+    res = c1.eng.infer_batch(inst, toks, lens)
+    ref_scores, ref_labels, _ = c1.oracle_batch(inst, toks, lens)
+    err = logit_error(res.scores, ref_scores)
+    agree = float((res.labels == ref_labels).mean())
+    print(f"C1 logit err {err:.3e}, argmax agreement {agree:.4f}")
+    assert err <= TOL
+    assert agree >= 0.999
+
+    # routing, bit-exact
+    v, t, h, slots = c1.eng.debug_routing(len(inst))
+    assert np.array_equal(v, c1.inst_version[inst])
+    assert np.array_equal(t, inst) and np.array_equal(h, inst)
+    for l in range(c1.cfg.higher_layers):
+        for i, task in enumerate(inst):
+            assert slots[l, i] == c1.eng.pool_slot(int(task), l) >= 0
+
+    # gather indices and levels, bit-exact; h0 bit-exact in f64
+    rows, lev = c1.eng.debug_gather(len(inst))
+    S = rows.shape[1]
+    h0 = c1.eng.debug_h0(len(inst), S)
+    for i in range(len(inst)):
+        n = int(lens[i])
+        out, gather, levels, _ = c1.tree.retrieve(int(c1.inst_version[inst[i]]), toks[i, :n], 0)
+        assert np.array_equal(rows[i, :n], gather.astype(np.int32)), i
+        assert np.array_equal(lev[i, :n], levels.astype(np.int32)), i
+        assert (rows[i, n:] == -1).all() and (lev[i, n:] == 0).all()
+        assert np.array_equal(h0[i, :n].view(np.uint64), out.view(np.uint64)), i
+        assert (h0[i, n:] == 0).all()
+    c1.eng.set_debug(0)
+
+
+def test_c1_modes_identical(c1):
+    """SPEC.md:482 / acceptance #2: results identical across sync/coarse/fine."""
+    inst, toks, lens = c1.requests(11, 24, 96)
+    outs = []
+    for mode in (E.MODE_SYNC, E.MODE_COARSE, E.MODE_FINE):
+        w = World(oracle.TINY, n_tasks=16, r=16, labels=8, max_batch=32, pipeline_mode=mode)
+        outs.append(w.eng.infer_batch(inst, toks, lens))
+        w.eng.close()
+    for o in outs[1:]:
+        assert np.array_equal(o.scores, outs[0].scores)
+        assert np.array_equal(o.labels, outs[0].labels)
+
+
+def test_c1_permutation_and_batch_independence(c1):
+    """Requests are independent: permuting a batch permutes outputs exactly, and a
+    request's result does not depend on the rest of its batch (same padded length)."""
+    inst, toks, lens = c1.requests(13, 20, 128)
+    lens[0] = 128
+    a = c1.eng.infer_batch(inst, toks, lens)
+    perm = np.random.default_rng(0).permutation(20)
+    perm = np.r_[0, perm[perm != 0]]  # keep a full-length request so S is unchanged
+    b = c1.eng.infer_batch(inst[perm], toks[perm], lens[perm])
+    assert np.array_equal(a.scores[perm], b.scores)
+    single = c1.eng.infer_batch(inst[:1], toks[:1], lens[:1])
+    assert np.array_equal(single.scores[0], a.scores[0])
+
+
+def test_c1_swap_small_pool_bit_identical(c1):
+    """A pool holding only 3 tasks forces evictions and reloads every batch; outputs
+    are bit-identical to the all-resident run and the trace obeys the LRU law."""
+    layer_bytes = (256 * 16 * 2 + 16 + 256) * 4
+    w = World(oracle.TINY, n_tasks=16, r=16, labels=8, max_batch=32,
+              pool_bytes=3 * 2 * layer_bytes + 100, pipeline_mode=E.MODE_FINE)
+    inst, toks, lens = c1.requests(17, 3, 64)
+    inst[:] = [0, 5, 9]
+    outs = []
+    for k in range(4):
+        i2 = (inst + 3 * k) % 16
+        r = w.eng.infer_batch(i2, toks, lens, want_trace=True)
+        ref = c1.eng.infer_batch(i2, toks, lens)
+        assert np.array_equal(r.scores, ref.scores)
+        assert any(not t["hit"] for t in r.trace)
+        outs.append(r)
+    st = w.eng.pool_stats()
+    assert st["max_resident_bytes_seen"] <= st["capacity_bytes"]
+    assert st["loads"] > 0
+    w.eng.close()
+
+
+def test_routing_and_vocab_errors(c1):
+    inst, toks, lens = c1.requests(3, 2, 16)
+    bad = inst.copy()
+    bad[1] = 999
+    with pytest.raises(RoutingError):
+        c1.eng.infer_batch(bad, toks, lens)
+    t2 = toks.copy()
+    t2[0, 0] = c1.cfg.vocab_size
+    with pytest.raises(VocabularyError):
+        c1.eng.infer_batch(inst, t2, lens)
+    # the engine is still usable afterwards
+    c1.eng.infer_batch(inst, toks, lens)
+
+
+def test_token_tag_head():
+    w = World(oracle.TINY, n_tasks=4, r=16, labels=5, head_kind=E.HEAD_TAG, max_batch=8)
+    inst, toks, lens = w.requests(5, 6, 40, min_len=3)
+    res = w.eng.infer_batch(inst, toks, lens, want_tags=True)
+    _, _, tags = w.oracle_batch(inst, toks, lens)
+    agree = np.mean([np.mean(res.tags[i, :lens[i]] == tags[i]) for i in range(len(inst))])
+    assert agree >= 0.99
+    assert (res.labels == -1).all()
+    w.eng.close()
+
+
+def test_causal_lm_head():
+    """hGPT-style: causal retrieval + causal attention, lm head on row valid_len-1."""
+    cfg = oracle.Config(256, 4, 2, 2, 1024, 1024, 1, 3, 9)
+    w = World(cfg, n_tasks=6, r=16, labels=64, head_kind=E.HEAD_LM, max_batch=8)
+    inst, toks, lens = w.requests(21, 8, 100, min_len=2)
+    res = w.eng.infer_batch(inst, toks, lens)
+    ref_scores, ref_labels, _ = w.oracle_batch(inst, toks, lens)
+    assert logit_error(res.scores, ref_scores) <= TOL
+    assert (res.labels == ref_labels).mean() >= 0.999
+    w.eng.close()
+
+
+def test_bf16_operands_close():
+    """bf16 operands run through the same kernels (reported alongside fp16)."""
+    w = World(oracle.TINY, n_tasks=4, r=16, labels=8, max_batch=8, precision=1)
+    inst, toks, lens = w.requests(31, 8, 128)
+    res = w.eng.infer_batch(inst, toks, lens)
+    ref_scores, _, _ = w.oracle_batch(inst, toks, lens)
+    assert logit_error(res.scores, ref_scores) <= 0.1
+    w.eng.close()
+
+
+@pytest.mark.parametrize("n_req", [24])
+def test_base_parity(n_req):
+    """C2 shapes (hBERT-base: d=768, 12 heads, 6 higher layers, ffn 3072, r=64, 8 labels)."""
+    w = World(oracle.BASE, n_tasks=12, r=64, labels=8, max_batch=n_req,
+              branches=tuple((0, 60) for _ in range(8)), n_hot=64, n_bi=400, n_tri=400)
+    inst, toks, lens = w.requests(41, n_req, 128, min_len=100)
+    res = w.eng.infer_batch(inst, toks, lens)
+    ref_scores, ref_labels, _ = w.oracle_batch(inst, toks, lens, threads=32)
+    err = logit_error(res.scores, ref_scores)
+    print(f"C2 logit err {err:.3e}, argmax agreement {(res.labels == ref_labels).mean():.4f}")
+    assert err <= TOL
+    assert (res.labels == ref_labels).mean() >= 0.999
+    w.eng.close()

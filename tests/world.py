@@ -1,0 +1,80 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Shared fixture: one seeded multi-tenant "world" loaded into both the GPU
+engine and the CPU oracle (identical weights, tables, adapters, heads)."""
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+import oracle
+from paper_2504_17449_b200 import engine as E
+from tests.synth_tables import make_requests, make_tree
+
+ADAPTER_SEED = 1000       # adapter seed = 1000 + tenant_idx
+HEAD_SEED = 2_000_000     # head seed = 2e6 + tenant_idx
+
+
+class World:
+    def __init__(self, cfg: oracle.Config, n_tasks: int, r: int, labels: int, *,
+                 head_kind: int = 0, branches=((0, 40), (0, 40), (1, 30)), max_batch=32,
+                 max_seq=128, pool_bytes=0, pipeline_mode=E.MODE_FINE, precision=0,
+                 table_seed=1, n_hot=24, n_bi=80, n_tri=60, engine=True):
+        self.cfg, self.r, self.labels, self.head_kind = cfg, r, labels, head_kind
+        self.higher = oracle.generate_higher(cfg)
+        self.tables, self.hot = make_tree(table_seed, cfg.vocab_size, cfg.hidden_size,
+                                          cfg.max_fragment, n_hot=n_hot, n_bi=n_bi,
+                                          n_tri=n_tri, branches=branches)
+        self.tree = oracle.OracleTree(cfg.max_fragment, cfg.hidden_size)
+        for t in self.tables:
+            self.tree.add_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
+        self.adapters = [oracle.generate_adapter(cfg, r, ADAPTER_SEED + t) for t in range(n_tasks)]
+        self.heads = [oracle.generate_head(cfg.hidden_size, labels, HEAD_SEED + t)
+                      for t in range(n_tasks)]
+        self.n_versions = len(self.tables)
+        # instance i -> (version i % n_versions, task i, head i)
+        self.inst_version = np.arange(n_tasks) % self.n_versions
+        self.eng = None
+        if engine:
+            mc = E.model_config(cfg.hidden_size, cfg.heads, cfg.lower_layers, cfg.higher_layers,
+                                cfg.ffn_size, cfg.vocab_size, cfg.mode, cfg.max_fragment,
+                                cfg.seed)
+            self.eng = E.GpuEngine(mc, self.higher, precision=precision, max_batch=max_batch,
+                                   max_seq=max_seq, bottleneck=r, max_labels=labels,
+                                   pipeline_mode=pipeline_mode, pool_bytes=pool_bytes,
+                                   max_tasks=n_tasks, max_versions=max(8, self.n_versions))
+            for t in self.tables:
+                self.eng.upload_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
+            for t in range(n_tasks):
+                self.eng.register_task(t, self.adapters[t])
+                w, b = self.heads[t]
+                self.eng.register_head(t, head_kind, w, b)
+                self.eng.bind_instance(t, int(self.inst_version[t]), t, t)
+
+    def requests(self, seed, n, max_len, min_len=1, p_hot=0.9):
+        toks, lens = make_requests(seed, n, self.hot, self.cfg.vocab_size, max_len,
+                                   min_len=min_len, p_hot=p_hot)
+        inst = np.random.default_rng(seed + 99).integers(0, len(self.adapters), n)
+        return inst.astype(np.uint32), toks, lens
+
+    def oracle_one(self, inst, tokens, length):
+        w, b = self.heads[inst]
+        return oracle.infer_one(self.cfg, self.higher, self.tree, int(self.inst_version[inst]),
+                                tokens[:length], self.adapters[inst], self.r, w, b,
+                                head_kind=self.head_kind)
+
+    def oracle_batch(self, inst, toks, lens, threads=16):
+        with ThreadPoolExecutor(threads) as ex:
+            res = list(ex.map(lambda i: self.oracle_one(int(inst[i]), toks[i], int(lens[i])),
+                              range(len(inst))))
+        scores = np.stack([r[0] for r in res])
+        labels = np.array([r[1] for r in res])
+        tags = [r[2] for r in res]
+        return scores, labels, tags
+
+
+def logit_error(gpu_scores, ref_scores):
+    """max over requests of ||delta||_inf / ||ref||_inf."""
+    L = ref_scores.shape[1]
+    d = np.abs(gpu_scores[:, :L].astype(np.float64) - ref_scores).max(axis=1)
+    return float((d / np.abs(ref_scores).max(axis=1)).max())
