@@ -1,0 +1,435 @@
+# SPDX-License-Identifier: Apache-2.0
+"""bench.py — mixed-tenant hPLM serving throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c2] [--mode fine]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (tenant-sharded, weak scaling)
+    python bench.py --impl reference ...                        (reference CPU path, oracle/_ref)
+
+A step = one mixed-tenant batch (256 requests x 128 tokens per GPU) through the
+whole hot path: on-device routing + PLOT retrieval, 6 shared higher layers with
+the tenant-grouped adapter GEMMs, per-tenant heads. Rank r serves the tenants
+t with t % N == r (own slot pool, replicated shared layers and PLOT tables);
+the data path has no collective — torch.distributed is used only for the
+barrier and the max-over-ranks of the timings.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hBERT-base mixed-tenant req/s at 1/2/4/8 B200; % of bf16 tensor-core peak"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8 or not parts[0].isdigit() or int(parts[0]) != self.gpu:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if _cuda() else "gloo")
+    return world, rank, local
+
+
+def _cuda() -> bool:
+    import torch
+
+    return torch.cuda.is_available()
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if _cuda() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (oracle/_ref = the reference compiled from its sources)
+# ---------------------------------------------------------------------------
+def reference_world(wl, world, tenants):
+    import oracle
+
+    if oracle.ref() is None:
+        return None
+    cfg = oracle.Config(wl.hidden_size, wl.heads, wl.lower_layers, wl.higher_layers, wl.ffn_size,
+                        wl.vocab_size, wl.mode, wl.max_fragment, wl.model_seed)
+    model = oracle.RefModel(cfg)
+    t0 = world.tables[0]
+    tree = oracle.RefTree(wl.max_fragment, wl.hidden_size, t0["key_len"], t0["keys"], t0["reps"])
+    for t in world.tables[1:]:
+        v = tree.add_branch(t["parent"], t["key_len"], t["keys"], t["reps"])
+        assert v == t["version"]
+    tasks = {int(t): oracle.RefTask(cfg, f"task{t}", wl.r, 1000 + int(t), wl.labels,
+                                    2_000_000 + int(t), wl.head_kind) for t in tenants}
+    return model, tree, tasks
+
+
+def run_reference_sample(ref, world, wl, n, seed, threads):
+    import oracle
+
+    model, tree, tasks = ref
+    inst, toks, lens = world.requests(seed, n, tenants=list(tasks.keys()))
+    versions = np.array([world.tenant_version(int(t)) for t in inst], np.uint32)
+    t0 = time.perf_counter()
+    oracle.ref_infer(model, tree, versions, [tasks[int(t)] for t in inst], toks, lens, wl.labels,
+                     threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(wl, world, steps=1, threads=None, sample=None):
+    import oracle
+
+    threads = threads or os.cpu_count() or 1
+    sample = sample or max(4, threads)
+    rng = np.random.default_rng(7)
+    tenants = sorted(set(int(x) for x in rng.integers(0, wl.n_tenants, sample)))
+    ref = reference_world(wl, world, tenants)
+    kind = "reference"
+    if ref is None:
+        return None
+    secs = 0.0
+    for s in range(steps):
+        secs += run_reference_sample(ref, world, wl, sample, 9000 + s, threads)
+    v = steps * sample / secs
+    return {"value": v, "unit": "req/s", "cores": threads, "kind": kind,
+            "sample": f"{steps}x{sample} {wl.name} requests (seq {wl.seq}) through "
+                      f"retrieve_sequence + higher_stack_forward (HMI_KERNELS="
+                      f"{oracle.ref().ref_active_kernels().decode()}), {threads} threads"}
+
+
+def bench_reference(args, wl):
+    world_size, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from paper_2504_17449_b200.workload import World
+
+    world = World(wl)
+    threads = os.cpu_count() or 1
+    sample = max(2, threads)
+    rng = np.random.default_rng(7)
+    tenants = sorted(set(int(x) for x in rng.integers(0, wl.n_tenants, 4 * sample)))
+    ref = reference_world(wl, world, tenants)
+    cfgd = config_dict(wl, args, world_size)
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "reference sources and oracle/_ref both absent"}))
+        return
+    for s in range(args.warmup):
+        run_reference_sample(ref, world, wl, sample, 100 + s, threads)
+    secs = 0.0
+    for s in range(args.steps):
+        secs += run_reference_sample(ref, world, wl, sample, 200 + s, threads)
+    v = args.steps * sample / secs
+    import oracle
+
+    line = {
+        "metric": METRIC, "value": v, "unit": "req/s", "n_gpus": world_size, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": cfgd, "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "req/s", "cores": threads, "kind": "reference",
+                         "sample": f"each step {sample} requests, {threads} host threads, "
+                                   f"HMI_KERNELS={oracle.ref().ref_active_kernels().decode()}"},
+        "e2e": {"value": v, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(wl, args, world_size):
+    return {
+        "workload": f"{args.config.upper()} {wl.name}: {wl.n_tenants} tenants, "
+                    f"{wl.n_domains} domains{' x ' + str(wl.subdomains) + ' sub-domains' if wl.subdomains else ''}, "
+                    f"seq {wl.seq}, batch {wl.batch} per GPU, r={wl.r}, {wl.labels} labels",
+        "model": f"{wl.name} ({wl.lower_layers} PLOT + {wl.higher_layers} higher layers, d={wl.hidden_size})",
+        "global_batch": wl.batch * world_size,
+        "seq_len": wl.seq,
+        "parallelism": f"tenant-sharded x{world_size} (no collectives)",
+        "pipeline": args.mode,
+        "l2": "flushed (256 MiB write) before every timed step",
+    }
+
+
+# ---------------------------------------------------------------------------
+# our CUDA path
+# ---------------------------------------------------------------------------
+def bench_ours(args, wl):
+    import torch
+
+    world_size, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    from paper_2504_17449_b200 import engine as E
+    from paper_2504_17449_b200.workload import World
+
+    world = World(wl)
+    mode = {"sync": E.MODE_SYNC, "coarse": E.MODE_COARSE, "fine": E.MODE_FINE}[args.mode]
+    mc = E.model_config(wl.hidden_size, wl.heads, wl.lower_layers, wl.higher_layers, wl.ffn_size,
+                        wl.vocab_size, wl.mode, wl.max_fragment, wl.model_seed)
+    higher = E.generate_higher(mc)
+    my_tenants = [t for t in range(wl.n_tenants) if t % world_size == rank]
+    ref_layer_bytes = (wl.hidden_size * wl.r * 2 + wl.r + wl.hidden_size) * 4
+    pool_bytes = int(max(wl.batch, wl.pool_fraction * len(my_tenants))) * wl.higher_layers * ref_layer_bytes
+    eng = E.GpuEngine(mc, higher, device=local, precision=args.precision, max_batch=wl.batch,
+                      max_seq=wl.seq, bottleneck=wl.r, max_labels=wl.labels, pipeline_mode=mode,
+                      pool_bytes=pool_bytes, max_tasks=wl.n_tenants,
+                      max_versions=len(world.tables) + 1)
+    for t in world.tables:
+        eng.upload_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
+    for t in my_tenants:
+        eng.register_task(t, E.generate_adapter(mc, wl.r, 1000 + t))
+        w, b = E.generate_head(wl.hidden_size, wl.labels, 2_000_000 + t)
+        eng.register_head(t, wl.head_kind, w, b)
+        eng.bind_instance(t, world.tenant_version(t), t, t)
+
+    K, W = args.steps, args.warmup
+    batches = [world.requests(10_000 * (rank + 1) + s, wl.batch, tenants=my_tenants)
+               for s in range(W + K)]
+    dev = torch.device("cuda", local)
+    d_tok = [torch.from_numpy(b[1].astype(np.int32)).to(dev) for b in batches]
+    d_len = [torch.from_numpy(b[2].astype(np.int32)).to(dev) for b in batches]
+    d_scores = torch.zeros((wl.batch, wl.labels), dtype=torch.float32, device=dev)
+    d_labels = torch.zeros((wl.batch,), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+    torch.cuda.synchronize()
+
+    def run_device(i):
+        inst, _, lens = batches[i]
+        eng.infer_batch_device(inst, d_tok[i].data_ptr(), wl.seq, d_len[i].data_ptr(),
+                               int(lens.max()), d_scores.data_ptr(), d_labels.data_ptr())
+
+    # warm-up: one pass over every tenant of this rank (fills the slot pool up to its
+    # capacity), then W ordinary batches
+    for c in range(0, len(my_tenants), wl.batch):
+        chunk = np.array(my_tenants[c:c + wl.batch], np.uint32)
+        _, toks, lens = world.requests(77 + c, len(chunk), tenants=chunk)
+        eng.infer_batch(chunk, toks, lens)
+    for i in range(W):
+        run_device(i)
+    eng.synchronize()
+    for i in range(W):  # second pass so the pool is warm for the steady state
+        run_device(i)
+    eng.synchronize()
+
+    # ---- timed: inputs resident in HBM, L2 flushed before each step
+    c0 = E.engine_counters(eng)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(world_size)
+    torch.cuda.synchronize()
+    evs = []
+    with torch.cuda.stream(stream):
+        for k in range(K):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run_device(W + k)
+            b.record(stream)
+            evs.append((a, b))
+    eng.synchronize()
+    torch.cuda.synchronize()
+    barrier(world_size)
+    clk = clocks.stop()
+    c1 = E.engine_counters(eng)
+    local_ms = sum(a.elapsed_time(b) for a, b in evs)
+    max_ms = max_over_ranks(local_ms, world_size)
+    value = world_size * wl.batch * K / (max_ms / 1e3)
+
+    # ---- e2e: public host-buffer API, H2D of inputs + D2H of results inside the region
+    barrier(world_size)
+    torch.cuda.synchronize()
+    for i in range(min(W, 2)):
+        inst, toks, lens = batches[i]
+        eng.infer_batch(inst, toks, lens)
+    t0 = time.perf_counter()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for k in range(K):
+        inst, toks, lens = batches[W + k]
+        eng.infer_batch(inst, toks, lens)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max(a.elapsed_time(b), 1e3 * (time.perf_counter() - t0))
+    e2e_ms = max_over_ranks(e2e_ms, world_size)
+    e2e = world_size * wl.batch * K / (e2e_ms / 1e3)
+    h2d = wl.batch * (wl.seq * 4 + 4 + 4)          # tokens + lens + instance ids
+    d2h = wl.batch * (wl.labels * 4 + 4)           # scores + labels
+
+    # ---- per-kernel device time (events around every launch) for the roofline
+    eng.profile(True)
+    for k in range(K):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        run_device(W + k)
+    eng.synchronize()
+    prof = eng.profile_read()
+    eng.profile(False)
+
+    hbm, peak_burst, peak_sust, peak_src = peaks()
+    T = wl.batch * wl.seq
+    d, f, r = wl.hidden_size, wl.ffn_size, wl.r
+    flops = {"gemm_qkv": 2 * T * d * 3 * d, "gemm_oproj": 2 * T * d * d, "gemm_ffn1": 2 * T * d * f,
+             "gemm_ffn2": 2 * T * f * d, "adapter_down": 2 * T * d * r, "adapter_up": 2 * T * r * d}
+    step_ms = sum(v[0] for k, v in prof.items() if k not in ("step",)) / max(K, 1)
+    dom = max(flops, key=lambda k: prof[k][0])
+    ms_dom = prof[dom][0] / max(prof[dom][1], 1)
+    achieved = flops[dom] / (ms_dom * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            traffic = json.load(fh).get("kernels", {}).get(dom, {}).get("dram_bytes")
+    except Exception:
+        pass
+    kernels = {k: {"ms_per_launch": v[0] / max(v[1], 1), "launches": v[1],
+                   "share": v[0] / max(step_ms * K, 1e-9)} for k, v in prof.items() if v[1]}
+    for k in flops:
+        if k in kernels:
+            kernels[k]["tflops"] = flops[k] / (kernels[k]["ms_per_launch"] * 1e-3) / 1e12
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "req/s",
+        "n_gpus": world_size,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": max_ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp16 operands, fp32 accumulate" if args.precision == 0 else "bf16 operands, fp32 accumulate",
+        "data": "synthetic (seeded generate_model / adapters / heads, synthetic PLOT tables)",
+        "config": config_dict(wl, args, world_size),
+        "e2e": {"value": e2e, "unit": "req/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(c1["launches"] - c0["launches"]),
+        "roofline": {
+            "bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak_sust,
+            "unit": "TFLOP/s", "frac": achieved / peak_sust, "traffic": traffic,
+            "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+            "frac_of_burst": achieved / peak_burst,
+            "step_tensor_frac": value / world_size * wl.flops_per_request() / 1e12 / peak_burst,
+            "flops_per_request": wl.flops_per_request(),
+        },
+        "kernels": kernels,
+        "clocks": clk,
+        "pool": eng.pool_stats(),
+    }
+    if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, world)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--mode", default="fine", choices=["sync", "coarse", "fine"])
+    ap.add_argument("--precision", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    from paper_2504_17449_b200.workload import CONFIGS
+
+    wl = CONFIGS[args.config]
+    if args.impl == "reference":
+        bench_reference(args, wl)
+    else:
+        bench_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

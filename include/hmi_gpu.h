@@ -184,6 +184,20 @@ int hmi_gpu_profile(hmi_gpu_ctx* ctx, int enable);
 int hmi_gpu_profile_read(hmi_gpu_ctx* ctx, double* ms, uint64_t* count);
 const char* hmi_gpu_profile_name(int cls);
 
+/* ---- seeded artefact generators (host only) ------------------------------ */
+/* generate_model (weights.cpp:72-88): writes the f32 weights in HMI1 order;
+ * any output pointer may be NULL (its draws are still consumed).              */
+int hmi_generate_model(const hmi_model_config* cfg, float* token_embedding,
+                       float* position_embedding, float* lower, float* higher);
+/* generate_adapter_set (adapter_set.cpp:15-25): higher_layers ADP1 blocks.    */
+int hmi_generate_adapter(const hmi_model_config* cfg, uint32_t bottleneck, uint64_t seed,
+                         float* out);
+/* generate_output_head (weights.cpp:105-118): w [d x labels], b [labels].    */
+int hmi_generate_head(uint32_t hidden_size, uint32_t labels, uint64_t seed, float* w, float* b);
+
+/* Engine counters: out[0] kernel launches, [1] batches, [2] adapter copies. */
+int hmi_gpu_counters(hmi_gpu_ctx* ctx, uint64_t* out);
+
 /* ---- standalone slot-pool policy (host only; trace parity tests) ---------- */
 typedef struct hmi_pool hmi_pool;
 int hmi_pool_create(uint64_t capacity_bytes, hmi_pool** out);

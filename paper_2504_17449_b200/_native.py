@@ -136,6 +136,10 @@ def _sig(L):
     L.hmi_pool_op.argtypes = [vp, ctypes.c_int, u32, u32p, u32, P(LoadRecord), u32, u32p, u32,
                               P(i32)]
     L.hmi_pool_stats.argtypes = [vp, u64p]
+    L.hmi_generate_model.argtypes = [P(ModelConfig), f32p, f32p, f32p, f32p]
+    L.hmi_generate_adapter.argtypes = [P(ModelConfig), u32, u64, f32p]
+    L.hmi_generate_head.argtypes = [u32, u32, u64, f32p, f32p]
+    L.hmi_gpu_counters.argtypes = [vp, u64p]
 
 
 def lib() -> ctypes.CDLL:

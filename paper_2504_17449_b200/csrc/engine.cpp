@@ -179,6 +179,7 @@ struct Ctx {
   uint8_t* chunk_cur = nullptr;
   size_t chunk_left = 0;
   uint64_t bytes_copied = 0;
+  uint64_t n_launches = 0, n_batches = 0, n_copies = 0;
   std::vector<cudaEvent_t> ev_layer;
   // staging / in-flight batches
   Staging stg[kStaging];
@@ -532,6 +533,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
                                store[task] + static_cast<size_t>(l) * slot_bytes, slot_bytes,
                                cudaMemcpyHostToDevice, copy));
       bytes_copied += slot_bytes;
+      ++n_copies;
     }
     HMI_CUDA(cudaEventRecord(ev_layer[l], copy));
   }
@@ -622,6 +624,8 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   st.busy = true;
   inflight.push_back(Inflight{st.done, si, uniq});
   last_n = n_req;
+  n_launches += (delta.empty() ? 0 : 1) + 3 + 9ull * L;
+  ++n_batches;
   last_S = static_cast<uint32_t>(S);
   return si;
 }
@@ -1349,3 +1353,13 @@ int hmi_pool_stats(hmi_pool* pool, uint64_t* out) {
 }
 
 }  // extern "C"
+
+extern "C" int hmi_gpu_counters(hmi_gpu_ctx* ctx, uint64_t* out) {
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    out[0] = c.n_launches;
+    out[1] = c.n_batches;
+    out[2] = c.n_copies;
+  });
+}

@@ -20,18 +20,23 @@ KernelFn kernel_ptr() {
   return reinterpret_cast<KernelFn>(&gemm_tcgen05_kernel<BN, EPI>);
 }
 
-template <int BN>
-KernelFn pick_epi(int epi) {
+template <int BN, int T>
+KernelFn pick_epi_t(int epi) {
   switch (epi) {
-    case 0: return kernel_ptr<BN, 0>();
-    case kEpiRelu: return kernel_ptr<BN, kEpiRelu>();
-    case kEpiRes1: return kernel_ptr<BN, kEpiRes1>();
-    case kEpiRes2: return kernel_ptr<BN, kEpiRes2>();
-    case kEpiOutF32: return kernel_ptr<BN, kEpiOutF32>();
-    case kEpiRes1 | kEpiOutF32: return kernel_ptr<BN, kEpiRes1 | kEpiOutF32>();
-    case kEpiRes2 | kEpiOutF32: return kernel_ptr<BN, kEpiRes2 | kEpiOutF32>();
+    case 0: return kernel_ptr<BN, T>();
+    case kEpiRelu: return kernel_ptr<BN, T | kEpiRelu>();
+    case kEpiRes1: return kernel_ptr<BN, T | kEpiRes1>();
+    case kEpiRes2: return kernel_ptr<BN, T | kEpiRes2>();
+    case kEpiOutF32: return kernel_ptr<BN, T | kEpiOutF32>();
+    case kEpiRes1 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes1 | kEpiOutF32>();
+    case kEpiRes2 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes2 | kEpiOutF32>();
     default: return nullptr;
   }
+}
+
+template <int BN>
+KernelFn pick_epi(int epi) {
+  return (epi & kEpiBf16) ? pick_epi_t<BN, kEpiBf16>(epi & ~kEpiBf16) : pick_epi_t<BN, 0>(epi);
 }
 
 KernelFn pick_kernel(int bn, int epi, int* smem_bytes) {
@@ -53,7 +58,8 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   HMI_CHECK(s.N % s.bn == 0, HMI_CONFIG_ERROR, "gemm: N must be a multiple of the N tile");
   HMI_CHECK(s.a_rows % kBlockM == 0, HMI_CONFIG_ERROR, "gemm: A rows must be a multiple of 128");
   GemmPlan p;
-  p.fn = reinterpret_cast<void*>(pick_kernel(s.bn, s.epi, &p.smem_bytes));
+  const int epi = s.epi | (s.precision == 1 ? kEpiBf16 : 0);
+  p.fn = reinterpret_cast<void*>(pick_kernel(s.bn, epi, &p.smem_bytes));
   HMI_CHECK(p.fn != nullptr, HMI_CONFIG_ERROR, "gemm: unsupported epilogue");
   const CUtensorMapDataType t16 =
       s.precision == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;

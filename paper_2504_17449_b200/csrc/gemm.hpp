@@ -28,6 +28,7 @@ constexpr int kEpiRelu = 1;
 constexpr int kEpiRes1 = 2;  // add res0
 constexpr int kEpiRes2 = 4;  // add res0 + res1
 constexpr int kEpiOutF32 = 8;
+constexpr int kEpiBf16 = 16;  // 16-bit outputs / residuals are bf16 (set from precision)
 
 // Everything needed to bind one GEMM to fixed device buffers.
 struct GemmSpec {

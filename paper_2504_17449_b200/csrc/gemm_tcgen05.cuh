@@ -29,6 +29,38 @@ constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // 64 x 16-bit = 128 B = one SWIZZLE_128B atom row
 
 
+template <bool kBf16>
+__device__ __forceinline__ uint32_t pack_16x2(float a, float b) {
+  if constexpr (kBf16) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+}
+
+// v[0..N) += 16-bit residual row segment (16-byte vector loads)
+template <bool kBf16, int N>
+__device__ __forceinline__ void add_res16(float* v, const uint16_t* src) {
+#pragma unroll
+  for (int i = 0; i < N; i += 8) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src + i));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f;
+      if constexpr (kBf16) {
+        f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      } else {
+        f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+      }
+      v[i + 2 * e] += f.x;
+      v[i + 2 * e + 1] += f.y;
+    }
+  }
+}
+
 template <int BN>
 struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
@@ -53,6 +85,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   static_assert(kStages >= 2, "smem budget too small");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
+  constexpr bool kBf16 = (EPI & kEpiBf16) != 0;  // 16-bit tensors are bf16 (else fp16)
   constexpr int kCW = kOutF32 ? 32 : 64;  // output columns per 128-byte staging row
   static_assert(BN % kCW == 0, "BN must be a multiple of the store chunk");
 
@@ -183,32 +216,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
           if (row_ok) {
-            const int col = nt * BN + c;
-            const __half* r0 = args.res0 + static_cast<long long>(row) * args.res_ld + col;
-#pragma unroll
-            for (int i = 0; i < kCW; i += 8) {
-              const uint4 u = __ldg(reinterpret_cast<const uint4*>(r0 + i));
-              const __half2* h2 = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __half22float2(h2[e]);
-                v[i + 2 * e] += f.x;
-                v[i + 2 * e + 1] += f.y;
-              }
-            }
+            const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
+            add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off);
             if constexpr ((EPI & kEpiRes2) != 0) {
-              const __half* r1 = args.res1 + static_cast<long long>(row) * args.res_ld + col;
-#pragma unroll
-              for (int i = 0; i < kCW; i += 8) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(r1 + i));
-                const __half2* h2 = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f = __half22float2(h2[e]);
-                  v[i + 2 * e] += f.x;
-                  v[i + 2 * e + 1] += f.y;
-                }
-              }
+              add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off);
             }
           }
         }
@@ -223,10 +234,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int i = 0; i < 32; ++i) packed[i] = __float_as_uint(v[i]);
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-            packed[i] = *reinterpret_cast<const uint32_t*>(&h);
-          }
+          for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
         }
         // staging buffer reuse: the store issued two chunks ago must have read it
         if (lane == 0) tma_store_wait_read<1>();

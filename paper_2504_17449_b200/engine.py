@@ -291,3 +291,34 @@ class SlotPoolPolicy:
         keys = ("hits", "loads", "resident_bytes", "max_resident_bytes_seen",
                 "resident_task_count", "capacity_bytes")
         return {k: int(v) for k, v in zip(keys, o)}
+
+
+# ---------------------------------------------------------------------------
+# seeded generators (weights.cpp:72-118, adapter_set.cpp:15-25)
+# ---------------------------------------------------------------------------
+def generate_higher(cfg: ModelConfig) -> np.ndarray:
+    """Higher-stack weights of generate_model(cfg), f32, HMI1 per-layer order."""
+    out = np.empty((cfg.higher_layers, layer_floats(cfg)), np.float32)
+    check(_native.lib().hmi_generate_model(ctypes.byref(cfg), None, None, None,
+                                           _p(out, ctypes.c_float)))
+    return out
+
+
+def generate_adapter(cfg: ModelConfig, r: int, seed: int) -> np.ndarray:
+    out = np.empty((cfg.higher_layers, adapter_layer_floats(cfg, r)), np.float32)
+    check(_native.lib().hmi_generate_adapter(ctypes.byref(cfg), r, seed, _p(out, ctypes.c_float)))
+    return out
+
+
+def generate_head(d: int, labels: int, seed: int):
+    w = np.empty((d, labels), np.float32)
+    b = np.empty((labels,), np.float32)
+    check(_native.lib().hmi_generate_head(d, labels, seed, _p(w, ctypes.c_float),
+                                          _p(b, ctypes.c_float)))
+    return w, b
+
+
+def engine_counters(eng: GpuEngine) -> dict:
+    o = np.zeros(4, np.uint64)
+    check(_native.lib().hmi_gpu_counters(eng.h, _p(o, ctypes.c_uint64)))
+    return {"launches": int(o[0]), "batches": int(o[1]), "adapter_copies": int(o[2])}
