@@ -10,7 +10,7 @@
 //
 // Input : qkv [T x 3d] 16-bit (q | k | v column blocks), request b owns rows [b*S, b*S+S)
 // Output: ctx [T x d] 16-bit
-// dh = 64. One CTA = 4 warps = 64 query rows; K/V streamed through smem in 64-key
+// dh = 64. One CTA = 8 warps = 128 query rows (K/V read once per (request, head)); K/V streamed through smem in 64-key
 // blocks with an online softmax (fp32 statistics), tensor-core mma.sync m16n8k16.
 // Memory bound at hBERT shapes (reads 3 x 16 KB, writes 16 KB per (request, head)).
 #include <cuda_bf16.h>
@@ -25,7 +25,7 @@ namespace hmi_b200 {
 namespace {
 
 constexpr int kDh = 64;
-constexpr int kQB = 64;    // query rows per CTA
+constexpr int kQB = 128;   // query rows per CTA (8 warps x 16)
 constexpr int kKB = 64;    // keys per block
 constexpr int kPad = 72;   // smem row stride in 16-bit elements (144 B: conflict-free ldmatrix)
 
@@ -82,13 +82,14 @@ __device__ __forceinline__ uint32_t pack2(float x, float y) {
 }
 
 template <bool kBf16>
-__global__ void __launch_bounds__(128) attention_kernel(const uint16_t* __restrict__ qkv,
+__global__ void __launch_bounds__(256, 2) attention_kernel(const uint16_t* __restrict__ qkv,
                                                         uint16_t* __restrict__ ctx,
                                                         const int* __restrict__ lens, int S,
                                                         int d, int causal, float scale_log2) {
-  __shared__ __align__(128) uint16_t sQ[kQB * kPad];
-  __shared__ __align__(128) uint16_t sK[2][kKB * kPad];
-  __shared__ __align__(128) uint16_t sV[2][kKB * kPad];
+  extern __shared__ __align__(128) uint16_t att_smem[];
+  uint16_t* sQ = att_smem;                                   // [kQB][kPad]
+  uint16_t* const sK0 = sQ + kQB * kPad;       // [2][kKB][kPad]
+  uint16_t* const sV0 = sK0 + 2 * kKB * kPad;   // [2][kKB][kPad]
 
   const int qb = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -102,23 +103,24 @@ __global__ void __launch_bounds__(128) attention_kernel(const uint16_t* __restri
   // number of key blocks this CTA must visit
   int nkb;
   if (causal) {
-    nkb = qb + 1;
+    nkb = (qb + 1) * (kQB / kKB);
   } else {
     nkb = (valid + kKB - 1) / kKB;
   }
   if (nkb < 1) nkb = 1;
 
-  auto load_tile = [&](uint16_t* dst, const uint16_t* src) {
+  auto load_tile = [&](uint16_t* dst, const uint16_t* src) {  // 64 rows x 128 B
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int c = tid + i * 128;  // 512 chunks of 16 B
+    for (int i = 0; i < 2; ++i) {
+      const int c = tid + i * 256;  // 512 chunks of 16 B
       const int r = c >> 3, cc = c & 7;
       cp_async16(dst + r * kPad + cc * 8, src + static_cast<long long>(r) * ld + cc * 8);
     }
   };
   load_tile(sQ, gq);
-  load_tile(sK[0], gk);
-  load_tile(sV[0], gv);
+  load_tile(sQ + 64 * kPad, gq + 64ll * ld);
+  load_tile(sK0, gk);
+  load_tile(sV0, gv);
   cp_async_commit();
 
   const int g = lane >> 2, tq = lane & 3;
@@ -134,8 +136,8 @@ __global__ void __launch_bounds__(128) attention_kernel(const uint16_t* __restri
 
   for (int kb = 0; kb < nkb; ++kb) {
     if (kb + 1 < nkb) {
-      load_tile(sK[(kb + 1) & 1], gk + static_cast<long long>((kb + 1) * kKB) * ld);
-      load_tile(sV[(kb + 1) & 1], gv + static_cast<long long>((kb + 1) * kKB) * ld);
+      load_tile(sK0 + ((kb + 1) & 1) * kKB * kPad, gk + static_cast<long long>((kb + 1) * kKB) * ld);
+      load_tile(sV0 + ((kb + 1) & 1) * kKB * kPad, gv + static_cast<long long>((kb + 1) * kKB) * ld);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -147,8 +149,8 @@ __global__ void __launch_bounds__(128) attention_kernel(const uint16_t* __restri
       for (int ks = 0; ks < 4; ++ks)
         ldsm_x4(qf[ks], sQ + (warp * 16 + (lane & 15)) * kPad + ks * 16 + (lane >> 4) * 8);
     }
-    const uint16_t* K = sK[kb & 1];
-    const uint16_t* V = sV[kb & 1];
+    const uint16_t* K = sK0 + (kb & 1) * kKB * kPad;
+    const uint16_t* V = sV0 + (kb & 1) * kKB * kPad;
 
     // S = Q K^T : 16 x 64 per warp
     float s[8][4];
@@ -243,16 +245,26 @@ __global__ void __launch_bounds__(128) attention_kernel(const uint16_t* __restri
 void launch_attention(const void* qkv, void* ctx, const int* lens, int n_req, int S, int d,
                       int heads, int causal, int precision, cudaStream_t stream) {
   HMI_CHECK(d == heads * kDh, HMI_CONFIG_ERROR, "attention: head width must be 64");
-  HMI_CHECK(S % kQB == 0, HMI_DIMENSION_ERROR, "attention: padded length must be a multiple of 64");
+  HMI_CHECK(S % kQB == 0, HMI_DIMENSION_ERROR, "attention: padded length must be a multiple of 128");
   if (n_req <= 0) return;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(kDh));
   dim3 grid(S / kQB, heads, n_req);
+  const int smem = (kQB + 4 * kKB) * kPad * 2;
+  static bool configured[2] = {false, false};
+  if (!configured[precision == 1]) {
+    if (precision == 1) {
+      HMI_CUDA(cudaFuncSetAttribute(attention_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    } else {
+      HMI_CUDA(cudaFuncSetAttribute(attention_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    configured[precision == 1] = true;
+  }
   if (precision == 1) {
-    attention_kernel<true><<<grid, 128, 0, stream>>>(static_cast<const uint16_t*>(qkv),
+    attention_kernel<true><<<grid, 256, smem, stream>>>(static_cast<const uint16_t*>(qkv),
                                                      static_cast<uint16_t*>(ctx), lens, S, d,
                                                      causal, scale_log2);
   } else {
-    attention_kernel<false><<<grid, 128, 0, stream>>>(static_cast<const uint16_t*>(qkv),
+    attention_kernel<false><<<grid, 256, smem, stream>>>(static_cast<const uint16_t*>(qkv),
                                                       static_cast<uint16_t*>(ctx), lens, S, d,
                                                       causal, scale_log2);
   }

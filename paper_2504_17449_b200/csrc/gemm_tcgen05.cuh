@@ -13,10 +13,10 @@
 //     mode: every 128-row M tile belongs to exactly one request, and the B tile is
 //     gathered from that request's HBM slot (tile_slot[m_tile] selects the group).
 //
-// Roles (192 threads, 1 CTA per SM):
+// Roles (320 threads, 1 CTA per SM):
 //   warp 0      : TMA producer (one elected lane)      smem ring of kStages (A,B) tiles
 //   warp 1      : TMEM allocator + MMA issuer (lane 0)  2 TMEM accumulators of BN fp32 cols
-//   warps 2..5  : epilogue, TMEM -> regs -> bias/ReLU/residual -> 16/32-bit -> smem -> TMA store
+//   warps 2..9  : epilogue, TMEM -> regs -> bias/ReLU/residual -> 16/32-bit -> smem -> TMA store
 #pragma once
 
 #include "gemm.hpp"
@@ -24,7 +24,7 @@
 
 namespace hmi_b200 {
 
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // 64 x 16-bit = 128 B = one SWIZZLE_128B atom row
 
@@ -66,7 +66,7 @@ struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 warps x double buffer x (32 rows x 128 B)
+  static constexpr int kEpiBytes = 8 * 4096;  // 8 epilogue warps x (32 rows x 128 B)
   static constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 256 /*barriers*/;
   static constexpr int kStagesRaw = (kBudget - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], 8);
     }
     fence_mbar_init();
   }
@@ -176,9 +176,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // 8 warps: warp w reads TMEM lane quarter (w % 4) and every other kCW-column chunk
+    // (half = (w - 2) / 4), so two warps share each quarter.
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
-    uint32_t sbuf = 0, acc = 0, acc_phase = 0;
+    const int half = static_cast<int>(warp - 2) >> 2;
+    uint8_t* stg = sEpi + (warp - 2) * 4096;
+    uint32_t acc = 0, acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int mt = t / args.num_n_tiles;
       const int nt = t - mt * args.num_n_tiles;
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t t_row = tmem_base + ((q * 32) << 16) + acc * BN;
 
 #pragma unroll 1
-      for (int c = 0; c < BN; c += kCW) {
+      for (int c = half * kCW; c < BN; c += 2 * kCW) {
         float v[kCW];
 #pragma unroll
         for (int j = 0; j < kCW / 32; ++j) {
@@ -202,12 +205,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
-        }
-        if (c + kCW >= BN) {
-          // all TMEM reads of this accumulator are done: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
         }
 #pragma unroll
         for (int i = 0; i < kCW; i += 4) {
@@ -236,10 +233,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
         }
-        // staging buffer reuse: the store issued two chunks ago must have read it
-        if (lane == 0) tma_store_wait_read<1>();
+        // staging buffer reuse: this warp's previous TMA store must have read it
+        if (lane == 0) tma_store_wait_read<0>();
         __syncwarp();
-        uint8_t* buf = stg + sbuf * 4096;
+        uint8_t* buf = stg;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int phys = i ^ (lane & 7);  // SWIZZLE_128B: 16 B chunk ^= row % 8
@@ -252,8 +249,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_store_2d(&map_c, buf, nt * BN + c, row0);
           tma_store_commit();
         }
-        sbuf ^= 1;
       }
+      // all TMEM reads of this accumulator by this warp are done: hand it back
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }

@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-// K5: PLOT retrieval, one CTA per request.
+// K5: PLOT retrieval, one CTA per (request, 32-position chunk).
+constexpr int kRetrieveChunk = 32;
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int32_t plot_find(const PlotDev& P, uint32_t version,
                                              const uint32_t* key, uint32_t len) {
@@ -117,18 +118,24 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
                                                        int32_t* __restrict__ gather,
                                                        int32_t* __restrict__ levels,
                                                        int32_t* __restrict__ err) {
-  extern __shared__ int32_t sm[];
+  constexpr int kMaxWin = kRetrieveChunk + kMaxNgram;
+  __shared__ int32_t wrow[kMaxWin * kMaxNgram];  // rep row per (window, offset)
+  __shared__ int32_t wlev[kMaxWin * kMaxNgram];  // sub-gram length
   const int n = P.ngram;
-  int32_t* wrow = sm;              // [S][n] rep row per (window, offset)
-  int32_t* wlev = sm + S * n;      // [S][n] sub-gram length
   const int b = blockIdx.x;
+  const int p0 = blockIdx.y * kRetrieveChunk;
+  const int p1 = p0 + kRetrieveChunk < S ? p0 + kRetrieveChunk : S;
   const int len = lens[b];
   const int version = req_version[b];
   const uint32_t* tok = tokens + static_cast<long long>(b) * S;
   const int hl = (n - 1) / 2, hr = n - 1 - hl;
+  // windows this chunk of positions needs (encoder: centred windows covering them;
+  // causal: the window ending at each position)
+  const int c0 = causal ? p0 : (p0 - hr > 0 ? p0 - hr : 0);
+  const int c1 = causal ? (p1 < len ? p1 : len) - 1 : (p1 - 1 + hl < len - 1 ? p1 - 1 + hl : len - 1);
 
-  // ---- phase 1: resolve every window (resolve_window, retrieval.cpp:23-69)
-  for (int c = threadIdx.x; c < len; c += blockDim.x) {
+  // ---- phase 1: resolve every needed window (resolve_window, retrieval.cpp:23-69)
+  for (int c = c0 + static_cast<int>(threadIdx.x); c <= c1; c += blockDim.x) {
     int start, end;
     if (causal) {
       start = c + 1 >= n ? c + 1 - n : 0;
@@ -161,8 +168,8 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
         }
       }
       if (row < 0) atomicExch(err, HMI_BUILD_ERROR);  // uni-gram backstop missing
-      wrow[c * n + p] = row;
-      wlev[c * n + p] = lev;
+      wrow[(c - c0) * n + p] = row;
+      wlev[(c - c0) * n + p] = lev;
     }
   }
   __syncthreads();
@@ -172,7 +179,7 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
   const int nwarps = blockDim.x >> 5;
   const int d = P.d;
   const int V = d / 128;  // float4 per lane
-  for (int p = warp; p < S; p += nwarps) {
+  for (int p = p0 + warp; p < p1; p += nwarps) {
     const long long orow = static_cast<long long>(b) * S + p;
     int32_t rows[kMaxNgram];
     int32_t levs[kMaxNgram];
@@ -180,16 +187,16 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
     if (p < len) {
       if (causal) {
         const int start = p + 1 >= n ? p + 1 - n : 0;
-        rows[0] = wrow[p * n + (p - start)];
-        levs[0] = wlev[p * n + (p - start)];
+        rows[0] = wrow[(p - c0) * n + (p - start)];
+        levs[0] = wlev[(p - c0) * n + (p - start)];
         cnt = 1;
       } else {
         const int c_lo = p - hr > 0 ? p - hr : 0;
         const int c_hi = p + hl < len - 1 ? p + hl : len - 1;
         for (int c = c_lo; c <= c_hi; ++c) {
           const int start = c >= hl ? c - hl : 0;
-          rows[cnt] = wrow[c * n + (p - start)];
-          levs[cnt] = wlev[c * n + (p - start)];
+          rows[cnt] = wrow[(c - c0) * n + (p - start)];
+          levs[cnt] = wlev[(c - c0) * n + (p - start)];
           ++cnt;
         }
       }
@@ -206,13 +213,22 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
     for (int i = 0; i < V; ++i) {
       const int col = (lane + 32 * i) * 4;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (int k = 0; k < cnt; ++k) {
-        const int32_t r = rows[k] < 0 ? 0 : rows[k];
-        const float4 x = __ldg(reinterpret_cast<const float4*>(P.reps + static_cast<long long>(r) * d + col));
-        a0 = a0 + static_cast<double>(x.x);
-        a1 = a1 + static_cast<double>(x.y);
-        a2 = a2 + static_cast<double>(x.z);
-        a3 = a3 + static_cast<double>(x.w);
+      float4 xs[kMaxNgram];
+#pragma unroll
+      for (int k = 0; k < kMaxNgram; ++k) {
+        if (k < cnt) {
+          const int32_t r = rows[k] < 0 ? 0 : rows[k];
+          xs[k] = __ldg(reinterpret_cast<const float4*>(P.reps + static_cast<long long>(r) * d + col));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kMaxNgram; ++k) {  // ascending window order (add_f64 sweep)
+        if (k < cnt) {
+          a0 = a0 + static_cast<double>(xs[k].x);
+          a1 = a1 + static_cast<double>(xs[k].y);
+          a2 = a2 + static_cast<double>(xs[k].z);
+          a3 = a3 + static_cast<double>(xs[k].w);
+        }
       }
       a0 *= inv; a1 *= inv; a2 *= inv; a3 *= inv;
       if (h64) {
@@ -335,12 +351,46 @@ __global__ void __launch_bounds__(256) head_kernel(HeadDev H, const float* __res
   __syncthreads();
   double best = -INFINITY;
   int besti = 0x7fffffff;
-  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-    double acc = 0.0;
-    for (int j = 0; j < d; ++j) acc += xs[j] * static_cast<double>(W[static_cast<long long>(j) * nl + l]);
-    acc += static_cast<double>(B[l]);
-    if (l < max_labels) scores[static_cast<long long>(b) * max_labels + l] = static_cast<float>(acc);
-    if (acc > best) { best = acc; besti = l; }  // labels visited in ascending order
+  if (nl <= 32) {
+    // narrow head (cls): split d across the block, reduce per label
+    double acc[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) acc[l] = 0.0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const double xj = xs[j];
+      const float* wr = W + static_cast<long long>(j) * nl;
+#pragma unroll
+      for (int l = 0; l < 32; ++l)
+        if (l < nl) acc[l] += xj * static_cast<double>(__ldg(wr + l));
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      if (l >= nl) break;
+      double v = acc[l];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) rv[warp * 32 + l] = v;  // rv has room for blockDim doubles
+    }
+    __syncthreads();
+    if (threadIdx.x < nl) {
+      const int l = threadIdx.x;
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += rv[w * 32 + l];
+      s += static_cast<double>(B[l]);
+      if (l < max_labels) scores[static_cast<long long>(b) * max_labels + l] = static_cast<float>(s);
+      best = s;
+      besti = l;
+    }
+    __syncthreads();
+  } else {
+    // wide head (lm): one label per thread, W rows read coalesced across the block
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) acc += xs[j] * static_cast<double>(W[static_cast<long long>(j) * nl + l]);
+      acc += static_cast<double>(B[l]);
+      if (l < max_labels) scores[static_cast<long long>(b) * max_labels + l] = static_cast<float>(acc);
+      if (acc > best) { best = acc; besti = l; }  // labels visited in ascending order
+    }
   }
   rv[threadIdx.x] = best;
   ri[threadIdx.x] = besti;
@@ -391,12 +441,8 @@ void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* len
                      int32_t* err, cudaStream_t stream) {
   if (n_req <= 0) return;
   HMI_CHECK(plot.d % 128 == 0, HMI_CONFIG_ERROR, "retrieve: d must be a multiple of 128");
-  const size_t smem = static_cast<size_t>(S) * plot.ngram * 2 * sizeof(int32_t);
-  if (smem > 48 * 1024) {
-    HMI_CUDA(cudaFuncSetAttribute(retrieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-  }
-  retrieve_kernel<<<n_req, 256, smem, stream>>>(plot, tokens, lens, req_version, S, causal, h16,
+  dim3 grid(n_req, (S + kRetrieveChunk - 1) / kRetrieveChunk);
+  retrieve_kernel<<<grid, 256, 0, stream>>>(plot, tokens, lens, req_version, S, causal, h16,
                                                 precision, h64_debug, gather, levels, err);
   HMI_CUDA(cudaGetLastError());
 }
