@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -91,6 +92,7 @@ struct LayerDev {
   uint16_t *wqkv, *wo, *w1, *w2;  // [N][K] 16-bit (transposed from [in x out])
   float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
   GemmPlan qkv, oproj, ad_down, ad_up, ffn1, ffn2;
+  GemmPlan ad_up_ln, ffn2_ln;  // LayerNorm fused into the epilogue (cluster row reduction)
 };
 
 struct Staging {
@@ -112,14 +114,39 @@ struct Inflight {
   std::vector<uint32_t> tasks;
 };
 
-int pick_bn(int N, int m_tiles, int sms) {
+// N tile with the least wave quantisation; `pair`: units are 256-row CTA-pair tiles
+// scheduled over sms/2 clusters (cta_group::2 kernel).
+int pick_bn(int N, int m_tiles, int sms, bool pair = false) {
   int best = -1;
   double best_eff = -1;
+  if (pair) {
+    m_tiles = (m_tiles + 1) / 2;
+    sms /= 2;
+  }
   for (int bn : {256, 192, 128, 64}) {
-    if (N % bn) continue;
+    if (N % bn || (pair && bn < 128)) continue;
     const long tiles = static_cast<long>(N / bn) * m_tiles;
     const long waves = (tiles + sms - 1) / sms;
     const double eff = static_cast<double>(tiles) / (waves * sms);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+// N tile of an LN-fused GEMM: one cluster of N / bn CTAs per 128-row tile; choose the
+// cluster width with the best occupancy x wave efficiency.
+int pick_bn_ln(int N, int m_tiles, int sms) {
+  int best = -1;
+  double best_eff = -1;
+  for (int bn : {256, 192, 128, 64}) {
+    if (N % bn || N / bn > 8) continue;
+    const int cs = N / bn;
+    const int clusters = sms / cs;
+    const long rounds = (m_tiles + clusters - 1) / clusters;
+    const double eff = static_cast<double>(m_tiles) * cs / (static_cast<double>(rounds) * sms);
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = bn;
@@ -188,6 +215,7 @@ struct Ctx {
   // last batch (introspection)
   uint32_t last_n = 0, last_S = 0;
   uint32_t debug_flags = 0;
+  bool fused_ln = true;  // HMI_UNFUSED_LN=1 selects the separate K4 LayerNorm kernels
   // profiling
   bool prof = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -340,12 +368,13 @@ void Ctx::build_plans() {
     s.b = w.wqkv; s.N = 3 * d; s.groups = 1; s.b_ld = d; s.b_group_stride_bytes = size_t(3) * d * d * 2;
     s.bias = w.bqkv; s.bias_group_stride = 0; s.tile_slot = nullptr;
     s.res0 = s.res1 = nullptr; s.res_ld = 0;
-    s.c = qkv16.p; s.c_ld = 3 * d; s.epi = 0; s.bn = pick_bn(3 * d, m_tiles, sms);
+    s.c = qkv16.p; s.c_ld = 3 * d; s.epi = 0; s.cta2 = true;
+    s.bn = pick_bn(3 * d, m_tiles, sms, true);
     w.qkv = make_gemm_plan(s);
     // O projection
     s.a = ctx16.p; s.a_ld = d; s.K = d;
     s.b = w.wo; s.N = d; s.b_ld = d; s.b_group_stride_bytes = size_t(d) * d * 2;
-    s.bias = w.bo; s.c = a16.p; s.c_ld = d; s.epi = 0; s.bn = pick_bn(d, m_tiles, sms);
+    s.bias = w.bo; s.c = a16.p; s.c_ld = d; s.epi = 0; s.bn = pick_bn(d, m_tiles, sms, true);
     w.oproj = make_gemm_plan(s);
     // adapter down (grouped): mid = relu(a . Wd + bd)
     s.a = a16.p; s.a_ld = d; s.K = d;
@@ -361,21 +390,50 @@ void Ctx::build_plans() {
     s.b = arena.p + off_wu; s.N = d; s.b_ld = r_pad;
     s.bias = reinterpret_cast<const float*>(arena.p + off_bu);
     s.res0 = a16.p; s.res1 = h16.p; s.res_ld = d;
-    s.c = y32.p; s.c_ld = d; s.epi = kEpiRes2 | kEpiOutF32; s.bn = pick_bn(d, m_tiles, sms);
+    s.c = y32.p; s.c_ld = d; s.epi = kEpiRes2 | kEpiOutF32; s.cta2 = false;
+    s.bn = pick_bn(d, m_tiles, sms);
     w.ad_up = make_gemm_plan(s);
     // FFN1: relu(x . W1 + b1)
     s.a = x16.p; s.a_ld = d; s.K = d;
     s.b = w.w1; s.N = f; s.groups = 1; s.b_ld = d; s.b_group_stride_bytes = size_t(f) * d * 2;
     s.bias = w.b1; s.bias_group_stride = 0; s.tile_slot = nullptr;
     s.res0 = s.res1 = nullptr;
-    s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.bn = pick_bn(f, m_tiles, sms);
+    s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.cta2 = true;
+    s.bn = pick_bn(f, m_tiles, sms, true);
     w.ffn1 = make_gemm_plan(s);
     // FFN2 + residual: y = ffn . W2 + b2 + x
     s.a = ffn16.p; s.a_ld = f; s.K = f;
     s.b = w.w2; s.N = d; s.b_ld = f; s.b_group_stride_bytes = size_t(d) * f * 2;
     s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
-    s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, m_tiles, sms);
+    s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, m_tiles, sms, true);
     w.ffn2 = make_gemm_plan(s);
+    // fused variants: adapter up + skip + residual + LN1 -> x16; FFN2 + residual + LN2 -> h16
+    {
+      GemmSpec u;
+      u.precision = prec;
+      u.a_rows = max_rows;
+      u.a = mid16.p; u.a_ld = r_pad; u.K = r_pad;
+      u.b = arena.p + off_wu; u.N = d; u.groups = static_cast<int>(n_slots); u.b_ld = r_pad;
+      u.b_group_stride_bytes = slot_bytes;
+      u.bias = reinterpret_cast<const float*>(arena.p + off_bu);
+      u.bias_group_stride = static_cast<long long>(slot_bytes / 4);
+      u.tile_slot = d_tile_slot.p + static_cast<size_t>(l) * tile_stride;
+      u.res0 = a16.p; u.res1 = h16.p; u.res_ld = d;
+      u.c = x16.p; u.c_ld = d; u.epi = kEpiRes2 | kEpiLN; u.bn = pick_bn_ln(d, m_tiles, sms);
+      u.ln_gamma = w.ln1g; u.ln_beta = w.ln1b;
+      w.ad_up_ln = make_gemm_plan(u);
+      GemmSpec g;
+      g.precision = prec;
+      g.a_rows = max_rows;
+      g.a = ffn16.p; g.a_ld = f; g.K = f;
+      g.b = w.w2; g.N = d; g.groups = 1; g.b_ld = f; g.b_group_stride_bytes = size_t(d) * f * 2;
+      g.bias = w.b2; g.res0 = x16.p; g.res_ld = d;
+      g.c = h16.p; g.c_ld = d; g.bn = pick_bn_ln(d, m_tiles, sms);
+      g.epi = kEpiRes1 | kEpiLN | (l == L - 1 ? kEpiOut2F32 : 0);
+      g.c2 = h32.p; g.c2_ld = d;
+      g.ln_gamma = w.ln2g; g.ln_beta = w.ln2b;
+      w.ffn2_ln = make_gemm_plan(g);
+    }
   }
 }
 
@@ -594,13 +652,19 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
     if (fine) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
     timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
-    timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
-    timed(P_LN1, s, [&] { launch_layernorm(y32.p, w.ln1g, w.ln1b, x16.p, nullptr, rows, d, prec, s); });
-    timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
-    timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
-    timed(P_LN2, s, [&] {
-      launch_layernorm(y32.p, w.ln2g, w.ln2b, h16.p, last ? h32.p : nullptr, rows, d, prec, s);
-    });
+    if (fused_ln) {
+      timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up_ln, rows, s); });
+      timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
+      timed(P_FFN2, s, [&] { launch_gemm(w.ffn2_ln, rows, s); });
+    } else {
+      timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
+      timed(P_LN1, s, [&] { launch_layernorm(y32.p, w.ln1g, w.ln1b, x16.p, nullptr, rows, d, prec, s); });
+      timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
+      timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
+      timed(P_LN2, s, [&] {
+        launch_layernorm(y32.p, w.ln2g, w.ln2b, h16.p, last ? h32.p : nullptr, rows, d, prec, s);
+      });
+    }
   }
   HeadDev H;
   H.arena = d_head_arena.p;
@@ -624,7 +688,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   st.busy = true;
   inflight.push_back(Inflight{st.done, si, uniq});
   last_n = n_req;
-  n_launches += (delta.empty() ? 0 : 1) + 3 + 9ull * L;
+  n_launches += (delta.empty() ? 0 : 1) + 3 + (fused_ln ? 7ull : 9ull) * L;
   ++n_batches;
   last_S = static_cast<uint32_t>(S);
   return si;
@@ -835,6 +899,7 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     c.pool = std::make_unique<SlotPool>(pool_bytes, static_cast<uint32_t>(n_slots64));
     c.arena.alloc(static_cast<size_t>(n_slots64) * c.slot_bytes);
     HMI_CUDA(cudaMemset(c.arena.p, 0, c.arena.n));
+    if (const char* env = std::getenv("HMI_UNFUSED_LN")) c.fused_ln = env[0] != '1';
     c.build_plans();
     HMI_CUDA(cudaDeviceSynchronize());
   });

@@ -13,38 +13,72 @@ namespace hmi_b200 {
 
 namespace {
 
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool C2>
 KernelFn kernel_ptr() {
-  return reinterpret_cast<KernelFn>(&gemm_tcgen05_kernel<BN, EPI>);
-}
-
-template <int BN, int T>
-KernelFn pick_epi_t(int epi) {
-  switch (epi) {
-    case 0: return kernel_ptr<BN, T>();
-    case kEpiRelu: return kernel_ptr<BN, T | kEpiRelu>();
-    case kEpiRes1: return kernel_ptr<BN, T | kEpiRes1>();
-    case kEpiRes2: return kernel_ptr<BN, T | kEpiRes2>();
-    case kEpiOutF32: return kernel_ptr<BN, T | kEpiOutF32>();
-    case kEpiRes1 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes1 | kEpiOutF32>();
-    case kEpiRes2 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes2 | kEpiOutF32>();
-    default: return nullptr;
+  if constexpr (C2) {
+    return reinterpret_cast<KernelFn>(&gemm2_tcgen05_kernel<BN, EPI>);
+  } else {
+    return reinterpret_cast<KernelFn>(&gemm_tcgen05_kernel<BN, EPI>);
   }
 }
 
-template <int BN>
-KernelFn pick_epi(int epi) {
-  return (epi & kEpiBf16) ? pick_epi_t<BN, kEpiBf16>(epi & ~kEpiBf16) : pick_epi_t<BN, 0>(epi);
+template <int BN, int T, bool C2>
+KernelFn pick_epi_t(int epi) {
+  switch (epi) {
+    case 0: return kernel_ptr<BN, T, C2>();
+    case kEpiRelu: return kernel_ptr<BN, T | kEpiRelu, C2>();
+    case kEpiRes1: return kernel_ptr<BN, T | kEpiRes1, C2>();
+    case kEpiRes2: return kernel_ptr<BN, T | kEpiRes2, C2>();
+    case kEpiOutF32: return kernel_ptr<BN, T | kEpiOutF32, C2>();
+    case kEpiRes1 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes1 | kEpiOutF32, C2>();
+    case kEpiRes2 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes2 | kEpiOutF32, C2>();
+    default: break;
+  }
+  if constexpr (!C2) {
+    switch (epi) {
+      case kEpiRes1 | kEpiLN: return kernel_ptr<BN, T | kEpiRes1 | kEpiLN, false>();
+      case kEpiRes2 | kEpiLN: return kernel_ptr<BN, T | kEpiRes2 | kEpiLN, false>();
+      case kEpiRes1 | kEpiLN | kEpiOut2F32:
+        return kernel_ptr<BN, T | kEpiRes1 | kEpiLN | kEpiOut2F32, false>();
+      case kEpiRes2 | kEpiLN | kEpiOut2F32:
+        return kernel_ptr<BN, T | kEpiRes2 | kEpiLN | kEpiOut2F32, false>();
+      default: break;
+    }
+  }
+  return nullptr;
 }
 
-KernelFn pick_kernel(int bn, int epi, int* smem_bytes) {
+template <int BN, bool C2>
+KernelFn pick_epi(int epi) {
+  return (epi & kEpiBf16) ? pick_epi_t<BN, kEpiBf16, C2>(epi & ~kEpiBf16)
+                          : pick_epi_t<BN, 0, C2>(epi);
+}
+
+KernelFn pick_kernel(int bn, int epi, bool c2, int* smem_bytes) {
+  if (c2) {
+    switch (bn) {
+      case 128: *smem_bytes = Gemm2Smem<128>::kTotal; return pick_epi<128, true>(epi);
+      case 192: *smem_bytes = Gemm2Smem<192>::kTotal; return pick_epi<192, true>(epi);
+      case 256: *smem_bytes = Gemm2Smem<256>::kTotal; return pick_epi<256, true>(epi);
+      default: return nullptr;
+    }
+  }
+  const bool ln = (epi & kEpiLN) != 0;
   switch (bn) {
-    case 64: *smem_bytes = GemmSmem<64>::kTotal; return pick_epi<64>(epi);
-    case 128: *smem_bytes = GemmSmem<128>::kTotal; return pick_epi<128>(epi);
-    case 192: *smem_bytes = GemmSmem<192>::kTotal; return pick_epi<192>(epi);
-    case 256: *smem_bytes = GemmSmem<256>::kTotal; return pick_epi<256>(epi);
+    case 64:
+      *smem_bytes = ln ? GemmSmem<64, true>::kTotal : GemmSmem<64>::kTotal;
+      return pick_epi<64, false>(epi);
+    case 128:
+      *smem_bytes = ln ? GemmSmem<128, true>::kTotal : GemmSmem<128>::kTotal;
+      return pick_epi<128, false>(epi);
+    case 192:
+      *smem_bytes = ln ? GemmSmem<192, true>::kTotal : GemmSmem<192>::kTotal;
+      return pick_epi<192, false>(epi);
+    case 256:
+      *smem_bytes = ln ? GemmSmem<256, true>::kTotal : GemmSmem<256>::kTotal;
+      return pick_epi<256, false>(epi);
     default: return nullptr;
   }
 }
@@ -59,18 +93,33 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   HMI_CHECK(s.a_rows % kBlockM == 0, HMI_CONFIG_ERROR, "gemm: A rows must be a multiple of 128");
   GemmPlan p;
   const int epi = s.epi | (s.precision == 1 ? kEpiBf16 : 0);
-  p.fn = reinterpret_cast<void*>(pick_kernel(s.bn, epi, &p.smem_bytes));
+  const bool ln = (s.epi & kEpiLN) != 0;
+  const bool c2 = s.cta2 && !ln && s.groups == 1 && s.tile_slot == nullptr && s.bn >= 128;
+  if (ln) {
+    HMI_CHECK(s.N / s.bn >= 1 && s.N / s.bn <= 8, HMI_CONFIG_ERROR,
+              "gemm: LayerNorm epilogue needs N / BN in [1, 8] (one cluster per row block)");
+    HMI_CHECK(s.bn % 64 == 0 && s.ln_gamma && s.ln_beta, HMI_CONFIG_ERROR, "gemm: LN epilogue args");
+    p.cluster_n = s.N / s.bn;
+  }
+  p.two_cta = c2;
+  p.fn = reinterpret_cast<void*>(pick_kernel(s.bn, epi, c2, &p.smem_bytes));
   HMI_CHECK(p.fn != nullptr, HMI_CONFIG_ERROR, "gemm: unsupported epilogue");
   const CUtensorMapDataType t16 =
       s.precision == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   p.map_a = make_tmap_2d(s.a, t16, s.K, s.a_rows, s.a_ld * 2ull, kBlockK, kBlockM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
   p.map_b = make_tmap_3d(s.b, t16, s.K, s.N, s.groups, s.b_ld * 2ull, s.b_group_stride_bytes,
-                         kBlockK, s.bn, CU_TENSOR_MAP_SWIZZLE_128B);
-  const bool f32 = (s.epi & kEpiOutF32) != 0;
+                         kBlockK, c2 ? s.bn / 2 : s.bn, CU_TENSOR_MAP_SWIZZLE_128B);
+  const bool f32 = (s.epi & kEpiOutF32) != 0 && !ln;
   p.map_c = make_tmap_2d(s.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : t16, s.N, s.a_rows,
                          s.c_ld * (f32 ? 4ull : 2ull), f32 ? 32 : 64, 32,
                          CU_TENSOR_MAP_SWIZZLE_128B);
+  p.map_c2 = p.map_c;
+  if (s.epi & kEpiOut2F32) {
+    HMI_CHECK(s.c2 != nullptr, HMI_CONFIG_ERROR, "gemm: f32 copy output missing");
+    p.map_c2 = make_tmap_2d(s.c2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, s.N, s.a_rows, s.c2_ld * 4ull,
+                            32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
   p.args = GemmArgs{};
   p.args.N = s.N;
   p.args.K = s.K;
@@ -81,7 +130,9 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.res0 = reinterpret_cast<const __half*>(s.res0);
   p.args.res1 = reinterpret_cast<const __half*>(s.res1);
   p.args.res_ld = s.res_ld;
-  p.args.idesc = idesc_f16(kBlockM, s.bn, s.precision == 1 ? 1u : 0u);
+  p.args.ln_gamma = s.ln_gamma;
+  p.args.ln_beta = s.ln_beta;
+  p.args.idesc = idesc_f16(c2 ? 2 * kBlockM : kBlockM, s.bn, s.precision == 1 ? 1u : 0u);
   p.max_rows = s.a_rows;
   return p;
 }
@@ -105,10 +156,38 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
   GemmArgs a = p.args;
   a.M = M;
   a.num_m_tiles = M / kBlockM;
-  const int tiles = a.num_m_tiles * a.num_n_tiles;
-  const int grid = tiles < device_sm_count() ? tiles : device_sm_count();
+  int grid;
+  if (p.cluster_n > 1 || (p.args.ln_gamma && p.cluster_n == 1)) {
+    // LN epilogue: one cluster of cluster_n CTAs per M tile
+    const int per = p.cluster_n;
+    const int clusters_max = device_sm_count() / per;
+    const int clusters = a.num_m_tiles < clusters_max ? a.num_m_tiles : clusters_max;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * per);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = per;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KernelFn fn = reinterpret_cast<KernelFn>(p.fn);
+    HMI_CUDA(cudaLaunchKernelEx(&cfg, fn, p.map_a, p.map_b, p.map_c, p.map_c2, a));
+    return;
+  }
+  if (p.two_cta) {
+    const int units = (a.num_m_tiles + 1) / 2 * a.num_n_tiles;
+    const int pairs = device_sm_count() / 2;
+    grid = 2 * (units < pairs ? units : pairs);
+  } else {
+    const int tiles = a.num_m_tiles * a.num_n_tiles;
+    grid = tiles < device_sm_count() ? tiles : device_sm_count();
+  }
   KernelFn fn = reinterpret_cast<KernelFn>(p.fn);
-  fn<<<grid, kGemmThreads, p.smem_bytes, stream>>>(p.map_a, p.map_b, p.map_c, a);
+  fn<<<grid, kGemmThreads, p.smem_bytes, stream>>>(p.map_a, p.map_b, p.map_c, p.map_c2, a);
   HMI_CUDA(cudaGetLastError());
 }
 
@@ -122,6 +201,8 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
                                   const int32_t* tile_slot, const uint16_t* res0,
                                   const uint16_t* res1, int epi, int bn, int precision,
                                   void* out, float* elapsed_ms) {
+  const bool cta2 = (epi & 256) != 0;  // probe flag: request the cta_group::2 kernel
+  epi &= ~256;
   using namespace hmi_b200;
   void *dA = nullptr, *dB = nullptr, *dBias = nullptr, *dC = nullptr, *dSlot = nullptr,
        *dR0 = nullptr, *dR1 = nullptr;
@@ -159,7 +240,7 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
     s.tile_slot = static_cast<const int*>(dSlot);
     s.res0 = dR0; s.res1 = dR1; s.res_ld = N;
     s.c = dC; s.c_ld = N;
-    s.epi = epi; s.bn = bn; s.precision = precision;
+    s.epi = epi; s.bn = bn; s.precision = precision; s.cta2 = cta2;
     GemmPlan p = make_gemm_plan(s);
     HMI_CUDA(cudaEventCreate(&e0));
     HMI_CUDA(cudaEventCreate(&e1));

@@ -21,6 +21,8 @@ struct GemmArgs {
   const __half* res1;
   int res_ld;
   uint32_t idesc;
+  const float* ln_gamma;       // kEpiLN: LayerNorm gain / shift over the full N-wide row
+  const float* ln_beta;
 };
 
 // Epilogue flags
@@ -29,6 +31,8 @@ constexpr int kEpiRes1 = 2;  // add res0
 constexpr int kEpiRes2 = 4;  // add res0 + res1
 constexpr int kEpiOutF32 = 8;
 constexpr int kEpiBf16 = 16;  // 16-bit outputs / residuals are bf16 (set from precision)
+constexpr int kEpiLN = 32;    // LayerNorm over the row (cluster of N/BN CTAs), 16-bit output
+constexpr int kEpiOut2F32 = 64;  // with kEpiLN: also write an f32 copy through map_c2
 
 // Everything needed to bind one GEMM to fixed device buffers.
 struct GemmSpec {
@@ -48,14 +52,21 @@ struct GemmSpec {
   int epi = 0;                       // kEpi* flags
   int bn = 256;                      // N tile
   int precision = 0;                 // 0 fp16, 1 bf16
+  bool cta2 = false;                 // cta_group::2 pair kernel (shared weights only)
+  const float* ln_gamma = nullptr;   // kEpiLN
+  const float* ln_beta = nullptr;
+  void* c2 = nullptr;                // kEpiOut2F32: f32 copy [a_rows][c2_ld]
+  int c2_ld = 0;
 };
 
 struct GemmPlan {
-  CUtensorMap map_a, map_b, map_c;
+  CUtensorMap map_a, map_b, map_c, map_c2;
   GemmArgs args;
   void* fn = nullptr;
   int smem_bytes = 0;
   int max_rows = 0;
+  bool two_cta = false;
+  int cluster_n = 1;  // kEpiLN: CTAs per cluster along N (= N / BN)
 };
 
 GemmPlan make_gemm_plan(const GemmSpec& s);

@@ -61,16 +61,247 @@ __device__ __forceinline__ void add_res16(float* v, const uint16_t* src) {
   }
 }
 
-template <int BN>
+// One accumulator tile (128 rows x BN cols in TMEM) -> bias / residual / ReLU -> 16/32-bit
+// -> swizzled smem staging -> TMA store. Called by 8 epilogue warps: warp (q, half) owns TMEM
+// lane quarter q and every other kCW-column chunk.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, int grp,
+                                              const GemmArgs& args, const CUtensorMap* map_c,
+                                              uint8_t* stg, uint32_t q, int half, uint32_t lane) {
+  constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
+  constexpr bool kBf16 = (EPI & kEpiBf16) != 0;  // 16-bit tensors are bf16 (else fp16)
+  constexpr int kCW = kOutF32 ? 32 : 64;         // output columns per 128-byte staging row
+  static_assert(BN % kCW == 0, "BN must be a multiple of the store chunk");
+  const float* bias = args.bias + grp * args.bias_slot_stride + nt * BN;
+  const int row0 = mt * kBlockM + static_cast<int>(q) * 32;
+  const int row = row0 + static_cast<int>(lane);
+  const bool row_ok = row < args.M;
+  const uint32_t t_row = t_acc + ((q * 32) << 16);
+#pragma unroll 1
+  for (int c = half * kCW; c < BN; c += 2 * kCW) {
+    float v[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW / 32; ++j) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kCW; i += 4) {
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
+      v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+    }
+    if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
+      if (row_ok) {
+        const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
+        add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off);
+        if constexpr ((EPI & kEpiRes2) != 0) {
+          add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off);
+        }
+      }
+    }
+    if constexpr ((EPI & kEpiRelu) != 0) {
+#pragma unroll
+      for (int i = 0; i < kCW; ++i) v[i] = fmaxf(v[i], 0.0f);
+    }
+    uint32_t packed[32];  // one 128-byte row per thread
+    if constexpr (kOutF32) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) packed[i] = __float_as_uint(v[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
+    }
+    // staging buffer reuse: this warp's previous TMA store must have read it
+    if (lane == 0) tma_store_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int phys = i ^ (lane & 7);  // SWIZZLE_128B: 16 B chunk ^= row % 8
+      *reinterpret_cast<uint4*>(stg + lane * 128 + phys * 16) =
+          make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && mt < args.num_m_tiles) {
+      tma_store_2d(map_c, stg, nt * BN + c, row0);
+      tma_store_commit();
+    }
+  }
+}
+
+// LayerNorm epilogue (kEpiLN): the CTA owns BN of the row's N = cluster_n * BN columns.
+// Pass 1 adds bias (+ residuals) and writes the pre-norm value back into TMEM while
+// accumulating per-row (sum, sum of squares); the two column halves combine in smem,
+// every CTA pushes (mean_c, M2_c) to all cluster peers over DSMEM, and the exact
+// parallel-variance merge gives the row's mean / variance (layer_norm, ops.cpp:92-116,
+// epsilon 1e-5, biased variance). Pass 2 re-reads TMEM, normalises with gamma/beta and
+// TMA-stores 16-bit (and optionally f32) rows.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile_ln(uint32_t t_acc, int mt, int nt, int grp,
+                                                 const GemmArgs& args, const CUtensorMap* map_c,
+                                                 const CUtensorMap* map_c2, uint8_t* stg,
+                                                 uint32_t q, int half, uint32_t lane,
+                                                 float2* partial, float2* stats,
+                                                 uint64_t* stats_bar, uint32_t iter,
+                                                 uint32_t cs, uint32_t rank) {
+  constexpr bool kBf16 = (EPI & kEpiBf16) != 0;
+  constexpr int kCW = 64;
+  static_assert(BN % kCW == 0, "LN epilogue works in 64-column chunks");
+  const float* bias = args.bias + grp * args.bias_slot_stride + nt * BN;
+  const int row_local = static_cast<int>(q) * 32 + static_cast<int>(lane);
+  const int row0 = mt * kBlockM + static_cast<int>(q) * 32;
+  const int row = row0 + static_cast<int>(lane);
+  const bool row_ok = row < args.M;
+  const uint32_t t_row = t_acc + ((q * 32) << 16);
+  // ---- pass 1
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll 1
+  for (int c = half * kCW; c < BN; c += 2 * kCW) {
+    float v[kCW];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kCW; i += 4) {
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
+      v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+    }
+    if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
+      if (row_ok) {
+        const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
+        add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off);
+        if constexpr ((EPI & kEpiRes2) != 0) {
+          add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kCW; ++i) {
+      s1 += v[i];
+      s2 += v[i] * v[i];
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint32_t r[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[32 * j + i]);
+      tmem_st_32x32b_x32(t_row + c + 32 * j, r);
+    }
+  }
+  tmem_st_wait();
+  // ---- row statistics: halves -> CTA -> cluster
+  if (half == 1) partial[row_local] = make_float2(s1, s2);
+  named_bar_sync(1, 256);
+  const uint32_t buf = iter & 1;
+  if (half == 0) {
+    s1 += partial[row_local].x;
+    s2 += partial[row_local].y;
+    const float mean_c = s1 * (1.0f / BN);
+    const float m2_c = fmaxf(s2 - s1 * mean_c, 0.0f);
+    const uint32_t dst = smem_u32(&stats[(buf * 8 + rank) * 128 + row_local]);
+    const uint32_t bar = smem_u32(&stats_bar[buf]);
+    for (uint32_t p = 0; p < cs; ++p) {
+      st_cluster_f32x2(mapa_shared(dst, p), mean_c, m2_c);
+      mbar_arrive_cluster(mapa_shared(bar, p));
+    }
+  }
+  mbar_wait(&stats_bar[buf], (iter >> 1) & 1);
+  float mean = 0.f;
+  for (uint32_t p = 0; p < cs; ++p) mean += stats[(buf * 8 + p) * 128 + row_local].x;
+  mean /= static_cast<float>(cs);
+  float m2 = 0.f;
+  for (uint32_t p = 0; p < cs; ++p) {
+    const float2 st = stats[(buf * 8 + p) * 128 + row_local];
+    const float dm = st.x - mean;
+    m2 += st.y + static_cast<float>(BN) * dm * dm;
+  }
+  const float inv = 1.0f / sqrtf(m2 / static_cast<float>(cs * BN) + 1e-5f);
+  // ---- pass 2
+  const float* gam = args.ln_gamma + nt * BN;
+  const float* bet = args.ln_beta + nt * BN;
+#pragma unroll 1
+  for (int c = half * kCW; c < BN; c += 2 * kCW) {
+    float v[kCW];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kCW; i += 4) {
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(gam + c + i));
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bet + c + i));
+      v[i] = (v[i] - mean) * inv * g4.x + b4.x;
+      v[i + 1] = (v[i + 1] - mean) * inv * g4.y + b4.y;
+      v[i + 2] = (v[i + 2] - mean) * inv * g4.z + b4.z;
+      v[i + 3] = (v[i + 3] - mean) * inv * g4.w + b4.w;
+    }
+    uint32_t packed[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
+    if (lane == 0) tma_store_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int phys = i ^ (lane & 7);
+      *reinterpret_cast<uint4*>(stg + lane * 128 + phys * 16) =
+          make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && mt < args.num_m_tiles) {
+      tma_store_2d(map_c, stg, nt * BN + c, row0);
+      tma_store_commit();
+    }
+    if constexpr ((EPI & kEpiOut2F32) != 0) {
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        if (lane == 0) tma_store_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int phys = i ^ (lane & 7);
+          *reinterpret_cast<float4*>(stg + lane * 128 + phys * 16) =
+              make_float4(v[32 * h2 + 4 * i], v[32 * h2 + 4 * i + 1], v[32 * h2 + 4 * i + 2],
+                          v[32 * h2 + 4 * i + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && mt < args.num_m_tiles) {
+          tma_store_2d(map_c2, stg, nt * BN + c + 32 * h2, row0);
+          tma_store_commit();
+        }
+      }
+    }
+  }
+}
+
+template <int BN, bool LN = false>
+struct GemmSmem;
+
+template <int BN, bool LN>
 struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kEpiBytes = 8 * 4096;  // 8 epilogue warps x (32 rows x 128 B)
+  // LN: stats[2 buffers][8 ranks][128 rows] float2 + partial[128] float2
+  static constexpr int kLnBytes = LN ? (2 * 8 * 128 + 128) * 8 : 0;
   static constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 256 /*barriers*/;
-  static constexpr int kStagesRaw = (kBudget - kEpiBytes) / kStageBytes;
+  static constexpr int kStagesRaw = (kBudget - kEpiBytes - kLnBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-  static constexpr int kTotal = 1024 + kStages * kStageBytes + kEpiBytes + 256;
+  static constexpr int kTotal = 1024 + kStages * kStageBytes + kEpiBytes + kLnBytes + 256;
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                  : 2 * BN <= 256 ? 256 : 512;
 };
@@ -79,15 +310,13 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
-                        const __grid_constant__ CUtensorMap map_c, const GemmArgs args) {
-  using L = GemmSmem<BN>;
+                        const __grid_constant__ CUtensorMap map_c,
+                        const __grid_constant__ CUtensorMap map_c2, const GemmArgs args) {
+  constexpr bool kLN = (EPI & kEpiLN) != 0;
+  using L = GemmSmem<BN, kLN>;
   constexpr int kStages = L::kStages;
   static_assert(kStages >= 2, "smem budget too small");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
-  constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
-  constexpr bool kBf16 = (EPI & kEpiBf16) != 0;  // 16-bit tensors are bf16 (else fp16)
-  constexpr int kCW = kOutF32 ? 32 : 64;  // output columns per 128-byte staging row
-  static_assert(BN % kCW == 0, "BN must be a multiple of the store chunk");
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -95,17 +324,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * L::kABytes;
   uint8_t* sEpi = smem + kStages * L::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes);
+  float2* ln_stats = reinterpret_cast<float2*>(sEpi + L::kEpiBytes);      // kLN only
+  float2* ln_partial = ln_stats + 2 * 8 * 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes + L::kLnBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tfull = bars + 2 * kStages;
   uint64_t* tempty = bars + 2 * kStages + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* stats_bar = bars + 2 * kStages + 4;  // kLN: [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int num_tiles = args.num_m_tiles * args.num_n_tiles;
   const int num_kb = args.K / kBlockK;
+  // tile schedule: persistent grid-stride, or (kLN) one cluster per M tile with
+  // CTA rank r owning N tile r, so each cluster covers whole rows
+  uint32_t cs = 1, crank = 0;
+  int t_first = blockIdx.x, t_step = gridDim.x;
+  if constexpr (kLN) {
+    cs = cluster_nctarank();
+    crank = cluster_ctarank();
+    t_first = static_cast<int>(cluster_id_x()) * args.num_n_tiles + static_cast<int>(crank);
+    t_step = static_cast<int>(ncluster_x()) * args.num_n_tiles;
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -118,12 +360,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8);
+      if constexpr (kLN) mbar_init(&stats_bar[s], 4 * 32 * cs);
     }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kLN) {
+    cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -133,7 +380,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_a = policy_evict_first();
       const uint64_t pol_b = policy_evict_last();
       uint32_t stage = 0, phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = t_first; t < num_tiles; t += t_step) {
         const int mt = t / args.num_n_tiles;
         const int nt = t - mt * args.num_n_tiles;
         const int grp = args.tile_slot ? __ldg(&args.tile_slot[mt]) : 0;
@@ -152,7 +399,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = t_first; t < num_tiles; t += t_step) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -176,79 +423,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    // 8 warps: warp w reads TMEM lane quarter (w % 4) and every other kCW-column chunk
-    // (half = (w - 2) / 4), so two warps share each quarter.
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = static_cast<int>(warp - 2) >> 2;
     uint8_t* stg = sEpi + (warp - 2) * 4096;
-    uint32_t acc = 0, acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    uint32_t acc = 0, acc_phase = 0, iter = 0;
+    for (int t = t_first; t < num_tiles; t += t_step, ++iter) {
       const int mt = t / args.num_n_tiles;
       const int nt = t - mt * args.num_n_tiles;
       const int grp = args.tile_slot ? __ldg(&args.tile_slot[mt]) : 0;
-      const float* bias = args.bias + grp * args.bias_slot_stride + nt * BN;
-      const int row0 = mt * kBlockM + q * 32;
-      const int row = row0 + lane;
-      const bool row_ok = row < args.M;
-
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((q * 32) << 16) + acc * BN;
-
-#pragma unroll 1
-      for (int c = half * kCW; c < BN; c += 2 * kCW) {
-        float v[kCW];
-#pragma unroll
-        for (int j = 0; j < kCW / 32; ++j) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < kCW; i += 4) {
-          const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
-          v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
-        }
-        if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
-          if (row_ok) {
-            const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
-            add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off);
-            if constexpr ((EPI & kEpiRes2) != 0) {
-              add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off);
-            }
-          }
-        }
-        if constexpr ((EPI & kEpiRelu) != 0) {
-#pragma unroll
-          for (int i = 0; i < kCW; ++i) v[i] = fmaxf(v[i], 0.0f);
-        }
-        // pack one 128-byte row per thread
-        uint32_t packed[32];
-        if constexpr (kOutF32) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) packed[i] = __float_as_uint(v[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
-        }
-        // staging buffer reuse: this warp's previous TMA store must have read it
-        if (lane == 0) tma_store_wait_read<0>();
-        __syncwarp();
-        uint8_t* buf = stg;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int phys = i ^ (lane & 7);  // SWIZZLE_128B: 16 B chunk ^= row % 8
-          *reinterpret_cast<uint4*>(buf + lane * 128 + phys * 16) =
-              make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&map_c, buf, nt * BN + c, row0);
-          tma_store_commit();
-        }
+      if constexpr (kLN) {
+        epilogue_tile_ln<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, &map_c2, stg,
+                                  q, half, lane, ln_partial, ln_stats, stats_bar, iter, cs, crank);
+      } else {
+        epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, stg, q, half,
+                               lane);
       }
       // all TMEM reads of this accumulator by this warp are done: hand it back
       tc_fence_before();
@@ -262,10 +452,168 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kLN) {
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<L::kTmemCols>(tmem_base);
+  }
+}
+
+// ===========================================================================
+// cta_group::2 variant for the shared-weight GEMMs: a CTA pair (cluster of 2)
+// computes a 256 x BN tile with UMMA M = 256. Each CTA TMA-loads its own 128
+// rows of A and half (BN/2 rows) of the B tile into its own smem, crediting the
+// leader's (rank 0) full barrier; the leader's single MMA thread issues
+// tcgen05.mma.cta_group::2 reading A and B from both CTAs, so per SM the smem
+// operand traffic per MMA is A/2 + B/2 of the 1-CTA kernel's. Commits multicast
+// to both CTAs' empty / tmem-full barriers; both CTAs' epilogues drain their
+// own 128 TMEM lanes and arrive on the leader's tmem-empty barrier.
+// ===========================================================================
+template <int BN>
+struct Gemm2Smem {
+  static constexpr int kABytes = kBlockM * kBlockK * 2;          // this CTA's 128 rows of A
+  static constexpr int kBBytes = (BN / 2) * kBlockK * 2;         // this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kEpiBytes = 8 * 4096;
+  static constexpr int kBudget = 227 * 1024 - 1024 - 256;
+  static constexpr int kStagesRaw = (kBudget - kEpiBytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kTotal = 1024 + kStages * kStageBytes + kEpiBytes + 256;
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+};
+
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm2_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
+                         const __grid_constant__ CUtensorMap map_b,
+                         const __grid_constant__ CUtensorMap map_c,
+                         const __grid_constant__ CUtensorMap map_c2, const GemmArgs args) {
+  using L = Gemm2Smem<BN>;
+  constexpr int kStages = L::kStages;
+  static_assert(kStages >= 3, "smem budget too small");
+  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "BN");
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * L::kABytes;
+  uint8_t* sEpi = smem + kStages * L::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* tempty = bars + 2 * kStages + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int n_pairs = (args.num_m_tiles + 1) / 2;
+  const int num_units = n_pairs * args.num_n_tiles;
+  const int cluster = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+  const int num_kb = args.K / kBlockK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    tma_prefetch_desc(&map_c);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 16);  // 8 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_2cta<L::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_first();
+      const uint64_t pol_b = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      for (int u = cluster; u < num_units; u += n_clusters) {
+        const int mp = u / args.num_n_tiles;
+        const int nt = u - mp * args.num_n_tiles;
+        const int mt = 2 * mp + static_cast<int>(rank);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
+          const uint32_t leader_full = mapa_shared(smem_u32(&full[stage]), 0);
+          tma_load_2d_2sm(sA + stage * L::kABytes, &map_a, leader_full, kb * kBlockK,
+                          mt * kBlockM, pol_a);
+          tma_load_3d_2sm(sB + stage * L::kBBytes, &map_b, leader_full, kb * kBlockK,
+                          nt * BN + static_cast<int>(rank) * (BN / 2), 0, pol_b);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (rank == 0 && lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int u = cluster; u < num_units; u += n_clusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a_desc = sdesc_k_sw128(smem_u32(sA + stage * L::kABytes));
+          const uint64_t b_desc = sdesc_k_sw128(smem_u32(sB + stage * L::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kBlockK / 16; ++k) {
+            umma_f16_2cta(d_tmem, a_desc + 2 * k, b_desc + 2 * k, args.idesc, (kb | k) != 0);
+          }
+          umma_commit_2cta_mc(&empty[stage], 0x3);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2cta_mc(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint32_t q = warp & 3;
+    const int half = static_cast<int>(warp - 2) >> 2;
+    uint8_t* stg = sEpi + (warp - 2) * 4096;
+    uint32_t acc = 0, acc_phase = 0;
+    for (int u = cluster; u < num_units; u += n_clusters) {
+      const int mp = u / args.num_n_tiles;
+      const int nt = u - mp * args.num_n_tiles;
+      const int mt = 2 * mp + static_cast<int>(rank);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, 0, args, &map_c, stg, q, half, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2cta<L::kTmemCols>(tmem_base);
   }
 }
 

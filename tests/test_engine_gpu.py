@@ -108,6 +108,21 @@ def test_c1_swap_small_pool_bit_identical(c1):
     w.eng.close()
 
 
+def test_fused_ln_matches_unfused(c1, monkeypatch):
+    """The LN-in-epilogue GEMMs (cluster row reduction) agree with the separate
+    K4 LayerNorm kernels; both meet the oracle tolerance."""
+    inst, toks, lens = c1.requests(23, 16, 128)
+    fused = c1.eng.infer_batch(inst, toks, lens)
+    monkeypatch.setenv("HMI_UNFUSED_LN", "1")
+    w = World(oracle.TINY, n_tasks=16, r=16, labels=8, max_batch=32)
+    unfused = w.eng.infer_batch(inst, toks, lens)
+    w.eng.close()
+    ref_scores, _, _ = c1.oracle_batch(inst, toks, lens)
+    assert logit_error(fused.scores, ref_scores) <= TOL
+    assert logit_error(unfused.scores, ref_scores) <= TOL
+    assert np.abs(fused.scores - unfused.scores).max() < 1e-2
+
+
 def test_routing_and_vocab_errors(c1):
     inst, toks, lens = c1.requests(3, 2, 16)
     bad = inst.copy()

@@ -73,6 +73,39 @@ def test_gemm_shared_bias(M, N, K, bn):
     assert err < 2e-3, err
 
 
+@pytest.mark.parametrize("M,N,K,bn,epi", [(256, 256, 64, 256, 0), (384, 768, 768, 192, 0),
+                                           (1024, 2304, 768, 256, 1), (512, 768, 3072, 192, 2 | 8),
+                                           (640, 3072, 768, 256, 1), (256, 128, 128, 128, 8)])
+def test_gemm_cta_pair(M, N, K, bn, epi):
+    """cta_group::2 kernel (UMMA M=256 over a CTA pair, B split across the pair);
+    odd M-tile counts exercise the idle half of the last pair."""
+    rng = np.random.default_rng(M * 7 + N)
+    a = rng.standard_normal((M, K)).astype(np.float16)
+    b = rng.uniform(-0.05, 0.05, (1, N, K)).astype(np.float16)
+    bias = rng.uniform(-0.05, 0.05, (1, N)).astype(np.float32)
+    r0 = rng.standard_normal((M, N)).astype(np.float16) if epi & 2 else None
+    out, _ = _probe(a, b, bias, res0=r0, epi=epi | 256, bn=bn)
+    ref = _ref(a, b, bias, None, r0, relu=bool(epi & 1))
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err < 2e-3, err
+
+
+def test_gemm_cta_pair_throughput():
+    rng = np.random.default_rng(6)
+    res = {}
+    for name, (M, N, K, bn) in {"qkv": (32768, 2304, 768, 256), "ffn1": (32768, 3072, 768, 256),
+                                "ffn2": (32768, 768, 3072, 192)}.items():
+        a = rng.standard_normal((M, K)).astype(np.float16)
+        b = rng.uniform(-0.05, 0.05, (1, N, K)).astype(np.float16)
+        bias = np.zeros((1, N), np.float32)
+        _, ms1 = _probe(a, b, bias, bn=bn)
+        out, ms2 = _probe(a, b, bias, bn=bn, epi=256)
+        res[name] = (2.0 * M * N * K / (ms1 * 1e-3) / 1e12, 2.0 * M * N * K / (ms2 * 1e-3) / 1e12)
+        ref = a[:256].astype(np.float64) @ b[0].astype(np.float64).T
+        assert np.abs(out[:256] - ref).max() / np.abs(ref).max() < 2e-3
+    print("TFLOP/s 1-CTA vs 2-CTA:", {k: (round(x), round(y)) for k, (x, y) in res.items()})
+
+
 def test_gemm_relu_f16():
     rng = np.random.default_rng(1)
     M, N, K = 512, 3072, 768
