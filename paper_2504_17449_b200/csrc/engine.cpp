@@ -136,20 +136,21 @@ int pick_bn(int N, int m_tiles, int sms, bool pair = false) {
   return best;
 }
 
-// N tile of an LN-fused GEMM: one cluster of N / bn CTAs per 128-row tile; choose the
-// cluster width with the best occupancy x wave efficiency.
-int pick_bn_ln(int N, int m_tiles, int sms) {
-  int best = -1;
-  double best_eff = -1;
+// LN-fused GEMM plan: one cluster of N / bn CTAs per 128-row tile. Per-tile time scales
+// with bn and the number of rounds with ceil(m_tiles / co-resident clusters); pick the
+// N tile minimising rounds x bn.
+GemmPlan best_ln_plan(GemmSpec s, int m_tiles) {
+  GemmPlan best;
+  long best_cost = -1;
   for (int bn : {256, 192, 128, 64}) {
-    if (N % bn || N / bn > 8) continue;
-    const int cs = N / bn;
-    const int clusters = sms / cs;
-    const long rounds = (m_tiles + clusters - 1) / clusters;
-    const double eff = static_cast<double>(m_tiles) * cs / (static_cast<double>(rounds) * sms);
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = bn;
+    if (s.N % bn || s.N / bn > 8) continue;
+    s.bn = bn;
+    GemmPlan p = make_gemm_plan(s);
+    const long rounds = (m_tiles + p.max_clusters - 1) / p.max_clusters;
+    const long cost = rounds * bn;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = p;
     }
   }
   return best;
@@ -419,20 +420,20 @@ void Ctx::build_plans() {
       u.bias_group_stride = static_cast<long long>(slot_bytes / 4);
       u.tile_slot = d_tile_slot.p + static_cast<size_t>(l) * tile_stride;
       u.res0 = a16.p; u.res1 = h16.p; u.res_ld = d;
-      u.c = x16.p; u.c_ld = d; u.epi = kEpiRes2 | kEpiLN; u.bn = pick_bn_ln(d, m_tiles, sms);
+      u.c = x16.p; u.c_ld = d; u.epi = kEpiRes2 | kEpiLN;
       u.ln_gamma = w.ln1g; u.ln_beta = w.ln1b;
-      w.ad_up_ln = make_gemm_plan(u);
+      w.ad_up_ln = best_ln_plan(u, m_tiles);
       GemmSpec g;
       g.precision = prec;
       g.a_rows = max_rows;
       g.a = ffn16.p; g.a_ld = f; g.K = f;
       g.b = w.w2; g.N = d; g.groups = 1; g.b_ld = f; g.b_group_stride_bytes = size_t(d) * f * 2;
       g.bias = w.b2; g.res0 = x16.p; g.res_ld = d;
-      g.c = h16.p; g.c_ld = d; g.bn = pick_bn_ln(d, m_tiles, sms);
+      g.c = h16.p; g.c_ld = d;
       g.epi = kEpiRes1 | kEpiLN | (l == L - 1 ? kEpiOut2F32 : 0);
       g.c2 = h32.p; g.c2_ld = d;
       g.ln_gamma = w.ln2g; g.ln_beta = w.ln2b;
-      w.ffn2_ln = make_gemm_plan(g);
+      w.ffn2_ln = best_ln_plan(g, m_tiles);
     }
   }
 }

@@ -134,6 +134,31 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.ln_beta = s.ln_beta;
   p.args.idesc = idesc_f16(c2 ? 2 * kBlockM : kBlockM, s.bn, s.precision == 1 ? 1u : 0u);
   p.max_rows = s.a_rows;
+  if (ln) {
+    // how many clusters of cluster_n CTAs (each ~210 KB smem) fit at once: GPCs do not
+    // divide evenly, so asking for sms / cluster_n would leave a second wave
+    HMI_CUDA(cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes));
+    if (p.cluster_n > 1) {
+      HMI_CUDA(cudaFuncSetAttribute(p.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.cluster_n * (device_sm_count() / p.cluster_n));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.cluster_n;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, p.fn, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = device_sm_count() / p.cluster_n;
+    }
+    p.max_clusters = n;
+  }
   return p;
 }
 
@@ -160,7 +185,7 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
   if (p.cluster_n > 1 || (p.args.ln_gamma && p.cluster_n == 1)) {
     // LN epilogue: one cluster of cluster_n CTAs per M tile
     const int per = p.cluster_n;
-    const int clusters_max = device_sm_count() / per;
+    const int clusters_max = p.max_clusters > 0 ? p.max_clusters : device_sm_count() / per;
     const int clusters = a.num_m_tiles < clusters_max ? a.num_m_tiles : clusters_max;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * per);

@@ -66,7 +66,8 @@ struct GemmPlan {
   int smem_bytes = 0;
   int max_rows = 0;
   bool two_cta = false;
-  int cluster_n = 1;  // kEpiLN: CTAs per cluster along N (= N / BN)
+  int cluster_n = 1;     // kEpiLN: CTAs per cluster along N (= N / BN)
+  int max_clusters = 0;  // kEpiLN: co-resident clusters (cudaOccupancyMaxActiveClusters)
 };
 
 GemmPlan make_gemm_plan(const GemmSpec& s);

@@ -156,45 +156,46 @@ __device__ __forceinline__ void epilogue_tile_ln(uint32_t t_acc, int mt, int nt,
   const int row = row0 + static_cast<int>(lane);
   const bool row_ok = row < args.M;
   const uint32_t t_row = t_acc + ((q * 32) << 16);
-  // ---- pass 1
+  // ---- pass 1 (32-column chunks, alternating between the two warps of a lane quarter)
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
-  for (int c = half * kCW; c < BN; c += 2 * kCW) {
-    float v[kCW];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < kCW; i += 4) {
-      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
-      v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
-    }
+  for (int c = half * 32; c < BN; c += 64) {
+    float v[32];
+    float rv[32];
     if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
+      // issue the residual loads before touching TMEM
+#pragma unroll
+      for (int i = 0; i < 32; ++i) rv[i] = 0.f;
       if (row_ok) {
         const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
-        add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off);
+        add_res16<kBf16, 32>(rv, reinterpret_cast<const uint16_t*>(args.res0) + off);
         if constexpr ((EPI & kEpiRes2) != 0) {
-          add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off);
+          add_res16<kBf16, 32>(rv, reinterpret_cast<const uint16_t*>(args.res1) + off);
         }
       }
     }
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(t_row + c, r);
+    tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < kCW; ++i) {
+    for (int i = 0; i < 32; i += 4) {
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
+      v[i] = __uint_as_float(r[i]) + b4.x;
+      v[i + 1] = __uint_as_float(r[i + 1]) + b4.y;
+      v[i + 2] = __uint_as_float(r[i + 2]) + b4.z;
+      v[i + 3] = __uint_as_float(r[i + 3]) + b4.w;
+    }
+    if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += rv[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
       s1 += v[i];
       s2 += v[i] * v[i];
+      r[i] = __float_as_uint(v[i]);
     }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      uint32_t r[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[32 * j + i]);
-      tmem_st_32x32b_x32(t_row + c + 32 * j, r);
-    }
+    tmem_st_32x32b_x32(t_row + c, r);
   }
   tmem_st_wait();
   // ---- row statistics: halves -> CTA -> cluster
