@@ -170,6 +170,7 @@ struct Ctx {
   std::mutex mu;
 
   std::vector<LayerDev> layers;
+  AttnPlan attn;
   // activations
   DevBuf<uint16_t> h16, qkv16, ctx16, a16, mid16, x16, ffn16;
   DevBuf<float> y32, h32;
@@ -352,6 +353,7 @@ void Ctx::convert_adapter(const float* src, uint8_t* dst) const {
 }
 
 void Ctx::build_plans() {
+  attn = make_attention_plan(qkv16.p, ctx16.p, max_rows, d, static_cast<int>(opt.precision));
   const int sms = device_sm_count();
   const int m_tiles = max_rows / 128;
   const int prec = static_cast<int>(opt.precision);
@@ -648,7 +650,12 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     const bool last = l == L - 1;
     timed(P_QKV, s, [&] { launch_gemm(w.qkv, rows, s); });
     timed(P_ATTN, s, [&] {
-      launch_attention(qkv16.p, ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal, prec, s);
+      if (S == 128) {
+        launch_attention_s128(attn, d_lens.p, static_cast<int>(n_req), heads, causal, s);
+      } else {
+        launch_attention(qkv16.p, ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal,
+                         prec, s);
+      }
     });
     timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
     if (fine) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));

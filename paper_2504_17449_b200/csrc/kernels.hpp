@@ -55,6 +55,16 @@ void launch_route(const uint32_t* instance_idx, int n_req, const int32_t* inst_v
                   int32_t* req_version, int32_t* req_task, int32_t* req_head,
                   int32_t* tile_slot, int32_t* err, cudaStream_t stream);
 
+// K3 fast path for padded length 128: persistent, TMA double-buffered (request, head) items.
+struct AttnPlan {
+  CUtensorMap map_qkv, map_ctx;
+  int d = 0;
+  int precision = 0;
+};
+AttnPlan make_attention_plan(const void* qkv, void* ctx, int max_rows, int d, int precision);
+void launch_attention_s128(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
+                           cudaStream_t stream);
+
 // K3: attention core.
 void launch_attention(const void* qkv, void* ctx, const int* lens, int n_req, int S, int d,
                       int heads, int causal, int precision, cudaStream_t stream);

@@ -137,6 +137,21 @@ def test_routing_and_vocab_errors(c1):
     c1.eng.infer_batch(inst, toks, lens)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_long_requests_s256(mode):
+    """Padded length 256 (two 128-row tiles per request) takes the general attention
+    kernel (online softmax over 64-key blocks) and multi-tile adapter routing."""
+    cfg = oracle.Config(256, 4, 2, 2, 1024, 1024, mode, 3, 13)
+    w = World(cfg, n_tasks=4, r=16, labels=8, max_batch=6, max_seq=256,
+              head_kind=E.HEAD_LM if mode else E.HEAD_CLS)
+    inst, toks, lens = w.requests(29, 6, 240, min_len=130)
+    res = w.eng.infer_batch(inst, toks, lens)
+    ref_scores, ref_labels, _ = w.oracle_batch(inst, toks, lens)
+    assert logit_error(res.scores, ref_scores) <= TOL
+    assert (res.labels == ref_labels).mean() >= 0.999
+    w.eng.close()
+
+
 def test_token_tag_head():
     w = World(oracle.TINY, n_tasks=4, r=16, labels=5, head_kind=E.HEAD_TAG, max_batch=8)
     inst, toks, lens = w.requests(5, 6, 40, min_len=3)
