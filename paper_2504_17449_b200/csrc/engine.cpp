@@ -145,7 +145,12 @@ GemmPlan best_ln_plan(GemmSpec s, int m_tiles) {
   for (int bn : {256, 192, 128, 64}) {
     if (s.N % bn || s.N / bn > 8) continue;
     s.bn = bn;
-    GemmPlan p = make_gemm_plan(s);
+    GemmPlan p;
+    try {
+      p = make_gemm_plan(s);
+    } catch (const HmiError&) {
+      continue;  // no kernel instance for this tile width (e.g. smem budget)
+    }
     const long rounds = (m_tiles + p.max_clusters - 1) / p.max_clusters;
     const long cost = rounds * bn;
     if (best_cost < 0 || cost < best_cost) {
@@ -153,6 +158,7 @@ GemmPlan best_ln_plan(GemmSpec s, int m_tiles) {
       best = p;
     }
   }
+  HMI_CHECK(best_cost >= 0, HMI_CONFIG_ERROR, "no LayerNorm-fused GEMM fits this hidden size");
   return best;
 }
 
@@ -422,7 +428,7 @@ void Ctx::build_plans() {
       u.bias_group_stride = static_cast<long long>(slot_bytes / 4);
       u.tile_slot = d_tile_slot.p + static_cast<size_t>(l) * tile_stride;
       u.res0 = a16.p; u.res1 = h16.p; u.res_ld = d;
-      u.c = x16.p; u.c_ld = d; u.epi = kEpiRes2 | kEpiLN;
+      u.c = x16.p; u.c_ld = d; u.epi = kEpiRes2 | kEpiLN | kEpiResTma;
       u.ln_gamma = w.ln1g; u.ln_beta = w.ln1b;
       w.ad_up_ln = best_ln_plan(u, m_tiles);
       GemmSpec g;

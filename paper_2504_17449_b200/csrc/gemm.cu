@@ -13,7 +13,7 @@ namespace hmi_b200 {
 
 namespace {
 
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
+using KernelFn = void (*)(GemmMaps, GemmArgs);
 
 template <int BN, int EPI, bool C2>
 KernelFn kernel_ptr() {
@@ -44,6 +44,9 @@ KernelFn pick_epi_t(int epi) {
         return kernel_ptr<BN, T | kEpiRes1 | kEpiLN | kEpiOut2F32, false>();
       case kEpiRes2 | kEpiLN | kEpiOut2F32:
         return kernel_ptr<BN, T | kEpiRes2 | kEpiLN | kEpiOut2F32, false>();
+      case kEpiRes2 | kEpiLN | kEpiResTma:
+        if constexpr (BN <= 192) return kernel_ptr<BN, T | kEpiRes2 | kEpiLN | kEpiResTma, false>();
+        return nullptr;
       default: break;
     }
   }
@@ -66,21 +69,17 @@ KernelFn pick_kernel(int bn, int epi, bool c2, int* smem_bytes) {
     }
   }
   const bool ln = (epi & kEpiLN) != 0;
+  const bool rt = (epi & kEpiResTma) != 0;
+#define HMI_SMEM(B) (rt ? (B <= 192 ? GemmSmem<(B <= 192 ? B : 64), true, true>::kTotal : 0) \
+                     : ln ? GemmSmem<B, true>::kTotal : GemmSmem<B>::kTotal)
   switch (bn) {
-    case 64:
-      *smem_bytes = ln ? GemmSmem<64, true>::kTotal : GemmSmem<64>::kTotal;
-      return pick_epi<64, false>(epi);
-    case 128:
-      *smem_bytes = ln ? GemmSmem<128, true>::kTotal : GemmSmem<128>::kTotal;
-      return pick_epi<128, false>(epi);
-    case 192:
-      *smem_bytes = ln ? GemmSmem<192, true>::kTotal : GemmSmem<192>::kTotal;
-      return pick_epi<192, false>(epi);
-    case 256:
-      *smem_bytes = ln ? GemmSmem<256, true>::kTotal : GemmSmem<256>::kTotal;
-      return pick_epi<256, false>(epi);
+    case 64: *smem_bytes = HMI_SMEM(64); return pick_epi<64, false>(epi);
+    case 128: *smem_bytes = HMI_SMEM(128); return pick_epi<128, false>(epi);
+    case 192: *smem_bytes = HMI_SMEM(192); return pick_epi<192, false>(epi);
+    case 256: *smem_bytes = HMI_SMEM(256); return pick_epi<256, false>(epi);
     default: return nullptr;
   }
+#undef HMI_SMEM
 }
 
 }  // namespace
@@ -106,18 +105,27 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   HMI_CHECK(p.fn != nullptr, HMI_CONFIG_ERROR, "gemm: unsupported epilogue");
   const CUtensorMapDataType t16 =
       s.precision == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  p.map_a = make_tmap_2d(s.a, t16, s.K, s.a_rows, s.a_ld * 2ull, kBlockK, kBlockM,
+  p.maps.a = make_tmap_2d(s.a, t16, s.K, s.a_rows, s.a_ld * 2ull, kBlockK, kBlockM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
-  p.map_b = make_tmap_3d(s.b, t16, s.K, s.N, s.groups, s.b_ld * 2ull, s.b_group_stride_bytes,
+  p.maps.b = make_tmap_3d(s.b, t16, s.K, s.N, s.groups, s.b_ld * 2ull, s.b_group_stride_bytes,
                          kBlockK, c2 ? s.bn / 2 : s.bn, CU_TENSOR_MAP_SWIZZLE_128B);
   const bool f32 = (s.epi & kEpiOutF32) != 0 && !ln;
-  p.map_c = make_tmap_2d(s.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : t16, s.N, s.a_rows,
+  p.maps.c = make_tmap_2d(s.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : t16, s.N, s.a_rows,
                          s.c_ld * (f32 ? 4ull : 2ull), f32 ? 32 : 64, 32,
                          CU_TENSOR_MAP_SWIZZLE_128B);
-  p.map_c2 = p.map_c;
+  p.maps.c2 = p.maps.c;
+  p.maps.r0 = p.maps.c;
+  p.maps.r1 = p.maps.c;
+  if (s.epi & kEpiResTma) {
+    HMI_CHECK(ln && s.res0 && s.res1, HMI_CONFIG_ERROR, "gemm: TMA residuals need LN + 2 residuals");
+    p.maps.r0 = make_tmap_2d(s.res0, t16, s.N, s.a_rows, s.res_ld * 2ull, 64, 128,
+                             CU_TENSOR_MAP_SWIZZLE_128B);
+    p.maps.r1 = make_tmap_2d(s.res1, t16, s.N, s.a_rows, s.res_ld * 2ull, 64, 128,
+                             CU_TENSOR_MAP_SWIZZLE_128B);
+  }
   if (s.epi & kEpiOut2F32) {
     HMI_CHECK(s.c2 != nullptr, HMI_CONFIG_ERROR, "gemm: f32 copy output missing");
-    p.map_c2 = make_tmap_2d(s.c2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, s.N, s.a_rows, s.c2_ld * 4ull,
+    p.maps.c2 = make_tmap_2d(s.c2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, s.N, s.a_rows, s.c2_ld * 4ull,
                             32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   p.args = GemmArgs{};
@@ -200,7 +208,7 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     KernelFn fn = reinterpret_cast<KernelFn>(p.fn);
-    HMI_CUDA(cudaLaunchKernelEx(&cfg, fn, p.map_a, p.map_b, p.map_c, p.map_c2, a));
+    HMI_CUDA(cudaLaunchKernelEx(&cfg, fn, p.maps, a));
     return;
   }
   if (p.two_cta) {
@@ -212,7 +220,7 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
     grid = tiles < device_sm_count() ? tiles : device_sm_count();
   }
   KernelFn fn = reinterpret_cast<KernelFn>(p.fn);
-  fn<<<grid, kGemmThreads, p.smem_bytes, stream>>>(p.map_a, p.map_b, p.map_c, p.map_c2, a);
+  fn<<<grid, kGemmThreads, p.smem_bytes, stream>>>(p.maps, a);
   HMI_CUDA(cudaGetLastError());
 }
 

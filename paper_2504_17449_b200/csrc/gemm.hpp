@@ -33,6 +33,12 @@ constexpr int kEpiOutF32 = 8;
 constexpr int kEpiBf16 = 16;  // 16-bit outputs / residuals are bf16 (set from precision)
 constexpr int kEpiLN = 32;    // LayerNorm over the row (cluster of N/BN CTAs), 16-bit output
 constexpr int kEpiOut2F32 = 64;  // with kEpiLN: also write an f32 copy through map_c2
+constexpr int kEpiResTma = 128;  // with kEpiLN: residual tiles TMA-prefetched into smem
+
+// All tensor maps of one GEMM (passed as one __grid_constant__ kernel parameter).
+struct GemmMaps {
+  CUtensorMap a, b, c, c2, r0, r1;
+};
 
 // Everything needed to bind one GEMM to fixed device buffers.
 struct GemmSpec {
@@ -60,7 +66,7 @@ struct GemmSpec {
 };
 
 struct GemmPlan {
-  CUtensorMap map_a, map_b, map_c, map_c2;
+  GemmMaps maps;
   GemmArgs args;
   void* fn = nullptr;
   int smem_bytes = 0;

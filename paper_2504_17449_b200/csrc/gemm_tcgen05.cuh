@@ -40,6 +40,28 @@ __device__ __forceinline__ uint32_t pack_16x2(float a, float b) {
   }
 }
 
+// v[0..32) += 32 16-bit residuals of one row of a SWIZZLE_128B smem box, starting at
+// 16-byte chunk ch0 of the row (row base `rowp`, rsw = row % 8)
+template <bool kBf16>
+__device__ __forceinline__ void add_res16_smem(float* v, const uint8_t* rowp, int ch0, int rsw) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 u = *reinterpret_cast<const uint4*>(rowp + (((ch0 + k) ^ rsw) << 4));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f;
+      if constexpr (kBf16) {
+        f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      } else {
+        f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+      }
+      v[8 * k + 2 * e] += f.x;
+      v[8 * k + 2 * e + 1] += f.y;
+    }
+  }
+}
+
 // v[0..N) += 16-bit residual row segment (16-byte vector loads)
 template <bool kBf16, int N>
 __device__ __forceinline__ void add_res16(float* v, const uint16_t* src) {
@@ -146,8 +168,10 @@ __device__ __forceinline__ void epilogue_tile_ln(uint32_t t_acc, int mt, int nt,
                                                  uint32_t q, int half, uint32_t lane,
                                                  float2* partial, float2* stats,
                                                  uint64_t* stats_bar, uint32_t iter,
-                                                 uint32_t cs, uint32_t rank) {
+                                                 uint32_t cs, uint32_t rank,
+                                                 const uint8_t* res_smem, uint64_t* res_empty) {
   constexpr bool kBf16 = (EPI & kEpiBf16) != 0;
+  constexpr bool kResTma = (EPI & kEpiResTma) != 0;
   constexpr int kCW = 64;
   static_assert(BN % kCW == 0, "LN epilogue works in 64-column chunks");
   const float* bias = args.bias + grp * args.bias_slot_stride + nt * BN;
@@ -166,7 +190,15 @@ __device__ __forceinline__ void epilogue_tile_ln(uint32_t t_acc, int mt, int nt,
       // issue the residual loads before touching TMEM
 #pragma unroll
       for (int i = 0; i < 32; ++i) rv[i] = 0.f;
-      if (row_ok) {
+      if constexpr (kResTma) {
+        // residual tiles staged by TMA: [res][BN/64 boxes][128 rows x 128 B], SWIZZLE_128B
+        const uint8_t* box = res_smem + (c >> 6) * 16384 + row_local * 128;
+        const int ch0 = (c & 63) >> 3;
+        add_res16_smem<kBf16>(rv, box, ch0, row_local & 7);
+        if constexpr ((EPI & kEpiRes2) != 0) {
+          add_res16_smem<kBf16>(rv, box + (BN / 64) * 16384, ch0, row_local & 7);
+        }
+      } else if (row_ok) {
         const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
         add_res16<kBf16, 32>(rv, reinterpret_cast<const uint16_t*>(args.res0) + off);
         if constexpr ((EPI & kEpiRes2) != 0) {
@@ -198,6 +230,10 @@ __device__ __forceinline__ void epilogue_tile_ln(uint32_t t_acc, int mt, int nt,
     tmem_st_32x32b_x32(t_row + c, r);
   }
   tmem_st_wait();
+  if constexpr (kResTma) {  // residual tiles consumed: the producer may stage the next tile's
+    __syncwarp();
+    if (lane == 0) mbar_arrive(res_empty);
+  }
   // ---- row statistics: halves -> CTA -> cluster
   if (half == 1) partial[row_local] = make_float2(s1, s2);
   named_bar_sync(1, 256);
@@ -288,10 +324,10 @@ __device__ __forceinline__ void epilogue_tile_ln(uint32_t t_acc, int mt, int nt,
   }
 }
 
-template <int BN, bool LN = false>
+template <int BN, bool LN = false, bool RT = false>
 struct GemmSmem;
 
-template <int BN, bool LN>
+template <int BN, bool LN, bool RT>
 struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
   static constexpr int kBBytes = BN * kBlockK * 2;
@@ -299,22 +335,28 @@ struct GemmSmem {
   static constexpr int kEpiBytes = 8 * 4096;  // 8 epilogue warps x (32 rows x 128 B)
   // LN: stats[2 buffers][8 ranks][128 rows] float2 + partial[128] float2
   static constexpr int kLnBytes = LN ? (2 * 8 * 128 + 128) * 8 : 0;
+  // RT: two residual tiles of 128 rows x BN (BN/64 SWIZZLE_128B boxes of 16 KB each)
+  static constexpr int kResBytes = RT ? 2 * (BN / 64) * 16384 : 0;
   static constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 256 /*barriers*/;
-  static constexpr int kStagesRaw = (kBudget - kEpiBytes - kLnBytes) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-  static constexpr int kTotal = 1024 + kStages * kStageBytes + kEpiBytes + kLnBytes + 256;
+  static constexpr int kStagesRaw = (kBudget - kEpiBytes - kLnBytes - kResBytes) / kStageBytes;
+  static constexpr int kStagesCap = RT ? 2 : 6;  // RT GEMMs have a single K block (K = r)
+  static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
+  static constexpr int kTotal =
+      1024 + kStages * kStageBytes + kEpiBytes + kLnBytes + kResBytes + 256;
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                  : 2 * BN <= 256 ? 256 : 512;
 };
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b,
-                        const __grid_constant__ CUtensorMap map_c,
-                        const __grid_constant__ CUtensorMap map_c2, const GemmArgs args) {
+    gemm_tcgen05_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args) {
+  const CUtensorMap& map_a = maps.a;
+  const CUtensorMap& map_b = maps.b;
+  const CUtensorMap& map_c = maps.c;
+  const CUtensorMap& map_c2 = maps.c2;
   constexpr bool kLN = (EPI & kEpiLN) != 0;
-  using L = GemmSmem<BN, kLN>;
+  constexpr bool kRT = (EPI & kEpiResTma) != 0;
+  using L = GemmSmem<BN, kLN, kRT>;
   constexpr int kStages = L::kStages;
   static_assert(kStages >= 2, "smem budget too small");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
@@ -327,13 +369,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sEpi = smem + kStages * L::kStageBytes;
   float2* ln_stats = reinterpret_cast<float2*>(sEpi + L::kEpiBytes);      // kLN only
   float2* ln_partial = ln_stats + 2 * 8 * 128;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes + L::kLnBytes);
+  uint8_t* sRes = sEpi + L::kEpiBytes + L::kLnBytes;                       // kRT only
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRes + L::kResBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tfull = bars + 2 * kStages;
   uint64_t* tempty = bars + 2 * kStages + 2;
   uint64_t* stats_bar = bars + 2 * kStages + 4;  // kLN: [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
+  uint64_t* res_full = bars + 2 * kStages + 6;   // kRT
+  uint64_t* res_empty = bars + 2 * kStages + 7;  // kRT
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -363,6 +408,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tempty[s], 8);
       if constexpr (kLN) mbar_init(&stats_bar[s], 4 * 32 * cs);
     }
+    if constexpr (kRT) {
+      mbar_init(res_full, 1);
+      mbar_init(res_empty, 8);
+      tma_prefetch_desc(&maps.r0);
+      tma_prefetch_desc(&maps.r1);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -380,11 +431,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_first();
       const uint64_t pol_b = policy_evict_last();
-      uint32_t stage = 0, phase = 0;
+      uint32_t stage = 0, phase = 0, res_phase = 0;
       for (int t = t_first; t < num_tiles; t += t_step) {
         const int mt = t / args.num_n_tiles;
         const int nt = t - mt * args.num_n_tiles;
         const int grp = args.tile_slot ? __ldg(&args.tile_slot[mt]) : 0;
+        if constexpr (kRT) {
+          // residual tiles for this tile's epilogue (single buffer, released after pass 1)
+          mbar_wait(res_empty, res_phase ^ 1);
+          constexpr int nbox = BN / 64;
+          mbar_arrive_expect_tx(res_full, 2 * nbox * 16384);
+          for (int j = 0; j < nbox; ++j) {
+            tma_load_2d(sRes + j * 16384, &maps.r0, res_full, nt * BN + j * 64, mt * kBlockM);
+            tma_load_2d(sRes + (nbox + j) * 16384, &maps.r1, res_full, nt * BN + j * 64,
+                        mt * kBlockM);
+          }
+          res_phase ^= 1;
+        }
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
@@ -435,8 +498,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if constexpr (kLN) {
+        if constexpr (kRT) mbar_wait(res_full, iter & 1);
         epilogue_tile_ln<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, &map_c2, stg,
-                                  q, half, lane, ln_partial, ln_stats, stats_bar, iter, cs, crank);
+                                  q, half, lane, ln_partial, ln_stats, stats_bar, iter, cs, crank,
+                                  kRT ? sRes : nullptr, kRT ? res_empty : nullptr);
       } else {
         epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, stg, q, half,
                                lane);
@@ -489,10 +554,10 @@ struct Gemm2Smem {
 
 template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    gemm2_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
-                         const __grid_constant__ CUtensorMap map_b,
-                         const __grid_constant__ CUtensorMap map_c,
-                         const __grid_constant__ CUtensorMap map_c2, const GemmArgs args) {
+    gemm2_tcgen05_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args) {
+  const CUtensorMap& map_a = maps.a;
+  const CUtensorMap& map_b = maps.b;
+  const CUtensorMap& map_c = maps.c;
   using L = Gemm2Smem<BN>;
   constexpr int kStages = L::kStages;
   static_assert(kStages >= 3, "smem budget too small");
