@@ -93,7 +93,18 @@ struct LayerDev {
   float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
   GemmPlan qkv, oproj, ad_down, ad_up, ffn1, ffn2;
   GemmPlan ad_up_ln, ffn2_ln;  // LayerNorm fused into the epilogue (cluster row reduction)
+  // LayerNorm folding (default mode): gamma folded into the consumer's weights, beta.W into
+  // its bias, and the per-column sums of the folded 16-bit weights for the mean correction
+  void* mem_fold = nullptr;
+  uint16_t *wqkv_f = nullptr, *w1_f = nullptr;   // [N][K] 16-bit
+  float *bqkv_f = nullptr, *cs_qkv = nullptr, *b1_f = nullptr, *cs_1 = nullptr;
 };
+
+// LN-fold of one consumer GEMM: W' = diag(gamma) W (rounded to 16-bit), b' = b + beta.W,
+// colsum[n] = sum_k W'[k][n] over the rounded values (what the tensor core multiplies).
+void fold_weights(const float* w, size_t in, size_t out, const float* bias, const float* gamma,
+                  const float* beta, int prec, std::vector<uint16_t>& wt,
+                  std::vector<float>& bias_f, std::vector<float>& colsum);
 
 struct Staging {
   uint32_t* inst = nullptr;
@@ -134,6 +145,33 @@ int pick_bn(int N, int m_tiles, int sms, bool pair = false) {
     }
   }
   return best;
+}
+
+void fold_weights(const float* w, size_t in, size_t out, const float* bias, const float* gamma,
+                  const float* beta, int prec, std::vector<uint16_t>& wt,
+                  std::vector<float>& bias_f, std::vector<float>& colsum) {
+  wt.assign(in * out, 0);
+  bias_f.assign(out, 0.f);
+  colsum.assign(out, 0.f);
+  for (size_t o = 0; o < out; ++o) {
+    double cs = 0.0, bb = static_cast<double>(bias[o]);
+    for (size_t i = 0; i < in; ++i) {
+      const float wv = w[i * out + o];
+      const uint16_t h = f2h(static_cast<float>(static_cast<double>(gamma[i]) * wv), prec);
+      wt[o * in + i] = h;
+      float back;
+      if (prec == 1) {
+        const uint32_t u = static_cast<uint32_t>(h) << 16;
+        std::memcpy(&back, &u, 4);
+      } else {
+        back = __half2float(*reinterpret_cast<const __half*>(&h));
+      }
+      cs += back;
+      bb += static_cast<double>(beta[i]) * wv;
+    }
+    colsum[o] = static_cast<float>(cs);
+    bias_f[o] = static_cast<float>(bb);
+  }
 }
 
 // LN-fused GEMM plan: one cluster of N / bn CTAs per 128-row tile. Per-tile time scales
@@ -223,7 +261,12 @@ struct Ctx {
   // last batch (introspection)
   uint32_t last_n = 0, last_S = 0;
   uint32_t debug_flags = 0;
-  bool fused_ln = true;  // HMI_UNFUSED_LN=1 selects the separate K4 LayerNorm kernels
+  // LayerNorm placement: 0 folded into the consumers (default), 1 separate K4 kernels
+  // (HMI_LN_MODE=unfused), 2 cluster-reduced GEMM epilogues (HMI_LN_MODE=cluster)
+  int ln_mode = 0;
+  DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
+  static constexpr int kStatsLd = 16;
+  int stats1_bn = 0, stats2_bn = 0, stats1_n = 0, stats2_n = 0;
   // profiling
   bool prof = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -303,8 +346,12 @@ struct Ctx {
 Ctx::~Ctx() {
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  for (auto& l : layers)
+  for (auto& l : layers) {
     if (l.mem) cudaFree(l.mem);
+    if (l.mem_fold) cudaFree(l.mem_fold);
+  }
+  d_stats1.free();
+  d_stats2.free();
   for (auto& s : stg) {
     for (void* p : {static_cast<void*>(s.inst), static_cast<void*>(s.tokens),
                     static_cast<void*>(s.lens), static_cast<void*>(s.delta),
@@ -361,6 +408,15 @@ void Ctx::convert_adapter(const float* src, uint8_t* dst) const {
 void Ctx::build_plans() {
   attn = make_attention_plan(qkv16.p, ctx16.p, max_rows, d, static_cast<int>(opt.precision));
   const int sms = device_sm_count();
+  {  // statistics producers' N tiles fix the number of partials per row
+    const int mt = max_rows / 128;
+    stats1_bn = pick_bn(d, mt, sms);
+    stats2_bn = pick_bn(d, mt, sms, true);
+    stats1_n = 2 * (d / stats1_bn);
+    stats2_n = 2 * (d / stats2_bn);
+    HMI_CHECK(stats1_n <= kStatsLd && stats2_n <= kStatsLd, HMI_CONFIG_ERROR,
+              "hidden size too wide for the LayerNorm statistics buffer");
+  }
   const int m_tiles = max_rows / 128;
   const int prec = static_cast<int>(opt.precision);
   const size_t off_wu = static_cast<size_t>(r_pad) * d * 2;
@@ -416,8 +472,73 @@ void Ctx::build_plans() {
     s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
     s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, m_tiles, sms, true);
     w.ffn2 = make_gemm_plan(s);
+    if (ln_mode == 0) {
+      // LayerNorm folding. Buffers hold PRE-norm rows: x16 = y1 (pre-LN1), h16 = y2 (pre-LN2
+      // of layer l-1; h0 for l = 0); d_stats1/2 their partial row sums.
+      const LayerDev* prev = l > 0 ? &layers[l - 1] : nullptr;
+      const float inv_d = 1.0f / static_cast<float>(d);
+      if (prev) {  // QKV on LN2_{l-1}(y2): gamma folded into W, mean corrected in the epilogue
+        GemmSpec q;
+        q.precision = prec;
+        q.a_rows = max_rows;
+        q.a = h16.p; q.a_ld = d; q.K = d;
+        q.b = w.wqkv_f; q.N = 3 * d; q.groups = 1; q.b_ld = d;
+        q.b_group_stride_bytes = size_t(3) * d * d * 2;
+        q.bias = w.bqkv_f; q.c = qkv16.p; q.c_ld = 3 * d; q.epi = kEpiFoldLN; q.cta2 = true;
+        q.a_stats = d_stats2.p; q.a_stats_n = stats2_n; q.colsum = w.cs_qkv; q.inv_n = inv_d;
+        q.bn = pick_bn(3 * d, m_tiles, sms, true);
+        w.qkv = make_gemm_plan(q);
+      }
+      {  // adapter up: y1 = mid.Wu + bu + a + LN2_{l-1}(y2)  (+ partial stats of y1)
+        GemmSpec u;
+        u.precision = prec;
+        u.a_rows = max_rows;
+        u.a = mid16.p; u.a_ld = r_pad; u.K = r_pad;
+        u.b = arena.p + off_wu; u.N = d; u.groups = static_cast<int>(n_slots); u.b_ld = r_pad;
+        u.b_group_stride_bytes = slot_bytes;
+        u.bias = reinterpret_cast<const float*>(arena.p + off_bu);
+        u.bias_group_stride = static_cast<long long>(slot_bytes / 4);
+        u.tile_slot = d_tile_slot.p + static_cast<size_t>(l) * tile_stride;
+        u.res0 = a16.p; u.res1 = h16.p; u.res_ld = d;
+        u.c = x16.p; u.c_ld = d;
+        u.epi = kEpiRes2 | kEpiStats | (prev ? kEpiRes1LN : 0);
+        u.stats_out = d_stats1.p; u.stats_ld = kStatsLd;
+        if (prev) {
+          u.r_stats = d_stats2.p; u.r_stats_n = stats2_n;
+          u.r_gamma = prev->ln2g; u.r_beta = prev->ln2b; u.inv_n = inv_d;
+        }
+        u.bn = stats1_bn;
+        w.ad_up = make_gemm_plan(u);
+      }
+      {  // FFN1 on LN1(y1)
+        GemmSpec g;
+        g.precision = prec;
+        g.a_rows = max_rows;
+        g.a = x16.p; g.a_ld = d; g.K = d;
+        g.b = w.w1_f; g.N = f; g.groups = 1; g.b_ld = d; g.b_group_stride_bytes = size_t(f) * d * 2;
+        g.bias = w.b1_f; g.c = ffn16.p; g.c_ld = f; g.epi = kEpiRelu | kEpiFoldLN; g.cta2 = true;
+        g.a_stats = d_stats1.p; g.a_stats_n = stats1_n; g.colsum = w.cs_1; g.inv_n = inv_d;
+        g.bn = pick_bn(f, m_tiles, sms, true);
+        w.ffn1 = make_gemm_plan(g);
+      }
+      {  // FFN2: y2 = ffn.W2 + b2 + LN1(y1)  (+ partial stats of y2)
+        GemmSpec g;
+        g.precision = prec;
+        g.a_rows = max_rows;
+        g.a = ffn16.p; g.a_ld = f; g.K = f;
+        g.b = w.w2; g.N = d; g.groups = 1; g.b_ld = f; g.b_group_stride_bytes = size_t(d) * f * 2;
+        g.bias = w.b2; g.res0 = x16.p; g.res_ld = d; g.c = h16.p; g.c_ld = d;
+        g.epi = kEpiRes1 | kEpiRes0LN | kEpiStats; g.cta2 = true;
+        g.stats_out = d_stats2.p; g.stats_ld = kStatsLd;
+        g.r_stats = d_stats1.p; g.r_stats_n = stats1_n; g.r_gamma = w.ln1g; g.r_beta = w.ln1b;
+        g.inv_n = inv_d;
+        g.bn = stats2_bn;
+        w.ffn2 = make_gemm_plan(g);
+      }
+      continue;
+    }
     // fused variants: adapter up + skip + residual + LN1 -> x16; FFN2 + residual + LN2 -> h16
-    {
+    if (ln_mode == 2) {
       GemmSpec u;
       u.precision = prec;
       u.a_rows = max_rows;
@@ -666,7 +787,11 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
     if (fine) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
     timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
-    if (fused_ln) {
+    if (ln_mode == 0) {
+      timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
+      timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
+      timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
+    } else if (ln_mode == 2) {
       timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up_ln, rows, s); });
       timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
       timed(P_FFN2, s, [&] { launch_gemm(w.ffn2_ln, rows, s); });
@@ -686,6 +811,16 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   H.labels = d_head_labels.p;
   H.kind = d_head_kind.p;
   timed(P_HEAD, s, [&] {
+    if (ln_mode == 0) {  // the head applies the last layer's LN2 to its pre-norm row
+      H.y16 = h16.p;
+      H.ln_g = layers[L - 1].ln2g;
+      H.ln_b = layers[L - 1].ln2b;
+      H.bf16 = prec;
+      if (debug_flags & 2) {
+        launch_normalize_rows(h16.p, d_stats2.p, stats2_n, 1.0f / d, layers[L - 1].ln2g,
+                              layers[L - 1].ln2b, h32.p, rows, d, prec, s);
+      }
+    }
     launch_head(H, h32.p, d_req_head.p, d_lens.p, static_cast<int>(n_req), S, d,
                 static_cast<int>(opt.max_labels), d_scores_out ? d_scores_out : d_scores.p,
                 d_labels_out ? d_labels_out : d_labels.p, d_tags.p, s);
@@ -702,7 +837,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   st.busy = true;
   inflight.push_back(Inflight{st.done, si, uniq});
   last_n = n_req;
-  n_launches += (delta.empty() ? 0 : 1) + 3 + (fused_ln ? 7ull : 9ull) * L;
+  n_launches += (delta.empty() ? 0 : 1) + 3 + (ln_mode == 1 ? 9ull : 7ull) * L;
   ++n_batches;
   last_S = static_cast<uint32_t>(S);
   return si;
@@ -845,6 +980,48 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       v32.insert(v32.end(), g2, g2 + d);
       v32.insert(v32.end(), s2, s2 + d);
       HMI_CUDA(cudaMemcpy(p32, v32.data(), v32.size() * 4, cudaMemcpyHostToDevice));
+      // LN folding: FFN1 consumes pre-LN1 y1 (this layer's LN1); QKV of layer l >= 1
+      // consumes pre-LN2 y2 of layer l-1 (that layer's LN2)
+      {
+        std::vector<uint16_t> wf1, wfq, tmpq;
+        std::vector<float> bf1, cs1, bfq, csq;
+        fold_weights(w1, d, f, b1, g1, s1, prec, wf1, bf1, cs1);
+        const size_t bytes = (3 * d * d + f * d) * 2 + (2 * 3 * d + 2 * f) * 4 + 1024;
+        HMI_CUDA(cudaMalloc(&L.mem_fold, bytes));
+        uint16_t* f16p = static_cast<uint16_t*>(L.mem_fold);
+        L.wqkv_f = f16p;
+        L.w1_f = f16p + 3 * d * d;
+        float* f32p = reinterpret_cast<float*>(L.w1_f + f * d);
+        L.bqkv_f = f32p;
+        L.cs_qkv = f32p + 3 * d;
+        L.b1_f = f32p + 6 * d;
+        L.cs_1 = f32p + 6 * d + f;
+        HMI_CUDA(cudaMemcpy(L.w1_f, wf1.data(), wf1.size() * 2, cudaMemcpyHostToDevice));
+        HMI_CUDA(cudaMemcpy(L.b1_f, bf1.data(), f * 4, cudaMemcpyHostToDevice));
+        HMI_CUDA(cudaMemcpy(L.cs_1, cs1.data(), f * 4, cudaMemcpyHostToDevice));
+        if (l > 0) {
+          const float* pw = higher_f32 + (l - 1) * lf;
+          const float* pg2 = pw + 4 * (d * d + d) + (d * f + f) + (f * d + d) + 2 * d;
+          const float* ps2 = pg2 + d;
+          // concatenated [wq | wk | wv] as one [d][3d] matrix, biases [bq | bk | bv]
+          std::vector<float> wcat(d * 3 * d), bcat(3 * d);
+          for (size_t i = 0; i < d; ++i)
+            for (size_t o = 0; o < d; ++o) {
+              wcat[i * 3 * d + o] = wq[i * d + o];
+              wcat[i * 3 * d + d + o] = wk[i * d + o];
+              wcat[i * 3 * d + 2 * d + o] = wv[i * d + o];
+            }
+          for (size_t o = 0; o < d; ++o) {
+            bcat[o] = bq[o];
+            bcat[d + o] = bk[o];
+            bcat[2 * d + o] = bv[o];
+          }
+          fold_weights(wcat.data(), d, 3 * d, bcat.data(), pg2, ps2, prec, wfq, bfq, csq);
+          HMI_CUDA(cudaMemcpy(L.wqkv_f, wfq.data(), wfq.size() * 2, cudaMemcpyHostToDevice));
+          HMI_CUDA(cudaMemcpy(L.bqkv_f, bfq.data(), 3 * d * 4, cudaMemcpyHostToDevice));
+          HMI_CUDA(cudaMemcpy(L.cs_qkv, csq.data(), 3 * d * 4, cudaMemcpyHostToDevice));
+        }
+      }
     }
 
     // ---- activations
@@ -913,7 +1090,12 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     c.pool = std::make_unique<SlotPool>(pool_bytes, static_cast<uint32_t>(n_slots64));
     c.arena.alloc(static_cast<size_t>(n_slots64) * c.slot_bytes);
     HMI_CUDA(cudaMemset(c.arena.p, 0, c.arena.n));
-    if (const char* env = std::getenv("HMI_UNFUSED_LN")) c.fused_ln = env[0] != '1';
+    if (const char* env = std::getenv("HMI_LN_MODE")) {
+      const std::string m(env);
+      c.ln_mode = m == "unfused" ? 1 : m == "cluster" ? 2 : 0;
+    }
+    c.d_stats1.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
+    c.d_stats2.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.build_plans();
     HMI_CUDA(cudaDeviceSynchronize());
   });

@@ -34,6 +34,14 @@ KernelFn pick_epi_t(int epi) {
     case kEpiOutF32: return kernel_ptr<BN, T | kEpiOutF32, C2>();
     case kEpiRes1 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes1 | kEpiOutF32, C2>();
     case kEpiRes2 | kEpiOutF32: return kernel_ptr<BN, T | kEpiRes2 | kEpiOutF32, C2>();
+    // LayerNorm folding
+    case kEpiFoldLN: return kernel_ptr<BN, T | kEpiFoldLN, C2>();
+    case kEpiRelu | kEpiFoldLN: return kernel_ptr<BN, T | kEpiRelu | kEpiFoldLN, C2>();
+    case kEpiRes1 | kEpiRes0LN | kEpiStats:
+      return kernel_ptr<BN, T | kEpiRes1 | kEpiRes0LN | kEpiStats, C2>();
+    case kEpiRes2 | kEpiStats: return kernel_ptr<BN, T | kEpiRes2 | kEpiStats, C2>();
+    case kEpiRes2 | kEpiRes1LN | kEpiStats:
+      return kernel_ptr<BN, T | kEpiRes2 | kEpiRes1LN | kEpiStats, C2>();
     default: break;
   }
   if constexpr (!C2) {
@@ -140,6 +148,20 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.res_ld = s.res_ld;
   p.args.ln_gamma = s.ln_gamma;
   p.args.ln_beta = s.ln_beta;
+  p.args.stats_out = s.stats_out;
+  p.args.stats_ld = s.stats_ld;
+  p.args.a_stats = s.a_stats;
+  p.args.a_stats_n = s.a_stats_n;
+  p.args.colsum = s.colsum;
+  p.args.r_stats = s.r_stats;
+  p.args.r_stats_n = s.r_stats_n;
+  p.args.r_gamma = s.r_gamma;
+  p.args.r_beta = s.r_beta;
+  p.args.inv_n = s.inv_n;
+  if (s.epi & kEpiStats) HMI_CHECK(s.stats_out && 2 * (s.N / s.bn) <= s.stats_ld, HMI_CONFIG_ERROR, "gemm: stats buffer");
+  if (s.epi & kEpiFoldLN) HMI_CHECK(s.a_stats && s.colsum && s.inv_n > 0.f, HMI_CONFIG_ERROR, "gemm: fold args");
+  if (s.epi & (kEpiRes0LN | kEpiRes1LN))
+    HMI_CHECK(s.r_stats && s.r_gamma && s.r_beta && s.inv_n > 0.f, HMI_CONFIG_ERROR, "gemm: residual LN args");
   p.args.idesc = idesc_f16(c2 ? 2 * kBlockM : kBlockM, s.bn, s.precision == 1 ? 1u : 0u);
   p.max_rows = s.a_rows;
   if (ln) {

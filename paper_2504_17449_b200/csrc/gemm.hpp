@@ -23,6 +23,17 @@ struct GemmArgs {
   uint32_t idesc;
   const float* ln_gamma;       // kEpiLN: LayerNorm gain / shift over the full N-wide row
   const float* ln_beta;
+  // --- LayerNorm folding (kEpiStats / kEpiFoldLN / kEpiRes0LN / kEpiRes1LN) ---
+  float2* stats_out;           // kEpiStats: per (row, n tile, column half) (sum, sum of squares)
+  int stats_ld;                // float2 entries per row
+  const float2* a_stats;       // kEpiFoldLN: partial stats of A's (pre-norm) rows
+  int a_stats_n;               // partials per row
+  const float* colsum;         // kEpiFoldLN: sum_k of the gamma-folded 16-bit weights, per column
+  const float2* r_stats;       // kEpiRes0LN/kEpiRes1LN: partial stats of the pre-norm residual
+  int r_stats_n;
+  const float* r_gamma;        // LayerNorm applied on the fly to that residual
+  const float* r_beta;
+  float inv_n;                 // 1 / (row width the statistics cover)
 };
 
 // Epilogue flags
@@ -34,6 +45,11 @@ constexpr int kEpiBf16 = 16;  // 16-bit outputs / residuals are bf16 (set from p
 constexpr int kEpiLN = 32;    // LayerNorm over the row (cluster of N/BN CTAs), 16-bit output
 constexpr int kEpiOut2F32 = 64;  // with kEpiLN: also write an f32 copy through map_c2
 constexpr int kEpiResTma = 128;  // with kEpiLN: residual tiles TMA-prefetched into smem
+// LayerNorm folding: LN(y) is never materialised; its consumers apply it.
+constexpr int kEpiStats = 256;   // write per-row partial (sum, sumsq) of the output
+constexpr int kEpiFoldLN = 512;  // A is pre-norm y: out = inv*(acc - mean*colsum) + bias
+constexpr int kEpiRes0LN = 1024; // residual res0 is pre-norm: add LN(res0) (r_* args)
+constexpr int kEpiRes1LN = 2048; // residual res1 is pre-norm: add LN(res1)
 
 // All tensor maps of one GEMM (passed as one __grid_constant__ kernel parameter).
 struct GemmMaps {
@@ -63,6 +79,16 @@ struct GemmSpec {
   const float* ln_beta = nullptr;
   void* c2 = nullptr;                // kEpiOut2F32: f32 copy [a_rows][c2_ld]
   int c2_ld = 0;
+  float2* stats_out = nullptr;       // kEpiStats
+  int stats_ld = 0;
+  const float2* a_stats = nullptr;   // kEpiFoldLN
+  int a_stats_n = 0;
+  const float* colsum = nullptr;
+  const float2* r_stats = nullptr;   // kEpiRes0LN / kEpiRes1LN
+  int r_stats_n = 0;
+  const float* r_gamma = nullptr;
+  const float* r_beta = nullptr;
+  float inv_n = 0.f;
 };
 
 struct GemmPlan {

@@ -83,9 +83,45 @@ __device__ __forceinline__ void add_res16(float* v, const uint16_t* src) {
   }
 }
 
+// Row (mean, 1/sqrt(var + eps)) of a pre-norm row from P partial (sum, sumsq) entries
+// (layer_norm, ops.cpp:92-116: biased variance, epsilon 1e-5).
+__device__ __forceinline__ float2 row_stats(const float2* part, int n, float inv_n) {
+  float s1 = 0.f, s2 = 0.f;
+  for (int i = 0; i < n; ++i) {
+    const float2 p = __ldg(part + i);
+    s1 += p.x;
+    s2 += p.y;
+  }
+  const float mean = s1 * inv_n;
+  const float var = fmaxf(s2 * inv_n - mean * mean, 0.0f);
+  return make_float2(mean, 1.0f / sqrtf(var + 1e-5f));
+}
+
+// v[0..N) += LN(pre-norm 16-bit residual row segment): (y - mean) * inv * gamma + beta
+template <bool kBf16, int N>
+__device__ __forceinline__ void add_res16_ln(float* v, const uint16_t* src, float2 st,
+                                             const float* gamma, const float* beta) {
+  float r[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) r[i] = 0.f;
+  add_res16<kBf16, N>(r, src);
+#pragma unroll
+  for (int i = 0; i < N; i += 4) {
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + i));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(beta + i));
+    v[i] += (r[i] - st.x) * st.y * g.x + b.x;
+    v[i + 1] += (r[i + 1] - st.x) * st.y * g.y + b.y;
+    v[i + 2] += (r[i + 2] - st.x) * st.y * g.z + b.z;
+    v[i + 3] += (r[i + 3] - st.x) * st.y * g.w + b.w;
+  }
+}
+
 // One accumulator tile (128 rows x BN cols in TMEM) -> bias / residual / ReLU -> 16/32-bit
 // -> swizzled smem staging -> TMA store. Called by 8 epilogue warps: warp (q, half) owns TMEM
 // lane quarter q and every other kCW-column chunk.
+// LayerNorm folding: kEpiFoldLN rescales the accumulator of a pre-norm A operand by its
+// row statistics; kEpiRes{0,1}LN normalise a pre-norm residual on the fly; kEpiStats
+// emits this thread's partial row (sum, sumsq) for the next consumer.
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, int grp,
                                               const GemmArgs& args, const CUtensorMap* map_c,
@@ -99,6 +135,16 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
   const int row = row0 + static_cast<int>(lane);
   const bool row_ok = row < args.M;
   const uint32_t t_row = t_acc + ((q * 32) << 16);
+  float2 a_st = make_float2(0.f, 1.f), r_st = make_float2(0.f, 1.f);
+  if constexpr ((EPI & kEpiFoldLN) != 0) {
+    if (row_ok) a_st = row_stats(args.a_stats + static_cast<long long>(row) * args.a_stats_n,
+                                 args.a_stats_n, args.inv_n);
+  }
+  if constexpr ((EPI & (kEpiRes0LN | kEpiRes1LN)) != 0) {
+    if (row_ok) r_st = row_stats(args.r_stats + static_cast<long long>(row) * args.r_stats_n,
+                                 args.r_stats_n, args.inv_n);
+  }
+  float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
   for (int c = half * kCW; c < BN; c += 2 * kCW) {
     float v[kCW];
@@ -110,6 +156,17 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
     }
+    if constexpr ((EPI & kEpiFoldLN) != 0) {
+      const float* cs = args.colsum + nt * BN + c;
+#pragma unroll
+      for (int i = 0; i < kCW; i += 4) {
+        const float4 c4 = __ldg(reinterpret_cast<const float4*>(cs + i));
+        v[i] = a_st.y * (v[i] - a_st.x * c4.x);
+        v[i + 1] = a_st.y * (v[i + 1] - a_st.x * c4.y);
+        v[i + 2] = a_st.y * (v[i + 2] - a_st.x * c4.z);
+        v[i + 3] = a_st.y * (v[i + 3] - a_st.x * c4.w);
+      }
+    }
 #pragma unroll
     for (int i = 0; i < kCW; i += 4) {
       const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
@@ -117,16 +174,34 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
     }
     if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
       if (row_ok) {
-        const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
-        add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off);
+        const int col = nt * BN + c;
+        const long long off = static_cast<long long>(row) * args.res_ld + col;
+        if constexpr ((EPI & kEpiRes0LN) != 0) {
+          add_res16_ln<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off, r_st,
+                                   args.r_gamma + col, args.r_beta + col);
+        } else {
+          add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off);
+        }
         if constexpr ((EPI & kEpiRes2) != 0) {
-          add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off);
+          if constexpr ((EPI & kEpiRes1LN) != 0) {
+            add_res16_ln<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off, r_st,
+                                     args.r_gamma + col, args.r_beta + col);
+          } else {
+            add_res16<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res1) + off);
+          }
         }
       }
     }
     if constexpr ((EPI & kEpiRelu) != 0) {
 #pragma unroll
       for (int i = 0; i < kCW; ++i) v[i] = fmaxf(v[i], 0.0f);
+    }
+    if constexpr ((EPI & kEpiStats) != 0) {
+#pragma unroll
+      for (int i = 0; i < kCW; ++i) {
+        s1 += v[i];
+        s2 += v[i] * v[i];
+      }
     }
     uint32_t packed[32];  // one 128-byte row per thread
     if constexpr (kOutF32) {
@@ -150,6 +225,12 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
     if (lane == 0 && mt < args.num_m_tiles) {
       tma_store_2d(map_c, stg, nt * BN + c, row0);
       tma_store_commit();
+    }
+  }
+  if constexpr ((EPI & kEpiStats) != 0) {
+    if (row_ok) {
+      args.stats_out[static_cast<long long>(row) * args.stats_ld + nt * 2 + half] =
+          make_float2(s1, s2);
     }
   }
 }

@@ -79,7 +79,17 @@ struct HeadDev {
   const int64_t* offset = nullptr;  // [heads] float offset of W (d x labels) ; b follows
   const int32_t* labels = nullptr;  // [heads]
   const int32_t* kind = nullptr;    // [heads] 0 cls, 1 token_tag, 2 lm
+  // LN folding: rows come pre-norm (16-bit) and the head applies LayerNorm exactly (f64)
+  const void* y16 = nullptr;
+  const float* ln_g = nullptr;
+  const float* ln_b = nullptr;
+  int bf16 = 0;
 };
+
+// Final LayerNorm of pre-norm 16-bit rows from partial statistics (debug / introspection).
+void launch_normalize_rows(const void* y16, const float2* stats, int n_part, float inv_n,
+                           const float* gamma, const float* beta, float* out, int rows, int d,
+                           int precision, cudaStream_t stream);
 void launch_head(const HeadDev& heads, const float* h32, const int32_t* req_head,
                  const int* lens, int n_req, int S, int d, int max_labels, float* scores,
                  int32_t* labels_out, int32_t* tags, cudaStream_t stream);

@@ -303,6 +303,46 @@ __global__ void apply_deltas_kernel(int32_t* __restrict__ table, const int32_t* 
 // K7: heads. cls/lm: one CTA per request over the selected row; token_tag: one
 // warp per valid row. f64 accumulation of an f32 row against f32 weights.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ double load16(const void* p, long long i, int bf16) {
+  const uint16_t u = static_cast<const uint16_t*>(p)[i];
+  if (bf16) return static_cast<double>(__uint_as_float(static_cast<uint32_t>(u) << 16));
+  return static_cast<double>(__half2float(__ushort_as_half(u)));
+}
+
+// block-wide sum (all threads get the result); scratch holds blockDim doubles
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += scratch[w];
+  __syncthreads();
+  return t;
+}
+
+// Final LayerNorm of pre-norm 16-bit rows from partial statistics (warp per row).
+__global__ void normalize_rows_kernel(const uint16_t* __restrict__ y, const float2* __restrict__ st,
+                                      int n_part, float inv_n, const float* __restrict__ g,
+                                      const float* __restrict__ be, float* __restrict__ out,
+                                      int rows, int d, int bf16) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float s1 = 0.f, s2 = 0.f;
+  for (int i = 0; i < n_part; ++i) {
+    s1 += st[static_cast<long long>(row) * 16 + i].x;
+    s2 += st[static_cast<long long>(row) * 16 + i].y;
+  }
+  const float mean = s1 * inv_n;
+  const float inv = 1.0f / sqrtf(fmaxf(s2 * inv_n - mean * mean, 0.f) + 1e-5f);
+  for (int j = lane; j < d; j += 32) {
+    const float v = static_cast<float>(load16(y, static_cast<long long>(row) * d + j, bf16));
+    out[static_cast<long long>(row) * d + j] = (v - mean) * inv * g[j] + be[j];
+  }
+}
+
 __global__ void __launch_bounds__(256) head_kernel(HeadDev H, const float* __restrict__ h32,
                                                    const int32_t* __restrict__ req_head,
                                                    const int* __restrict__ lens, int S, int d,
@@ -321,14 +361,33 @@ __global__ void __launch_bounds__(256) head_kernel(HeadDev H, const float* __res
     // token_tag: rows < valid_len, argmax per row
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int r = warp; r < len; r += blockDim.x >> 5) {
-      const float* x = h32 + (static_cast<long long>(b) * S + r) * d;
+      const long long rbase = (static_cast<long long>(b) * S + r) * d;
+      const float* x = h32 + rbase;
+      double mean = 0.0, inv = 1.0;
+      if (H.y16) {  // LayerNorm of the pre-norm row, f64 (ops.cpp:92-116)
+        double s1 = 0.0;
+        for (int j = lane; j < d; j += 32) s1 += load16(H.y16, rbase + j, H.bf16);
+        for (int o = 16; o > 0; o >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        mean = s1 / d;
+        double s2 = 0.0;
+        for (int j = lane; j < d; j += 32) {
+          const double t = load16(H.y16, rbase + j, H.bf16) - mean;
+          s2 += t * t;
+        }
+        for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        inv = 1.0 / sqrt(s2 / d + 1e-5);
+      }
       double best = -INFINITY;
       int besti = 0;
       for (int l0 = 0; l0 < nl; l0 += 32) {
         const int l = l0 + lane;
         double acc = 0.0;
         if (l < nl) {
-          for (int j = 0; j < d; ++j) acc += static_cast<double>(x[j]) * W[static_cast<long long>(j) * nl + l];
+          for (int j = 0; j < d; ++j) {
+            const double xj = H.y16 ? (load16(H.y16, rbase + j, H.bf16) - mean) * inv * H.ln_g[j] + H.ln_b[j]
+                                    : static_cast<double>(x[j]);
+            acc += xj * W[static_cast<long long>(j) * nl + l];
+          }
           acc += B[l];
         }
         // serial first-max scan over this chunk in label order (model.cpp:122-128)
@@ -343,11 +402,30 @@ __global__ void __launch_bounds__(256) head_kernel(HeadDev H, const float* __res
     return;
   }
   const int row = kind == 0 ? 0 : len - 1;
-  const float* x = h32 + (static_cast<long long>(b) * S + row) * d;
+  const long long rbase = (static_cast<long long>(b) * S + row) * d;
+  const float* x = h32 + rbase;
   double* xs = shd;                       // d
   double* rv = shd + d;                   // blockDim reduction values
   int* ri = reinterpret_cast<int*>(rv + blockDim.x);
-  for (int j = threadIdx.x; j < d; j += blockDim.x) xs[j] = x[j];
+  if (H.y16) {
+    // LayerNorm of the pre-norm row in f64 (ops.cpp:92-116), then the head product
+    double s1 = 0.0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      xs[j] = load16(H.y16, rbase + j, H.bf16);
+      s1 += xs[j];
+    }
+    const double mean = block_sum(s1, rv) / d;
+    double s2 = 0.0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const double t = xs[j] - mean;
+      s2 += t * t;
+    }
+    const double inv = 1.0 / sqrt(block_sum(s2, rv) / d + 1e-5);
+    for (int j = threadIdx.x; j < d; j += blockDim.x)
+      xs[j] = (xs[j] - mean) * inv * H.ln_g[j] + H.ln_b[j];
+  } else {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) xs[j] = x[j];
+  }
   __syncthreads();
   double best = -INFINITY;
   int besti = 0x7fffffff;
@@ -456,6 +534,16 @@ void launch_route(const uint32_t* instance_idx, int n_req, const int32_t* inst_v
   route_kernel<<<(n_req + 127) / 128, 128, 0, stream>>>(
       instance_idx, n_req, inst_version, inst_task, inst_head, n_instances, slot_of, layers,
       tiles_per_req, tile_stride, req_version, req_task, req_head, tile_slot, err);
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_normalize_rows(const void* y16, const float2* stats, int n_part, float inv_n,
+                           const float* gamma, const float* beta, float* out, int rows, int d,
+                           int precision, cudaStream_t stream) {
+  if (rows <= 0) return;
+  normalize_rows_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(
+      static_cast<const uint16_t*>(y16), stats, n_part, inv_n, gamma, beta, out, rows, d,
+      precision);
   HMI_CUDA(cudaGetLastError());
 }
 

@@ -108,19 +108,21 @@ def test_c1_swap_small_pool_bit_identical(c1):
     w.eng.close()
 
 
-def test_fused_ln_matches_unfused(c1, monkeypatch):
-    """The LN-in-epilogue GEMMs (cluster row reduction) agree with the separate
-    K4 LayerNorm kernels; both meet the oracle tolerance."""
+@pytest.mark.parametrize("mode", ["unfused", "cluster"])
+def test_layernorm_placements_agree(c1, monkeypatch, mode):
+    """The three LayerNorm placements — folded into the consumers (default), separate
+    K4 kernels, cluster-reduced GEMM epilogues — agree and all meet the tolerance."""
     inst, toks, lens = c1.requests(23, 16, 128)
-    fused = c1.eng.infer_batch(inst, toks, lens)
-    monkeypatch.setenv("HMI_UNFUSED_LN", "1")
+    folded = c1.eng.infer_batch(inst, toks, lens)
+    monkeypatch.setenv("HMI_LN_MODE", mode)
     w = World(oracle.TINY, n_tasks=16, r=16, labels=8, max_batch=32)
-    unfused = w.eng.infer_batch(inst, toks, lens)
+    other = w.eng.infer_batch(inst, toks, lens)
     w.eng.close()
-    ref_scores, _, _ = c1.oracle_batch(inst, toks, lens)
-    assert logit_error(fused.scores, ref_scores) <= TOL
-    assert logit_error(unfused.scores, ref_scores) <= TOL
-    assert np.abs(fused.scores - unfused.scores).max() < 1e-2
+    ref_scores, ref_labels, _ = c1.oracle_batch(inst, toks, lens)
+    assert logit_error(folded.scores, ref_scores) <= TOL
+    assert logit_error(other.scores, ref_scores) <= TOL
+    assert (folded.labels == ref_labels).mean() >= 0.999
+    assert np.abs(folded.scores - other.scores).max() < 1e-2
 
 
 def test_routing_and_vocab_errors(c1):
