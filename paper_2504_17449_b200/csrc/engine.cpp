@@ -265,7 +265,7 @@ struct Ctx {
   // (HMI_LN_MODE=unfused), 2 cluster-reduced GEMM epilogues (HMI_LN_MODE=cluster)
   int ln_mode = 0;
   DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
-  static constexpr int kStatsLd = 16;
+  static constexpr int kStatsLd = kStatsStride;
   int stats1_bn = 0, stats2_bn = 0, stats1_n = 0, stats2_n = 0;
   // profiling
   bool prof = false;

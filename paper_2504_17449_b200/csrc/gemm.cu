@@ -158,7 +158,7 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.r_gamma = s.r_gamma;
   p.args.r_beta = s.r_beta;
   p.args.inv_n = s.inv_n;
-  if (s.epi & kEpiStats) HMI_CHECK(s.stats_out && 2 * (s.N / s.bn) <= s.stats_ld, HMI_CONFIG_ERROR, "gemm: stats buffer");
+  if (s.epi & kEpiStats) HMI_CHECK(s.stats_out && s.stats_ld == kStatsStride && 2 * (s.N / s.bn) <= kStatsStride, HMI_CONFIG_ERROR, "gemm: stats buffer");
   if (s.epi & kEpiFoldLN) HMI_CHECK(s.a_stats && s.colsum && s.inv_n > 0.f, HMI_CONFIG_ERROR, "gemm: fold args");
   if (s.epi & (kEpiRes0LN | kEpiRes1LN))
     HMI_CHECK(s.r_stats && s.r_gamma && s.r_beta && s.inv_n > 0.f, HMI_CONFIG_ERROR, "gemm: residual LN args");

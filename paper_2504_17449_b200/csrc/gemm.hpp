@@ -47,6 +47,7 @@ constexpr int kEpiOut2F32 = 64;  // with kEpiLN: also write an f32 copy through 
 constexpr int kEpiResTma = 128;  // with kEpiLN: residual tiles TMA-prefetched into smem
 // LayerNorm folding: LN(y) is never materialised; its consumers apply it.
 constexpr int kEpiStats = 256;   // write per-row partial (sum, sumsq) of the output
+constexpr int kStatsStride = 16; // float2 entries per row of a partial-statistics buffer
 constexpr int kEpiFoldLN = 512;  // A is pre-norm y: out = inv*(acc - mean*colsum) + bias
 constexpr int kEpiRes0LN = 1024; // residual res0 is pre-norm: add LN(res0) (r_* args)
 constexpr int kEpiRes1LN = 2048; // residual res1 is pre-norm: add LN(res1)

@@ -137,11 +137,11 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
   const uint32_t t_row = t_acc + ((q * 32) << 16);
   float2 a_st = make_float2(0.f, 1.f), r_st = make_float2(0.f, 1.f);
   if constexpr ((EPI & kEpiFoldLN) != 0) {
-    if (row_ok) a_st = row_stats(args.a_stats + static_cast<long long>(row) * args.a_stats_n,
+    if (row_ok) a_st = row_stats(args.a_stats + static_cast<long long>(row) * kStatsStride,
                                  args.a_stats_n, args.inv_n);
   }
   if constexpr ((EPI & (kEpiRes0LN | kEpiRes1LN)) != 0) {
-    if (row_ok) r_st = row_stats(args.r_stats + static_cast<long long>(row) * args.r_stats_n,
+    if (row_ok) r_st = row_stats(args.r_stats + static_cast<long long>(row) * kStatsStride,
                                  args.r_stats_n, args.inv_n);
   }
   float s1 = 0.f, s2 = 0.f;
