@@ -116,6 +116,24 @@ __device__ __forceinline__ void add_res16_ln(float* v, const uint16_t* src, floa
   }
 }
 
+// Row statistics the LN-folding epilogue modes need (fetched before the accumulator wait)
+template <int EPI>
+__device__ __forceinline__ void epi_row_stats(const GemmArgs& args, int mt, uint32_t q,
+                                              uint32_t lane, float2& a_st, float2& r_st) {
+  a_st = make_float2(0.f, 1.f);
+  r_st = make_float2(0.f, 1.f);
+  const int row = mt * kBlockM + static_cast<int>(q) * 32 + static_cast<int>(lane);
+  if (row >= args.M) return;
+  if constexpr ((EPI & kEpiFoldLN) != 0) {
+    a_st = row_stats(args.a_stats + static_cast<long long>(row) * kStatsStride, args.a_stats_n,
+                     args.inv_n);
+  }
+  if constexpr ((EPI & (kEpiRes0LN | kEpiRes1LN)) != 0) {
+    r_st = row_stats(args.r_stats + static_cast<long long>(row) * kStatsStride, args.r_stats_n,
+                     args.inv_n);
+  }
+}
+
 // One accumulator tile (128 rows x BN cols in TMEM) -> bias / residual / ReLU -> 16/32-bit
 // -> swizzled smem staging -> TMA store. Called by 8 epilogue warps: warp (q, half) owns TMEM
 // lane quarter q and every other kCW-column chunk.
@@ -125,7 +143,9 @@ __device__ __forceinline__ void add_res16_ln(float* v, const uint16_t* src, floa
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, int grp,
                                               const GemmArgs& args, const CUtensorMap* map_c,
-                                              uint8_t* stg, uint32_t q, int half, uint32_t lane) {
+                                              uint8_t* stg, uint32_t& sbuf, uint32_t q,
+                                              int half, uint32_t lane, float2 a_st,
+                                              float2 r_st) {
   constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
   constexpr bool kBf16 = (EPI & kEpiBf16) != 0;  // 16-bit tensors are bf16 (else fp16)
   constexpr int kCW = kOutF32 ? 32 : 64;         // output columns per 128-byte staging row
@@ -135,15 +155,6 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
   const int row = row0 + static_cast<int>(lane);
   const bool row_ok = row < args.M;
   const uint32_t t_row = t_acc + ((q * 32) << 16);
-  float2 a_st = make_float2(0.f, 1.f), r_st = make_float2(0.f, 1.f);
-  if constexpr ((EPI & kEpiFoldLN) != 0) {
-    if (row_ok) a_st = row_stats(args.a_stats + static_cast<long long>(row) * kStatsStride,
-                                 args.a_stats_n, args.inv_n);
-  }
-  if constexpr ((EPI & (kEpiRes0LN | kEpiRes1LN)) != 0) {
-    if (row_ok) r_st = row_stats(args.r_stats + static_cast<long long>(row) * kStatsStride,
-                                 args.r_stats_n, args.inv_n);
-  }
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
   for (int c = half * kCW; c < BN; c += 2 * kCW) {
@@ -212,18 +223,21 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
       for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
     }
     // staging buffer reuse: this warp's previous TMA store must have read it
-    if (lane == 0) tma_store_wait_read<0>();
+    // double-buffered staging: the store issued from this buffer two chunks ago is read
+    if (lane == 0) tma_store_wait_read<1>();
     __syncwarp();
+    uint8_t* buf = stg + sbuf * 4096;
+    sbuf ^= 1;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int phys = i ^ (lane & 7);  // SWIZZLE_128B: 16 B chunk ^= row % 8
-      *reinterpret_cast<uint4*>(stg + lane * 128 + phys * 16) =
+      *reinterpret_cast<uint4*>(buf + lane * 128 + phys * 16) =
           make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
     }
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0 && mt < args.num_m_tiles) {
-      tma_store_2d(map_c, stg, nt * BN + c, row0);
+      tma_store_2d(map_c, buf, nt * BN + c, row0);
       tma_store_commit();
     }
   }
@@ -413,7 +427,8 @@ struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = 8 * 4096;  // 8 epilogue warps x (32 rows x 128 B)
+  // 8 epilogue warps x (32 rows x 128 B), double-buffered except for the LN epilogue
+  static constexpr int kEpiBytes = LN ? 8 * 4096 : 8 * 2 * 4096;
   // LN: stats[2 buffers][8 ranks][128 rows] float2 + partial[128] float2
   static constexpr int kLnBytes = LN ? (2 * 8 * 128 + 128) * 8 : 0;
   // RT: two residual tiles of 128 rows x BN (BN/64 SWIZZLE_128B boxes of 16 KB each)
@@ -570,12 +585,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = static_cast<int>(warp - 2) >> 2;
-    uint8_t* stg = sEpi + (warp - 2) * 4096;
+    uint8_t* stg = sEpi + (warp - 2) * (kLN ? 4096 : 2 * 4096);
+    uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0, iter = 0;
     for (int t = t_first; t < num_tiles; t += t_step, ++iter) {
       const int mt = t / args.num_n_tiles;
       const int nt = t - mt * args.num_n_tiles;
       const int grp = args.tile_slot ? __ldg(&args.tile_slot[mt]) : 0;
+      float2 a_st, r_st;
+      epi_row_stats<EPI>(args, mt, q, lane, a_st, r_st);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if constexpr (kLN) {
@@ -584,8 +602,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                   q, half, lane, ln_partial, ln_stats, stats_bar, iter, cs, crank,
                                   kRT ? sRes : nullptr, kRT ? res_empty : nullptr);
       } else {
-        epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, stg, q, half,
-                               lane);
+        epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, stg, sbuf, q,
+                               half, lane, a_st, r_st);
       }
       // all TMEM reads of this accumulator by this warp are done: hand it back
       tc_fence_before();
@@ -625,7 +643,7 @@ struct Gemm2Smem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;          // this CTA's 128 rows of A
   static constexpr int kBBytes = (BN / 2) * kBlockK * 2;         // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = 8 * 4096;
+  static constexpr int kEpiBytes = 8 * 2 * 4096;
   static constexpr int kBudget = 227 * 1024 - 1024 - 256;
   static constexpr int kStagesRaw = (kBudget - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
@@ -737,15 +755,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     const uint32_t q = warp & 3;
     const int half = static_cast<int>(warp - 2) >> 2;
-    uint8_t* stg = sEpi + (warp - 2) * 4096;
+    uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
+    uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0;
     for (int u = cluster; u < num_units; u += n_clusters) {
       const int mp = u / args.num_n_tiles;
       const int nt = u - mp * args.num_n_tiles;
       const int mt = 2 * mp + static_cast<int>(rank);
+      float2 a_st, r_st;
+      epi_row_stats<EPI>(args, mt, q, lane, a_st, r_st);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, 0, args, &map_c, stg, q, half, lane);
+      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, 0, args, &map_c, stg, sbuf, q, half,
+                             lane, a_st, r_st);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
