@@ -501,7 +501,7 @@ void Ctx::build_plans() {
         u.tile_slot = d_tile_slot.p + static_cast<size_t>(l) * tile_stride;
         u.res0 = a16.p; u.res1 = h16.p; u.res_ld = d;
         u.c = x16.p; u.c_ld = d;
-        u.epi = kEpiRes2 | kEpiStats | (prev ? kEpiRes1LN : 0);
+        u.epi = kEpiRes2 | kEpiStats | (prev ? kEpiRes1LN : 0) | (stats1_bn <= 192 ? kEpiResTma : 0);
         u.stats_out = d_stats1.p; u.stats_ld = kStatsLd;
         if (prev) {
           u.r_stats = d_stats2.p; u.r_stats_n = stats2_n;

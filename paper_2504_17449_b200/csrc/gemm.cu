@@ -44,6 +44,15 @@ KernelFn pick_epi_t(int epi) {
       return kernel_ptr<BN, T | kEpiRes2 | kEpiRes1LN | kEpiStats, C2>();
     default: break;
   }
+  if constexpr (!C2 && BN <= 192) {  // adapter up with TMA-staged residuals
+    switch (epi) {
+      case kEpiRes2 | kEpiStats | kEpiResTma:
+        return kernel_ptr<BN, T | kEpiRes2 | kEpiStats | kEpiResTma, false>();
+      case kEpiRes2 | kEpiRes1LN | kEpiStats | kEpiResTma:
+        return kernel_ptr<BN, T | kEpiRes2 | kEpiRes1LN | kEpiStats | kEpiResTma, false>();
+      default: break;
+    }
+  }
   if constexpr (!C2) {
     switch (epi) {
       case kEpiRes1 | kEpiLN: return kernel_ptr<BN, T | kEpiRes1 | kEpiLN, false>();
@@ -78,8 +87,11 @@ KernelFn pick_kernel(int bn, int epi, bool c2, int* smem_bytes) {
   }
   const bool ln = (epi & kEpiLN) != 0;
   const bool rt = (epi & kEpiResTma) != 0;
-#define HMI_SMEM(B) (rt ? (B <= 192 ? GemmSmem<(B <= 192 ? B : 64), true, true>::kTotal : 0) \
-                     : ln ? GemmSmem<B, true>::kTotal : GemmSmem<B>::kTotal)
+#define HMI_SMEM(B)                                                                   \
+  (rt ? (B <= 192 ? (ln ? GemmSmem<(B <= 192 ? B : 64), true, true>::kTotal              \
+                        : GemmSmem<(B <= 192 ? B : 64), false, true>::kTotal)            \
+                  : 0)                                                                    \
+      : ln ? GemmSmem<B, true>::kTotal : GemmSmem<B>::kTotal)
   switch (bn) {
     case 64: *smem_bytes = HMI_SMEM(64); return pick_epi<64, false>(epi);
     case 128: *smem_bytes = HMI_SMEM(128); return pick_epi<128, false>(epi);
@@ -125,7 +137,7 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.maps.r0 = p.maps.c;
   p.maps.r1 = p.maps.c;
   if (s.epi & kEpiResTma) {
-    HMI_CHECK(ln && s.res0 && s.res1, HMI_CONFIG_ERROR, "gemm: TMA residuals need LN + 2 residuals");
+    HMI_CHECK(s.res0 && s.res1 && !c2, HMI_CONFIG_ERROR, "gemm: TMA residuals need 2 residuals (1-CTA)");
     p.maps.r0 = make_tmap_2d(s.res0, t16, s.N, s.a_rows, s.res_ld * 2ull, 64, 128,
                              CU_TENSOR_MAP_SWIZZLE_128B);
     p.maps.r1 = make_tmap_2d(s.res1, t16, s.N, s.a_rows, s.res_ld * 2ull, 64, 128,

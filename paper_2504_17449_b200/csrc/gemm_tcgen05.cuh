@@ -116,6 +116,40 @@ __device__ __forceinline__ void add_res16_ln(float* v, const uint16_t* src, floa
   }
 }
 
+// r[0..N) = 16-bit residuals of (row_local, columns c..c+N) from TMA-staged SWIZZLE_128B
+// boxes [BN/64][128 rows][128 B]
+template <bool kBf16, int N>
+__device__ __forceinline__ void res_from_smem(float* r, const uint8_t* boxes, int row_local,
+                                              int c) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) r[i] = 0.f;
+#pragma unroll
+  for (int i = 0; i < N; i += 32) {
+    const uint8_t* rowp = boxes + ((c + i) >> 6) * 16384 + row_local * 128;
+    add_res16_smem<kBf16>(r + i, rowp, ((c + i) & 63) >> 3, row_local & 7);
+  }
+}
+
+// v += r, or v += LN(r) = (r - mean) * inv * gamma + beta
+template <int N, bool kLn>
+__device__ __forceinline__ void add_res_vals(float* v, const float* r, float2 st,
+                                             const float* gamma, const float* beta) {
+  if constexpr (kLn) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + i));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(beta + i));
+      v[i] += (r[i] - st.x) * st.y * g.x + b.x;
+      v[i + 1] += (r[i + 1] - st.x) * st.y * g.y + b.y;
+      v[i + 2] += (r[i + 2] - st.x) * st.y * g.z + b.z;
+      v[i + 3] += (r[i + 3] - st.x) * st.y * g.w + b.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] += r[i];
+  }
+}
+
 // Row statistics the LN-folding epilogue modes need (fetched before the accumulator wait)
 template <int EPI>
 __device__ __forceinline__ void epi_row_stats(const GemmArgs& args, int mt, uint32_t q,
@@ -145,7 +179,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
                                               const GemmArgs& args, const CUtensorMap* map_c,
                                               uint8_t* stg, uint32_t& sbuf, uint32_t q,
                                               int half, uint32_t lane, float2 a_st,
-                                              float2 r_st) {
+                                              float2 r_st, const uint8_t* res_smem) {
+  constexpr bool kResTma = (EPI & kEpiResTma) != 0;  // residual tiles staged in smem by TMA
   constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
   constexpr bool kBf16 = (EPI & kEpiBf16) != 0;  // 16-bit tensors are bf16 (else fp16)
   constexpr int kCW = kOutF32 ? 32 : 64;         // output columns per 128-byte staging row
@@ -184,8 +219,19 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
       v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
     }
     if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
-      if (row_ok) {
-        const int col = nt * BN + c;
+      const int col = nt * BN + c;
+      if constexpr (kResTma) {
+        const int row_local = static_cast<int>(q) * 32 + static_cast<int>(lane);
+        float r[kCW];
+        res_from_smem<kBf16, kCW>(r, res_smem, row_local, c);
+        add_res_vals<kCW, (EPI & kEpiRes0LN) != 0>(v, r, r_st, args.r_gamma + col,
+                                                   args.r_beta + col);
+        if constexpr ((EPI & kEpiRes2) != 0) {
+          res_from_smem<kBf16, kCW>(r, res_smem + (BN / 64) * 16384, row_local, c);
+          add_res_vals<kCW, (EPI & kEpiRes1LN) != 0>(v, r, r_st, args.r_gamma + col,
+                                                     args.r_beta + col);
+        }
+      } else if (row_ok) {
         const long long off = static_cast<long long>(row) * args.res_ld + col;
         if constexpr ((EPI & kEpiRes0LN) != 0) {
           add_res16_ln<kBf16, kCW>(v, reinterpret_cast<const uint16_t*>(args.res0) + off, r_st,
@@ -428,7 +474,7 @@ struct GemmSmem {
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // 8 epilogue warps x (32 rows x 128 B), double-buffered except for the LN epilogue
-  static constexpr int kEpiBytes = LN ? 8 * 4096 : 8 * 2 * 4096;
+  static constexpr int kEpiBytes = (LN || RT) ? 8 * 4096 : 8 * 2 * 4096;
   // LN: stats[2 buffers][8 ranks][128 rows] float2 + partial[128] float2
   static constexpr int kLnBytes = LN ? (2 * 8 * 128 + 128) * 8 : 0;
   // RT: two residual tiles of 128 rows x BN (BN/64 SWIZZLE_128B boxes of 16 KB each)
@@ -585,7 +631,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = static_cast<int>(warp - 2) >> 2;
-    uint8_t* stg = sEpi + (warp - 2) * (kLN ? 4096 : 2 * 4096);
+    uint8_t* stg = sEpi + (warp - 2) * ((kLN || kRT) ? 4096 : 2 * 4096);
     uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0, iter = 0;
     for (int t = t_first; t < num_tiles; t += t_step, ++iter) {
@@ -602,8 +648,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                   q, half, lane, ln_partial, ln_stats, stats_bar, iter, cs, crank,
                                   kRT ? sRes : nullptr, kRT ? res_empty : nullptr);
       } else {
+        if constexpr (kRT) mbar_wait(res_full, iter & 1);
         epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, stg, sbuf, q,
-                               half, lane, a_st, r_st);
+                               half, lane, a_st, r_st, sRes);
+        if constexpr (kRT) {  // residual tiles consumed: the producer may stage the next tile's
+          __syncwarp();
+          if (lane == 0) mbar_arrive(res_empty);
+        }
       }
       // all TMEM reads of this accumulator by this warp are done: hand it back
       tc_fence_before();
@@ -767,7 +818,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, 0, args, &map_c, stg, sbuf, q, half,
-                             lane, a_st, r_st);
+                             lane, a_st, r_st, nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
