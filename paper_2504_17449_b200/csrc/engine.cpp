@@ -1129,6 +1129,11 @@ int hmi_gpu_upload_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t parent_
       for (int32_t p : c.h_parent)
         if (p == -1) throw HmiError(HMI_CONFLICT_ERROR, "a root table is already registered");
     }
+    if (parent_id != kNoParent) {  // device retrieval resolves chains of up to 8 tables
+      int depth = 2;
+      for (int32_t v = c.h_parent[parent_id]; v >= 0; v = c.h_parent[v]) ++depth;
+      HMI_CHECK(depth <= 8, HMI_CONFIG_ERROR, "version tree deeper than 8 levels");
+    }
     const uint32_t n = static_cast<uint32_t>(c.ngram);
     uint64_t rows = 0;
     for (uint32_t e = 0; e < n_entries; ++e) {

@@ -134,9 +134,28 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
   const int c0 = causal ? p0 : (p0 - hr > 0 ? p0 - hr : 0);
   const int c1 = causal ? (p1 < len ? p1 : len) - 1 : (p1 - 1 + hl < len - 1 ? p1 - 1 + hl : len - 1);
 
-  // ---- phase 1: resolve every needed window (resolve_window, retrieval.cpp:23-69)
-  for (int c = c0 + static_cast<int>(threadIdx.x); c <= c1; c += blockDim.x) {
-    int start, end;
+  // ---- phase 1a: every (window, sub-gram, tree depth) probe of this chunk in parallel.
+  // The version chain (VersionTree::lookup walks branch -> parent -> ... -> root,
+  // version_tree.cpp:64-77) is resolved once; probe (w, o, k, depth) looks the sub-gram
+  // tokens[start_w + o, +k) up in the depth-th table of the chain only.
+  constexpr int kMaxDepth = 8;
+  constexpr int kSub = kMaxNgram * kMaxNgram;  // (o, k-1) slots per window
+  __shared__ int32_t chain[kMaxDepth];
+  __shared__ int32_t probe[kMaxWin * kSub * kMaxDepth];
+  __shared__ int32_t n_chain;
+  if (threadIdx.x == 0) {
+    int v = version, dd = 0;
+    while (v >= 0 && dd < kMaxDepth) {
+      chain[dd++] = v;
+      v = __ldg(&P.parent[v]);
+    }
+    n_chain = dd;
+  }
+  __syncthreads();
+  const int depth = n_chain;
+  const int n_win = c1 - c0 + 1;
+  auto win_bounds = [&](int c, int& start, int& wl) {
+    int end;
     if (causal) {
       start = c + 1 >= n ? c + 1 - n : 0;
       end = c;
@@ -144,33 +163,49 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
       start = c >= hl ? c - hl : 0;
       end = c + hr < len - 1 ? c + hr : len - 1;
     }
-    const int wl = end - start + 1;
-    uint32_t w[kMaxNgram];
-    for (int j = 0; j < wl; ++j) w[j] = tok[start + j];
-    int32_t memo[kMaxNgram][kMaxNgram + 1];
-    uint32_t done = 0;  // bit (o * 6 + k)
-    for (int p = 0; p < wl; ++p) {
-      int32_t row = -1, lev = 0;
-      for (int k = wl; k >= 1 && row < 0; --k) {
-        const int o_lo = p + 1 >= k ? p + 1 - k : 0;
-        const int o_hi = p < wl - k ? p : wl - k;
-        for (int o = o_lo; o <= o_hi; ++o) {
-          const uint32_t bit = 1u << (o * 6 + k);
-          if (!(done & bit)) {
-            memo[o][k] = plot_lookup(P, version, w + o, static_cast<uint32_t>(k));
-            done |= bit;
-          }
-          if (memo[o][k] >= 0) {
-            row = memo[o][k] + (p - o);
+    wl = end - start + 1;
+  };
+  for (int t = threadIdx.x; t < n_win * kSub * depth; t += blockDim.x) {
+    const int dd = t % depth;
+    const int si = (t / depth) % kSub;
+    const int wi = t / (depth * kSub);
+    const int o = si / kMaxNgram, k = si % kMaxNgram + 1;
+    int start, wl;
+    win_bounds(c0 + wi, start, wl);
+    int32_t r = -1;
+    if (o + k <= wl) {
+      uint32_t key[kMaxNgram];
+      for (int j = 0; j < k; ++j) key[j] = tok[start + o + j];
+      r = plot_find(P, static_cast<uint32_t>(chain[dd]), key, static_cast<uint32_t>(k));
+    }
+    probe[(wi * kSub + si) * kMaxDepth + dd] = r;
+  }
+  __syncthreads();
+  // ---- phase 1b: resolve_window (retrieval.cpp:23-69): for position p of the window, the
+  // longest stored sub-gram containing it, leftmost among equals; first chain hit wins
+  for (int t = threadIdx.x; t < n_win * n; t += blockDim.x) {
+    const int wi = t / n, p = t % n;
+    int start, wl;
+    win_bounds(c0 + wi, start, wl);
+    if (p >= wl) continue;
+    int32_t row = -1, lev = 0;
+    for (int k = wl; k >= 1 && row < 0; --k) {
+      const int o_lo = p + 1 >= k ? p + 1 - k : 0;
+      const int o_hi = p < wl - k ? p : wl - k;
+      for (int o = o_lo; o <= o_hi && row < 0; ++o) {
+        const int32_t* pr = &probe[(wi * kSub + o * kMaxNgram + (k - 1)) * kMaxDepth];
+        for (int dd = 0; dd < depth; ++dd) {
+          if (pr[dd] >= 0) {
+            row = pr[dd] + (p - o);
             lev = k;
             break;
           }
         }
       }
-      if (row < 0) atomicExch(err, HMI_BUILD_ERROR);  // uni-gram backstop missing
-      wrow[(c - c0) * n + p] = row;
-      wlev[(c - c0) * n + p] = lev;
     }
+    if (row < 0) atomicExch(err, HMI_BUILD_ERROR);  // uni-gram backstop missing
+    wrow[wi * n + p] = row;
+    wlev[wi * n + p] = lev;
   }
   __syncthreads();
 
