@@ -765,6 +765,13 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   P.reps = d_reps.p;
   P.ngram = ngram;
   P.d = d;
+  P.max_depth = 1;
+  for (size_t v = 0; v < h_parent.size(); ++v) {
+    if (h_parent[v] == -2) continue;
+    int depth = 1;
+    for (int32_t u = h_parent[v]; u >= 0; u = h_parent[u]) ++depth;
+    P.max_depth = std::max(P.max_depth, depth);
+  }
   const int causal = cfg.mode == 1 ? 1 : 0;
   const int prec = static_cast<int>(opt.precision);
   timed(P_RETRIEVE, s, [&] {

@@ -40,6 +40,7 @@ struct PlotDev {
   const float* reps = nullptr;     // [rows][d] f32, float32-exact PLOT values
   int ngram = 3;
   int d = 0;
+  int max_depth = 1;               // longest version chain (branch -> ... -> root), <= 8
 };
 
 // K5: on-device PLOT retrieval (retrieve_sequence, proj/src/plot/retrieval.cpp:82-124).

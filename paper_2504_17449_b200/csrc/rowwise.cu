@@ -110,7 +110,7 @@ __device__ __forceinline__ int32_t plot_lookup(const PlotDev& P, int32_t version
   return -1;
 }
 
-__global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t* __restrict__ tokens,
+__global__ void __launch_bounds__(256, 6) retrieve_kernel(PlotDev P, const uint32_t* __restrict__ tokens,
                                                        const int* __restrict__ lens,
                                                        const int* __restrict__ req_version,
                                                        int S, int causal, void* __restrict__ h16,
@@ -139,20 +139,29 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
   // version_tree.cpp:64-77) is resolved once; probe (w, o, k, depth) looks the sub-gram
   // tokens[start_w + o, +k) up in the depth-th table of the chain only.
   constexpr int kMaxDepth = 8;
-  constexpr int kSub = kMaxNgram * kMaxNgram;  // (o, k-1) slots per window
+  const int n_sub = n * (n + 1) / 2;           // valid (o, k) sub-grams of a full window
+  extern __shared__ int32_t probe[];           // [window][sub-gram][P.max_depth]
   __shared__ int32_t chain[kMaxDepth];
-  __shared__ int32_t probe[kMaxWin * kSub * kMaxDepth];
+  __shared__ int8_t sub_o[kMaxNgram * (kMaxNgram + 1) / 2], sub_k[kMaxNgram * (kMaxNgram + 1) / 2];
   __shared__ int32_t n_chain;
   if (threadIdx.x == 0) {
     int v = version, dd = 0;
-    while (v >= 0 && dd < kMaxDepth) {
+    while (v >= 0 && dd < P.max_depth) {
       chain[dd++] = v;
       v = __ldg(&P.parent[v]);
     }
     n_chain = dd;
+    int si = 0;
+    for (int k = 1; k <= n; ++k)
+      for (int o = 0; o + k <= n; ++o) {
+        sub_o[si] = static_cast<int8_t>(o);
+        sub_k[si] = static_cast<int8_t>(k);
+        ++si;
+      }
   }
   __syncthreads();
   const int depth = n_chain;
+  const int md = P.max_depth;
   const int n_win = c1 - c0 + 1;
   auto win_bounds = [&](int c, int& start, int& wl) {
     int end;
@@ -165,11 +174,11 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
     }
     wl = end - start + 1;
   };
-  for (int t = threadIdx.x; t < n_win * kSub * depth; t += blockDim.x) {
+  for (int t = threadIdx.x; t < n_win * n_sub * depth; t += blockDim.x) {
     const int dd = t % depth;
-    const int si = (t / depth) % kSub;
-    const int wi = t / (depth * kSub);
-    const int o = si / kMaxNgram, k = si % kMaxNgram + 1;
+    const int si = (t / depth) % n_sub;
+    const int wi = t / (depth * n_sub);
+    const int o = sub_o[si], k = sub_k[si];
     int start, wl;
     win_bounds(c0 + wi, start, wl);
     int32_t r = -1;
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
       for (int j = 0; j < k; ++j) key[j] = tok[start + o + j];
       r = plot_find(P, static_cast<uint32_t>(chain[dd]), key, static_cast<uint32_t>(k));
     }
-    probe[(wi * kSub + si) * kMaxDepth + dd] = r;
+    probe[(wi * n_sub + si) * md + dd] = r;
   }
   __syncthreads();
   // ---- phase 1b: resolve_window (retrieval.cpp:23-69): for position p of the window, the
@@ -193,7 +202,9 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
       const int o_lo = p + 1 >= k ? p + 1 - k : 0;
       const int o_hi = p < wl - k ? p : wl - k;
       for (int o = o_lo; o <= o_hi && row < 0; ++o) {
-        const int32_t* pr = &probe[(wi * kSub + o * kMaxNgram + (k - 1)) * kMaxDepth];
+        // sub-gram index of (o, k): sub-grams are ordered by k, then o
+        const int si = (k - 1) * n - (k - 1) * (k - 2) / 2 + o;
+        const int32_t* pr = &probe[(wi * n_sub + si) * md];
         for (int dd = 0; dd < depth; ++dd) {
           if (pr[dd] >= 0) {
             row = pr[dd] + (p - o);
@@ -271,14 +282,18 @@ __global__ void __launch_bounds__(256) retrieve_kernel(PlotDev P, const uint32_t
         o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
       }
       uint2 pk;
+      // f64 -> f32 -> 16-bit with hardware conversions (the f64 values are the exact
+      // Eq. 2 result; the 16-bit copy is the GEMM operand)
+      const float f0 = __double2float_rn(a0), f1 = __double2float_rn(a1);
+      const float f2 = __double2float_rn(a2), f3 = __double2float_rn(a3);
       if (bf16) {
-        __nv_bfloat162 x = __halves2bfloat162(__double2bfloat16(a0), __double2bfloat16(a1));
-        __nv_bfloat162 y = __halves2bfloat162(__double2bfloat16(a2), __double2bfloat16(a3));
+        __nv_bfloat162 x = __floats2bfloat162_rn(f0, f1);
+        __nv_bfloat162 y = __floats2bfloat162_rn(f2, f3);
         pk.x = *reinterpret_cast<uint32_t*>(&x);
         pk.y = *reinterpret_cast<uint32_t*>(&y);
       } else {
-        __half2 x = __halves2half2(__double2half(a0), __double2half(a1));
-        __half2 y = __halves2half2(__double2half(a2), __double2half(a3));
+        __half2 x = __floats2half2_rn(f0, f1);
+        __half2 y = __floats2half2_rn(f2, f3);
         pk.x = *reinterpret_cast<uint32_t*>(&x);
         pk.y = *reinterpret_cast<uint32_t*>(&y);
       }
@@ -555,7 +570,10 @@ void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* len
   if (n_req <= 0) return;
   HMI_CHECK(plot.d % 128 == 0, HMI_CONFIG_ERROR, "retrieve: d must be a multiple of 128");
   dim3 grid(n_req, (S + kRetrieveChunk - 1) / kRetrieveChunk);
-  retrieve_kernel<<<grid, 256, 0, stream>>>(plot, tokens, lens, req_version, S, causal, h16,
+  const int n = plot.ngram;
+  const size_t smem = static_cast<size_t>(kRetrieveChunk + kMaxNgram) * (n * (n + 1) / 2) *
+                      plot.max_depth * sizeof(int32_t);
+  retrieve_kernel<<<grid, 256, smem, stream>>>(plot, tokens, lens, req_version, S, causal, h16,
                                                 precision, h64_debug, gather, levels, err);
   HMI_CUDA(cudaGetLastError());
 }
