@@ -1,0 +1,282 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K3 on the 5th-gen tensor cores, padded length 128 (the hBERT / hGPT serving shape).
+//
+// Same math as attention() (proj/src/transformer/model.cpp:39-74): per (request, head)
+// S = Q K^T / sqrt(64) over keys j < limit (valid_len, or i + 1 when causal), softmax,
+// ctx = P V. One persistent CTA per SM walks (request, head) items, double-buffered:
+//
+//   warp 0 (lane 0): TMA   Q, K, V tiles (128 x 64 16-bit, SWIZZLE_128B) -> smem[buf]
+//   warp 1 (lane 0): MMA   S[buf] = Q K^T   tcgen05 M=128 N=128 K=64 -> TMEM
+//                          O[buf] = P V     tcgen05 M=128 N=64 K=128, V as MN-major B
+//   warps 2..5     : softmax, one query row per thread: TMEM S row -> mask / max /
+//                    exp2 / sum -> 16-bit P row into swizzled smem (UMMA A operand);
+//                    epilogue: TMEM O row * 1/sum -> 16-bit -> smem -> TMA store
+//
+// Barriers per buffer: load_full (TMA tx), load_empty (MMA commit after P.V),
+// s_full (MMA commit), p_full (4 softmax warps), o_full (MMA commit), o_empty (4 warps).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+#include "sm100.cuh"
+
+namespace hmi_b200 {
+
+namespace {
+
+constexpr int kTcThreads = 192;
+constexpr int kT = 128 * 128;                // one 128 x 64 16-bit tile (bytes)
+constexpr int kBufBytes = 3 * kT + 2 * kT;   // Q, K, V + P (128 x 128 16-bit as two tiles)
+constexpr int kOStage = kT;                  // output staging tile
+constexpr int kSmem = 1024 + 2 * kBufBytes + kOStage + 256;
+
+// Shared-memory descriptor of an MN-major SWIZZLE_128B operand whose MN extent is one
+// 128-byte atom (64 x 16-bit): 8-row K groups are 1024 B apart.
+__device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(8192 >> 4) << 16;  // LBO: next MN atom (unused, N = 64)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO: next 8 K rows
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ uint32_t sw(int r, int chunk) {
+  return static_cast<uint32_t>(r * 128 + ((chunk ^ (r & 7)) << 4));
+}
+
+template <bool kBf16>
+__device__ __forceinline__ uint32_t pk2(float a, float b) {
+  if constexpr (kBf16) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
+    const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_ctx,
+    const int* __restrict__ lens, int n_items, int heads, int d, int causal, float scale_log2) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* base = raw + ((1024 - (smem_u32(raw) & 1023)) & 1023);
+  uint8_t* ostg = base + 2 * kBufBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ostg + kOStage);
+  uint64_t* load_full = bar;        // [2]
+  uint64_t* load_empty = bar + 2;   // [2]
+  uint64_t* s_full = bar + 4;       // [2]
+  uint64_t* p_full = bar + 6;       // [2]
+  uint64_t* o_full = bar + 8;       // [2]
+  uint64_t* o_empty = bar + 10;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_qkv);
+    tma_prefetch_desc(&map_ctx);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&load_full[b], 1);
+      mbar_init(&load_empty[b], 1);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 4);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S[0] 0..127, S[1] 128..255, O[0] 256..319, O[1] 320..383
+  const int my_first = blockIdx.x, step = gridDim.x;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int k = 0;
+      for (int item = my_first; item < n_items; item += step, ++k) {
+        const int b = k & 1;
+        const uint32_t ph = (k >> 1) & 1;
+        mbar_wait(&load_empty[b], ph ^ 1);
+        const int req = item / heads, h = item - req * heads;
+        uint8_t* dst = base + b * kBufBytes;
+        mbar_arrive_expect_tx(&load_full[b], 3 * kT);
+        tma_load_2d(dst, &map_qkv, &load_full[b], h * 64, req * 128);
+        tma_load_2d(dst + kT, &map_qkv, &load_full[b], d + h * 64, req * 128);
+        tma_load_2d(dst + 2 * kT, &map_qkv, &load_full[b], 2 * d + h * 64, req * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = idesc_f16(128, 128, kBf16 ? 1u : 0u);
+      const uint32_t id_o = idesc_f16(128, 64, kBf16 ? 1u : 0u) | (1u << 16);  // B MN-major
+      int k = 0;
+      for (int item = my_first; item < n_items; item += step, ++k) {
+        const int b = k & 1;
+        const uint32_t ph = (k >> 1) & 1;
+        uint8_t* buf = base + b * kBufBytes;
+        mbar_wait(&load_full[b], ph);
+        tc_fence_after();
+        // S[b] = Q K^T (K = 64 = 4 x 16; +32 B inside the swizzle atom per step)
+        const uint64_t qd = sdesc_k_sw128(smem_u32(buf));
+        const uint64_t kd = sdesc_k_sw128(smem_u32(buf + kT));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) umma_f16(tmem + b * 128, qd + 2 * kk, kd + 2 * kk, id_s, kk);
+        umma_commit(&s_full[b]);
+        // O[b] = P V once the softmax wrote P and the epilogue released O[b]
+        mbar_wait(&p_full[b], ph);
+        mbar_wait(&o_empty[b], ph ^ 1);
+        tc_fence_after();
+        const uint32_t p0 = smem_u32(buf + 3 * kT), vb = smem_u32(buf + 2 * kT);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // 16 keys per step
+          const uint64_t pd = sdesc_k_sw128(p0 + (kk >> 2) * kT) + 2 * (kk & 3);
+          const uint64_t vd = sdesc_mn_sw128(vb + kk * 2048);
+          umma_f16(tmem + 256 + b * 64, pd, vd, id_o, kk);
+        }
+        umma_commit(&o_full[b]);
+        umma_commit(&load_empty[b]);  // Q, K, V, P of buffer b consumed
+      }
+    }
+  } else {
+    const uint32_t q = warp & 3;      // TMEM lane quarter
+    const int r = static_cast<int>(q * 32 + lane);  // query row owned by this thread
+    const uint32_t lane_off = (q * 32) << 16;
+    float l_prev = 0.f;
+    int prev_item = -1, prev_b = 0;
+    uint32_t prev_ph = 0;
+    auto epilogue = [&](int item, int b, uint32_t ph, float l) {
+      mbar_wait(&o_full[b], ph);
+      tc_fence_after();
+      uint32_t o[64];
+      tmem_ld_32x32b_x32(tmem + lane_off + 256 + b * 64, *reinterpret_cast<uint32_t(*)[32]>(o));
+      tmem_ld_32x32b_x32(tmem + lane_off + 256 + b * 64 + 32,
+                         *reinterpret_cast<uint32_t(*)[32]>(o + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[b]);
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      // the staging tile is free once the previous item's store has read it; only the
+      // thread that issued that store can wait on it
+      if (q == 0 && lane == 0) tma_store_wait_read<0>();
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 v;
+        v.x = pk2<kBf16>(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv);
+        v.y = pk2<kBf16>(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv);
+        v.z = pk2<kBf16>(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv);
+        v.w = pk2<kBf16>(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv);
+        *reinterpret_cast<uint4*>(ostg + sw(r, c)) = v;
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (q == 0 && lane == 0) {
+        const int req = item / heads, h = item - req * heads;
+        tma_store_2d(&map_ctx, ostg, h * 64, req * 128);
+        tma_store_commit();
+      }
+    };
+    int k = 0;
+    for (int item = my_first; item < n_items; item += step, ++k) {
+      const int b = k & 1;
+      const uint32_t ph = (k >> 1) & 1;
+      const int req = item / heads;
+      const int valid = __ldg(&lens[req]);
+      const int lim = causal ? r + 1 : valid;
+      mbar_wait(&s_full[b], ph);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t t[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + b * 128 + 32 * j, t);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[32 * j + i] = __uint_as_float(t[i]);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 128; ++j) {
+        s[j] = j < lim ? s[j] * scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[j]);
+      }
+      const float mb = mx == -INFINITY ? 0.f : mx;
+      float l = 0.f;
+#pragma unroll
+      for (int j = 0; j < 128; ++j) {
+        s[j] = exp2f(s[j] - mb);
+        l += s[j];
+      }
+      // P row r -> two SWIZZLE_128B K-major tiles (keys 0-63, 64-127) of buffer b
+      uint8_t* P = base + b * kBufBytes + 3 * kT;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        uint4 v;
+        v.x = pk2<kBf16>(s[8 * c + 0], s[8 * c + 1]);
+        v.y = pk2<kBf16>(s[8 * c + 2], s[8 * c + 3]);
+        v.z = pk2<kBf16>(s[8 * c + 4], s[8 * c + 5]);
+        v.w = pk2<kBf16>(s[8 * c + 6], s[8 * c + 7]);
+        *reinterpret_cast<uint4*>(P + (c >> 3) * kT + sw(r, c & 7)) = v;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      // the previous item's output is ready by now (its P.V ran while we did this softmax)
+      if (prev_item >= 0) epilogue(prev_item, prev_b, prev_ph, l_prev);
+      prev_item = item;
+      prev_b = b;
+      prev_ph = ph;
+      l_prev = l;
+    }
+    if (prev_item >= 0) epilogue(prev_item, prev_b, prev_ph, l_prev);
+    if (q == 0 && lane == 0) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+void launch_attention_tc(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
+                         cudaStream_t stream) {
+  if (n_req <= 0) return;
+  const float scale_log2 = 1.4426950408889634f / sqrtf(64.0f);
+  const int items = n_req * heads;
+  const int grid = items < device_sm_count() ? items : device_sm_count();
+  static bool configured[2] = {false, false};
+  const int bf = p.precision == 1 ? 1 : 0;
+  if (!configured[bf]) {
+    if (bf) {
+      HMI_CUDA(cudaFuncSetAttribute(attention_tc_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    } else {
+      HMI_CUDA(cudaFuncSetAttribute(attention_tc_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    }
+    configured[bf] = true;
+  }
+  if (bf) {
+    attention_tc_kernel<true><<<grid, kTcThreads, kSmem, stream>>>(p.map_qkv, p.map_ctx, lens, items,
+                                                                   heads, p.d, causal, scale_log2);
+  } else {
+    attention_tc_kernel<false><<<grid, kTcThreads, kSmem, stream>>>(p.map_qkv, p.map_ctx, lens, items,
+                                                                    heads, p.d, causal, scale_log2);
+  }
+  HMI_CUDA(cudaGetLastError());
+}
+
+}  // namespace hmi_b200

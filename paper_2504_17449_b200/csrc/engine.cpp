@@ -264,6 +264,7 @@ struct Ctx {
   // LayerNorm placement: 0 folded into the consumers (default), 1 separate K4 kernels
   // (HMI_LN_MODE=unfused), 2 cluster-reduced GEMM epilogues (HMI_LN_MODE=cluster)
   int ln_mode = 0;
+  bool attn_tc = true;  // tcgen05 attention for padded length 128 (HMI_ATTN=mma selects mma.sync)
   DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
   static constexpr int kStatsLd = kStatsStride;
   int stats1_bn = 0, stats2_bn = 0, stats1_n = 0, stats2_n = 0;
@@ -784,7 +785,9 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     const bool last = l == L - 1;
     timed(P_QKV, s, [&] { launch_gemm(w.qkv, rows, s); });
     timed(P_ATTN, s, [&] {
-      if (S == 128) {
+      if (S == 128 && attn_tc) {
+        launch_attention_tc(attn, d_lens.p, static_cast<int>(n_req), heads, causal, s);
+      } else if (S == 128) {
         launch_attention_s128(attn, d_lens.p, static_cast<int>(n_req), heads, causal, s);
       } else {
         launch_attention(qkv16.p, ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal,
@@ -1101,6 +1104,7 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       const std::string m(env);
       c.ln_mode = m == "unfused" ? 1 : m == "cluster" ? 2 : 0;
     }
+    if (const char* env = std::getenv("HMI_ATTN")) c.attn_tc = std::string(env) != "mma";
     c.d_stats1.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.d_stats2.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.build_plans();

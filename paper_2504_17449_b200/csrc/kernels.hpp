@@ -65,6 +65,9 @@ struct AttnPlan {
 AttnPlan make_attention_plan(const void* qkv, void* ctx, int max_rows, int d, int precision);
 void launch_attention_s128(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
                            cudaStream_t stream);
+// Same, on tcgen05 (S and O in TMEM, softmax warps write P to smem): attention_tc.cu
+void launch_attention_tc(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
+                         cudaStream_t stream);
 
 // K3: attention core.
 void launch_attention(const void* qkv, void* ctx, const int* lens, int n_req, int S, int d,

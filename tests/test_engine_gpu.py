@@ -125,6 +125,25 @@ def test_layernorm_placements_agree(c1, monkeypatch, mode):
     assert np.abs(folded.scores - other.scores).max() < 1e-2
 
 
+@pytest.mark.parametrize("causal", [0, 1])
+def test_attention_tc_matches_mma(monkeypatch, causal):
+    """tcgen05 attention (default for padded length 128) vs the mma.sync kernel."""
+    cfg = oracle.Config(256, 4, 2, 2, 1024, 1024, causal, 3, 31)
+    kind = E.HEAD_LM if causal else E.HEAD_CLS
+    w = World(cfg, n_tasks=8, r=16, labels=8, max_batch=16, head_kind=kind)
+    inst, toks, lens = w.requests(37, 16, 128, min_len=1)
+    tc = w.eng.infer_batch(inst, toks, lens)
+    w.eng.close()
+    monkeypatch.setenv("HMI_ATTN", "mma")
+    w2 = World(cfg, n_tasks=8, r=16, labels=8, max_batch=16, head_kind=kind)
+    mma = w2.eng.infer_batch(inst, toks, lens)
+    w2.eng.close()
+    ref_scores, ref_labels, _ = w2.oracle_batch(inst, toks, lens)
+    assert logit_error(tc.scores, ref_scores) <= TOL
+    assert (tc.labels == ref_labels).mean() >= 0.999
+    assert np.abs(tc.scores - mma.scores).max() < 1e-2
+
+
 def test_routing_and_vocab_errors(c1):
     inst, toks, lens = c1.requests(3, 2, 16)
     bad = inst.copy()
