@@ -9,9 +9,11 @@
 //   warp 0 (lane 0): TMA   Q, K, V tiles (128 x 64 16-bit, SWIZZLE_128B) -> smem[buf]
 //   warp 1 (lane 0): MMA   S[buf] = Q K^T   tcgen05 M=128 N=128 K=64 -> TMEM
 //                          O[buf] = P V     tcgen05 M=128 N=64 K=128, V as MN-major B
-//   warps 2..5     : softmax, one query row per thread: TMEM S row -> mask / max /
-//                    exp2 / sum -> 16-bit P row into swizzled smem (UMMA A operand);
-//                    epilogue: TMEM O row * 1/sum -> 16-bit -> smem -> TMA store
+//   warps 2..9     : softmax, two groups of 4 warps (group g serves buffer g, i.e. every
+//                    other item, so two items' softmax overlap); one query row per
+//                    thread: TMEM S row -> mask / max / exp2 / sum -> 16-bit P row into
+//                    swizzled smem (UMMA A operand); epilogue: TMEM O row * 1/sum ->
+//                    16-bit -> smem -> TMA store
 //
 // Barriers per buffer: load_full (TMA tx), load_empty (MMA commit after P.V),
 // s_full (MMA commit), p_full (4 softmax warps), o_full (MMA commit), o_empty (4 warps).
@@ -27,11 +29,11 @@ namespace hmi_b200 {
 
 namespace {
 
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // TMA warp, MMA warp, 2 groups x 4 softmax warps
 constexpr int kT = 128 * 128;                // one 128 x 64 16-bit tile (bytes)
 constexpr int kBufBytes = 3 * kT + 2 * kT;   // Q, K, V + P (128 x 128 16-bit as two tiles)
 constexpr int kOStage = kT;                  // output staging tile
-constexpr int kSmem = 1024 + 2 * kBufBytes + kOStage + 256;
+constexpr int kSmem = 1024 + 2 * kBufBytes + 2 * kOStage + 256;
 
 // Shared-memory descriptor of an MN-major SWIZZLE_128B operand whose MN extent is one
 // 128-byte atom (64 x 16-bit): 8-row K groups are 1024 B apart.
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
   extern __shared__ uint8_t raw[];
   uint8_t* base = raw + ((1024 - (smem_u32(raw) & 1023)) & 1023);
   uint8_t* ostg = base + 2 * kBufBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ostg + kOStage);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ostg + 2 * kOStage);
   uint64_t* load_full = bar;        // [2]
   uint64_t* load_empty = bar + 2;   // [2]
   uint64_t* s_full = bar + 4;       // [2]
@@ -147,6 +149,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
     }
   } else {
     const uint32_t q = warp & 3;      // TMEM lane quarter
+    const int group = static_cast<int>(warp - 2) >> 2;  // serves buffer `group`
+    uint8_t* gstg = ostg + group * kOStage;
     const int r = static_cast<int>(q * 32 + lane);  // query row owned by this thread
     const uint32_t lane_off = (q * 32) << 16;
     float l_prev = 0.f;
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
       // the staging tile is free once the previous item's store has read it; only the
       // thread that issued that store can wait on it
       if (q == 0 && lane == 0) tma_store_wait_read<0>();
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + group, 128);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint4 v;
@@ -175,19 +179,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
         v.y = pk2<kBf16>(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv);
         v.z = pk2<kBf16>(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv);
         v.w = pk2<kBf16>(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv);
-        *reinterpret_cast<uint4*>(ostg + sw(r, c)) = v;
+        *reinterpret_cast<uint4*>(gstg + sw(r, c)) = v;
       }
       fence_proxy_async_smem();
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + group, 128);
       if (q == 0 && lane == 0) {
         const int req = item / heads, h = item - req * heads;
-        tma_store_2d(&map_ctx, ostg, h * 64, req * 128);
+        tma_store_2d(&map_ctx, gstg, h * 64, req * 128);
         tma_store_commit();
       }
     };
-    int k = 0;
-    for (int item = my_first; item < n_items; item += step, ++k) {
-      const int b = k & 1;
+    int k = group;
+    for (int item = my_first + group * step; item < n_items; item += 2 * step, k += 2) {
+      const int b = k & 1;  // == group
       const uint32_t ph = (k >> 1) & 1;
       const int req = item / heads;
       const int valid = __ldg(&lens[req]);
