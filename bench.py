@@ -244,6 +244,9 @@ def bench_ours(args, wl):
     import torch
 
     world_size, rank, local = dist_setup()
+    # one process per GPU; when more ranks than GPUs are launched (logic check on a
+    # single-GPU box) ranks share devices round-robin
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     from paper_2504_17449_b200 import engine as E
     from paper_2504_17449_b200.workload import World
