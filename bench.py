@@ -101,11 +101,19 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
 
+        global _BACKEND
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if _cuda() else "gloo")
+        # NCCL needs one GPU per rank; ranks sharing a device (logic check on a small box)
+        # or CPU-only runs use gloo. Only the barrier and the timing max go through it.
+        _BACKEND = "nccl" if _cuda() and world <= torch.cuda.device_count() else "gloo"
+        dist.init_process_group(_BACKEND)
     return world, rank, local
+
+
+_BACKEND = "gloo"
 
 
 def _cuda() -> bool:
@@ -127,7 +135,7 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if _cuda() else "cpu")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if _BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -253,6 +253,10 @@ struct Ctx {
   size_t chunk_left = 0;
   uint64_t bytes_copied = 0;
   uint64_t n_launches = 0, n_batches = 0, n_copies = 0;
+  std::vector<void*> cp_dst, cp_src;
+  std::vector<size_t> cp_size;
+  bool use_batch_copy = std::getenv("HMI_BATCH_COPY") == nullptr ||
+                        std::string(std::getenv("HMI_BATCH_COPY")) != "0";
   std::vector<cudaEvent_t> ev_layer;
   // staging / in-flight batches
   Staging stg[kStaging];
@@ -716,13 +720,39 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   }
 
   // ---- copy stream: adapter H2D into HBM slots, one event per layer
+  // One cudaMemcpyBatchAsync per layer: a miss-heavy batch issues hundreds of
+  // slot-sized copies, and per-call submission cost (not PCIe) bounded them.
   for (int l = 0; l < L; ++l) {
-    for (const auto& [task, slot] : loads[l]) {
-      HMI_CUDA(cudaMemcpyAsync(arena.p + static_cast<size_t>(slot) * slot_bytes,
-                               store[task] + static_cast<size_t>(l) * slot_bytes, slot_bytes,
-                               cudaMemcpyHostToDevice, copy));
-      bytes_copied += slot_bytes;
-      ++n_copies;
+    const size_t n = loads[l].size();
+    if (n != 0) {
+      cp_dst.resize(n);
+      cp_src.resize(n);
+      cp_size.assign(n, slot_bytes);
+      for (size_t i = 0; i < n; ++i) {
+        cp_dst[i] = arena.p + static_cast<size_t>(loads[l][i].second) * slot_bytes;
+        cp_src[i] = store[loads[l][i].first] + static_cast<size_t>(l) * slot_bytes;
+      }
+      bool batched = false;
+      if (n > 1 && use_batch_copy) {
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+        size_t attr_idx = 0, fail_idx = 0;
+        const cudaError_t e = cudaMemcpyBatchAsync(cp_dst.data(), cp_src.data(), cp_size.data(),
+                                                   n, &attr, &attr_idx, 1, &fail_idx, copy);
+        if (e == cudaSuccess) {
+          batched = true;
+        } else {
+          (void)cudaGetLastError();
+          use_batch_copy = false;  // driver without batch copies: per-copy path from now on
+        }
+      }
+      if (!batched) {
+        for (size_t i = 0; i < n; ++i)
+          HMI_CUDA(cudaMemcpyAsync(cp_dst[i], cp_src[i], slot_bytes, cudaMemcpyHostToDevice, copy));
+      }
+      bytes_copied += n * slot_bytes;
+      n_copies += n;
     }
     HMI_CUDA(cudaEventRecord(ev_layer[l], copy));
   }

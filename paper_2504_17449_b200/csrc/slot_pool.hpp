@@ -105,6 +105,13 @@ class SlotPool {
   std::vector<int32_t> free_slots_;
   std::map<uint32_t, TaskInfo> tasks_;
   std::map<uint32_t, Residency> resident_;
+  // (last_used, task) of every resident record: the reference scans all residents for the
+  // minimum last_used (device_pool.cpp:25-35); ticks are unique, so walking this ordered
+  // index from the front and skipping protected / pinned records picks the same victim
+  // in O(k log n) instead of O(n).
+  std::set<std::pair<uint64_t, uint32_t>> lru_;
+  void set_last_used(uint32_t task, Residency& r, uint64_t tick);
+  void forget(uint32_t task, const Residency& r) { lru_.erase({r.last_used, task}); }
   uint64_t resident_bytes_ = 0;
   uint64_t max_resident_bytes_ = 0;
   uint64_t tick_ = 0;
