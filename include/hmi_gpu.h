@@ -69,6 +69,9 @@ typedef struct hmi_gpu_options {
                              accounting (device_pool.hpp:40, adapter_set.hpp:24-27);
                              0 = room for every task (max_tasks)                          */
   uint32_t max_tasks, max_instances, max_heads, max_versions;
+  uint32_t max_new_tokens; /* causal mode: longest hmi_gpu_generate continuation; > 0 keeps
+                              every layer's prompt keys/values resident (KV cache)          */
+  uint32_t reserved;
 } hmi_gpu_options;
 
 typedef struct hmi_gpu_ctx hmi_gpu_ctx;
@@ -107,7 +110,13 @@ int hmi_gpu_replace_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapt
 int hmi_gpu_unregister_task(hmi_gpu_ctx* ctx, uint32_t task_idx);
 
 /* OutputHead (weights.hpp:45-53): kind 0 cls_classify, 1 token_tag,
- * 2 lm_logits; w [hidden x labels] f32, b [labels] f32.                      */
+ * 2 lm_logits; w [hidden x labels] f32, b [labels] f32.
+ * An lm_logits head wider than max_labels (a vocabulary head, e.g. hGPT-2's
+ * 50,257) is a "wide" head: its logits come from a tcgen05 GEMM over the
+ * batch's final rows, the top-8 candidates are rescored in f64 from the f32
+ * weights, and hmi_gpu_infer_batch reports label = argmax token and
+ * scores[i*max_labels] = its logit (other columns 0). One wide head may be
+ * shared by any number of instances; a batch may use at most one.           */
 int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, uint32_t labels,
                           const float* w, const float* b);
 
@@ -151,6 +160,20 @@ int hmi_gpu_infer_batch_device(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t*
                                const uint32_t* d_tokens, uint32_t stride,
                                const uint32_t* d_lens, uint32_t max_len, float* d_scores,
                                int32_t* d_labels);
+/* Greedy generation for causal (hGPT) models with a wide lm head: n_new
+ * tokens per request, token k+1 = argmax lm_logits at the last row of the
+ * prompt extended by tokens 1..k (apply_head, model.cpp:151-168; the reference
+ * has no decode loop). The prompt runs as one batched forward
+ * whose per-layer keys/values stay in HBM; each further token is one batched
+ * single-row step per request (on-device causal retrieval of the new
+ * position, cached attention, per-row tenant adapters). Every request must be
+ * bound to the same wide lm head. out_tokens / out_logits: [n_req x n_new]
+ * (out_logits nullable: the chosen token's f64-rescored logit).
+ * Errors: n_new > max_new_tokens or encoder mode -> CONFIG.                  */
+int hmi_gpu_generate(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                     const uint32_t* tokens, uint32_t stride, const uint32_t* lens,
+                     uint32_t n_new, int32_t* out_tokens, float* out_logits);
+
 /* Waits for every enqueued batch; returns the first device-side error. */
 int hmi_gpu_synchronize(hmi_gpu_ctx* ctx);
 /* cudaStream_t of the compute stream (for event timing by the caller). */

@@ -82,7 +82,8 @@ class Options(ctypes.Structure):
                 ("max_labels", ctypes.c_uint32), ("pipeline_mode", ctypes.c_uint32),
                 ("pool_bytes", ctypes.c_uint64), ("max_tasks", ctypes.c_uint32),
                 ("max_instances", ctypes.c_uint32), ("max_heads", ctypes.c_uint32),
-                ("max_versions", ctypes.c_uint32)]
+                ("max_versions", ctypes.c_uint32), ("max_new_tokens", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
 
 
 class LoadRecord(ctypes.Structure):
@@ -116,6 +117,7 @@ def _sig(L):
     L.hmi_gpu_infer_batch.argtypes = [vp, u32, u32p, u32p, u32, u32p, f32p, i32p, i32p,
                                       P(LoadRecord), u32, u32p, u32, u32p]
     L.hmi_gpu_infer_batch_device.argtypes = [vp, u32, u32p, vp, u32, vp, u32, vp, vp]
+    L.hmi_gpu_generate.argtypes = [vp, u32, u32p, u32p, u32, u32p, u32, i32p, f32p]
     L.hmi_gpu_synchronize.argtypes = [vp]
     L.hmi_gpu_stream.argtypes = [vp]
     L.hmi_gpu_stream.restype = vp

@@ -1,0 +1,432 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Causal (hGPT) generation: the wide lm head and the single-row decode step.
+//
+// The reference has no decode loop (SPEC.md:188 lists caching as a non-goal);
+// greedy generation here is defined as repeated causal forwards, token t+1 =
+// argmax of apply_head(lm_logits) at row valid_len - 1 (model.cpp:151-168,
+// first max wins, :122-128) of the sequence extended by token t. In causal mode
+// row i reads only keys j <= i (model.cpp:48-51) and PLOT rows of the window
+// ending at i (retrieval.cpp:92-99), so earlier rows never change and their
+// keys / values are cached: one new row per request per step.
+//
+//   lm_gather_kernel       final row (valid_len - 1) of each request, LayerNorm'd
+//                          (f64, ops.cpp:92-116) when the stack leaves it pre-norm;
+//                          f32 copy for rescoring, 16-bit copy as the GEMM operand
+//   (tcgen05 GEMM)         logits = h . W_lm + b over the padded vocabulary
+//   lm_argmax_kernel       top-8 candidates of the 16-bit-operand logits, rescored
+//                          in f64 from the f32 row and the f32 head weights; first
+//                          max of the rescored values; appends the token
+//   attn_decode_kernel     one query row per (request, head) against the cached
+//                          keys (prefill rows + generated rows); appends its k, v
+//   adapter_rows_ln_kernel per-row tenant adapter (each decode row may belong to a
+//                          different tenant: the slot is gathered per row), skip
+//                          and residual adds, LayerNorm1 (model.cpp:13-24, 87-92)
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "decode.hpp"
+
+namespace hmi_b200 {
+
+namespace {
+
+__device__ __forceinline__ float ld16(const uint16_t* p, long long i, int bf16) {
+  const uint16_t u = p[i];
+  if (bf16) return __uint_as_float(static_cast<uint32_t>(u) << 16);
+  return __half2float(__ushort_as_half(u));
+}
+
+__device__ __forceinline__ uint16_t st16(float v, int bf16) {
+  if (bf16) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  return __half_as_ushort(__float2half_rn(v));
+}
+
+// unpack 8 16-bit values of a uint4 into floats
+__device__ __forceinline__ void unpack8(const uint4& u, float* f, int bf16) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (bf16) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    } else {
+      const __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      const float2 t = __half22float2(h);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum_t(T v, T* scratch) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  T t = 0;
+  for (int w = 0; w < nw; ++w) t += scratch[w];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ float block_max_f(float v, float* scratch) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  float t = -INFINITY;
+  for (int w = 0; w < nw; ++w) t = fmaxf(t, scratch[w]);
+  __syncthreads();
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lm_gather_kernel(const uint16_t* __restrict__ y16,
+                                                        const float* __restrict__ h32,
+                                                        const float* __restrict__ g,
+                                                        const float* __restrict__ be,
+                                                        const int* __restrict__ lens, int S, int d,
+                                                        int bf16, float* __restrict__ out32,
+                                                        uint16_t* __restrict__ out16) {
+  extern __shared__ double xs[];
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  const long long rbase = (static_cast<long long>(b) * S + lens[b] - 1) * d;
+  if (y16) {
+    double s1 = 0.0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      xs[j] = ld16(y16, rbase + j, bf16);
+      s1 += xs[j];
+    }
+    const double mean = block_sum_t(s1, red) / d;
+    double s2 = 0.0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const double t = xs[j] - mean;
+      s2 += t * t;
+    }
+    const double inv = 1.0 / sqrt(block_sum_t(s2, red) / d + 1e-5);
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const float v = static_cast<float>((xs[j] - mean) * inv * g[j] + be[j]);
+      out32[static_cast<long long>(b) * d + j] = v;
+      out16[static_cast<long long>(b) * d + j] = st16(v, bf16);
+    }
+  } else {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const float v = h32[rbase + j];
+      out32[static_cast<long long>(b) * d + j] = v;
+      out16[static_cast<long long>(b) * d + j] = st16(v, bf16);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kTopK = 8;
+constexpr int kArgThreads = 256;
+
+__global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) {
+  __shared__ float cv[kArgThreads * kTopK];
+  __shared__ int ci[kArgThreads * kTopK];
+  __shared__ int cand[kTopK];
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  if (A.req_head && A.req_head[b] != A.head) return;  // another head serves this request
+  const float* lg = A.logits + static_cast<long long>(b) * A.ld;
+  // per-thread top-k (sorted descending; ties keep the lower index first)
+  float v[kTopK];
+  int ix[kTopK];
+#pragma unroll
+  for (int k = 0; k < kTopK; ++k) {
+    v[k] = -INFINITY;
+    ix[k] = 0x7fffffff;
+  }
+  for (int j = threadIdx.x; j < A.V; j += blockDim.x) {
+    const float x = lg[j];
+    if (x > v[kTopK - 1]) {
+      int k = kTopK - 1;
+      while (k > 0 && x > v[k - 1]) {
+        v[k] = v[k - 1];
+        ix[k] = ix[k - 1];
+        --k;
+      }
+      v[k] = x;
+      ix[k] = j;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kTopK; ++k) {
+    cv[threadIdx.x * kTopK + k] = v[k];
+    ci[threadIdx.x * kTopK + k] = ix[k];
+  }
+  __syncthreads();
+  // warp 0 extracts the block's top-k by repeated arg-max over the candidates
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    constexpr int per = kArgThreads * kTopK / 32;
+    for (int k = 0; k < kTopK; ++k) {
+      float bv = -INFINITY;
+      int bi = 0x7fffffff, bp = -1;
+      for (int t = 0; t < per; ++t) {
+        const int p = lane * per + t;
+        const float x = cv[p];
+        const int i = ci[p];
+        if (x > bv || (x == bv && i < bi)) {
+          bv = x;
+          bi = i;
+          bp = p;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+          bp = op;
+        }
+      }
+      if (lane == 0) {
+        cand[k] = bi < A.V ? bi : -1;
+        if (bp >= 0) cv[bp] = -INFINITY;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // f64 rescoring of the candidates: h (f32 row) . W[:, j] + b[j] (project_row, model.cpp:130-136)
+  const float* h = A.h32 + static_cast<long long>(b) * A.d;
+  double best = -INFINITY;
+  int besti = 0x7fffffff;
+  for (int k = 0; k < kTopK; ++k) {
+    const int j = cand[k];
+    if (j < 0) continue;  // uniform across the block
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < A.d; i += blockDim.x)
+      acc += static_cast<double>(h[i]) * static_cast<double>(__ldg(A.w + static_cast<long long>(i) * A.V + j));
+    acc = block_sum_t(acc, red) + static_cast<double>(A.bias[j]);
+    if (acc > best || (acc == best && j < besti)) {
+      best = acc;
+      besti = j;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int tok = besti == 0x7fffffff ? 0 : besti;
+    if (A.labels_out) A.labels_out[b] = tok;
+    if (A.scores_out) A.scores_out[static_cast<long long>(b) * A.scores_ld] = static_cast<float>(best);
+    if (A.gen_tokens) {
+      int pos = A.gen_pos[b];
+      if (A.advance) A.gen_pos[b] = ++pos;
+      A.gen_tokens[static_cast<long long>(b) * A.tok_stride + pos] = static_cast<uint32_t>(tok);
+      A.out_tokens[static_cast<long long>(b) * A.out_ld + A.step] = tok;
+      if (A.out_logits) A.out_logits[static_cast<long long>(b) * A.out_ld + A.step] = static_cast<float>(best);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One CTA per (head, request): q of the new row against keys 0..pos.
+__global__ void __launch_bounds__(128) attn_decode_kernel(AttnDecodeArgs A) {
+  extern __shared__ float sc[];  // [pos + 1] scores, then 4 x 64 partial contexts
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = A.d;
+  const int pos = A.gen_pos[b];
+  const int len0 = A.lens[b];
+  const int nk = pos + 1;
+  const uint16_t* qrow = A.qkv_new + static_cast<long long>(b) * 3 * d;
+  const float scale = A.scale;
+  float q0, q1;
+  {
+    const uint32_t u = reinterpret_cast<const uint32_t*>(qrow + h * 64)[lane];
+    float f[2];
+    if (A.bf16) {
+      f[0] = __uint_as_float(u << 16);
+      f[1] = __uint_as_float(u & 0xffff0000u);
+    } else {
+      const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&u));
+      f[0] = t.x;
+      f[1] = t.y;
+    }
+    q0 = f[0];
+    q1 = f[1];
+  }
+  // append this row's k, v (head slice) to the generated-rows cache
+  uint16_t* trow = A.tail + (static_cast<long long>(b) * A.tail_cap + (pos - len0)) * 2 * d;
+  if (threadIdx.x < 64) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(qrow + d + h * 64);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(trow + h * 64);
+    if (threadIdx.x < 32) dst[threadIdx.x] = src[threadIdx.x];
+    else {
+      reinterpret_cast<uint32_t*>(trow + d + h * 64)[threadIdx.x - 32] =
+          reinterpret_cast<const uint32_t*>(qrow + 2 * d + h * 64)[threadIdx.x - 32];
+    }
+  }
+  auto key_ptr = [&](int j) -> const uint16_t* {
+    if (j == pos) return qrow + d;                         // the new row itself
+    if (j < len0) return A.qkv_prefill + (static_cast<long long>(b) * A.S + j) * 3 * d + d;
+    return A.tail + (static_cast<long long>(b) * A.tail_cap + (j - len0)) * 2 * d;
+  };
+  auto val_ptr = [&](int j) -> const uint16_t* {
+    if (j == pos) return qrow + 2 * d;
+    if (j < len0) return A.qkv_prefill + (static_cast<long long>(b) * A.S + j) * 3 * d + 2 * d;
+    return A.tail + (static_cast<long long>(b) * A.tail_cap + (j - len0)) * 2 * d + d;
+  };
+  auto ld2 = [&](const uint16_t* p) -> float2 {
+    const uint32_t u = reinterpret_cast<const uint32_t*>(p + h * 64)[lane];
+    if (A.bf16) return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+    return __half22float2(*reinterpret_cast<const __half2*>(&u));
+  };
+  for (int j = warp; j < nk; j += 4) {
+    const float2 k = ld2(key_ptr(j));
+    float s = q0 * k.x + q1 * k.y;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sc[j] = s * scale;
+  }
+  __syncthreads();
+  __shared__ float red[32];
+  float m = -INFINITY;
+  for (int j = threadIdx.x; j < nk; j += blockDim.x) m = fmaxf(m, sc[j]);
+  m = block_max_f(m, red);
+  float sum = 0.f;
+  for (int j = threadIdx.x; j < nk; j += blockDim.x) {
+    const float e = __expf(sc[j] - m);
+    sc[j] = e;
+    sum += e;
+  }
+  sum = block_sum_t(sum, red);  // contains the barrier that publishes sc[]
+  float a0 = 0.f, a1 = 0.f;
+  for (int j = warp; j < nk; j += 4) {
+    const float p = sc[j];
+    const float2 v = ld2(val_ptr(j));
+    a0 += p * v.x;
+    a1 += p * v.y;
+  }
+  float* part = sc + ((nk + 3) & ~3);
+  part[warp * 64 + 2 * lane] = a0;
+  part[warp * 64 + 2 * lane + 1] = a1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int c = threadIdx.x;
+    const float o = (part[c] + part[64 + c] + part[128 + c] + part[192 + c]) / sum;
+    A.ctx[static_cast<long long>(b) * d + h * 64 + c] = st16(o, A.bf16);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One CTA per decode row: y = relu(a.Wd + bd).Wu + bu + a + h, x = LN1(y).
+__global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A) {
+  extern __shared__ float sm[];  // a[d], y[d], mid[r_pad]
+  __shared__ float red[32];
+  const int b = blockIdx.x;
+  const int d = A.d, rp = A.r_pad;
+  float* a = sm;
+  float* y = sm + d;
+  float* mid = sm + 2 * d;
+  const int task = A.req_task[b];
+  int slot = task >= 0 ? A.slot_of[static_cast<long long>(task) * A.layers + A.layer] : -1;
+  if (slot < 0) {
+    if (threadIdx.x == 0) atomicExch(A.err, HMI_SCHEDULING_BUG);
+    slot = 0;
+  }
+  const uint8_t* base = A.arena + static_cast<size_t>(slot) * A.slot_bytes;
+  const uint16_t* wd = reinterpret_cast<const uint16_t*>(base);          // [r_pad][d]
+  const uint16_t* wu = wd + static_cast<size_t>(rp) * d;                 // [d][r_pad]
+  const float* bd = reinterpret_cast<const float*>(wu + static_cast<size_t>(d) * rp);
+  const float* bu = bd + rp;
+  const uint16_t* arow = A.a16 + static_cast<long long>(b) * d;
+  const uint16_t* hrow = A.h16 + static_cast<long long>(b) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) a[i] = ld16(arow, i, A.bf16);
+  __syncthreads();
+  // down projection: warp per bottleneck unit, 16-byte weight vectors across the lanes
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < rp; j += nw) {
+    const uint4* w4 = reinterpret_cast<const uint4*>(wd + static_cast<size_t>(j) * d);
+    float acc = 0.f;
+    for (int c = lane; c < d / 8; c += 32) {
+      float f[8];
+      unpack8(__ldg(w4 + c), f, A.bf16);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += a[c * 8 + e] * f[e];
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) mid[j] = fmaxf(acc + bd[j], 0.f);
+  }
+  __syncthreads();
+  // the GEMM path rounds the bottleneck activations to 16 bits; so does this one
+  for (int j = threadIdx.x; j < rp; j += blockDim.x) {
+    const uint16_t u = st16(mid[j], A.bf16);
+    mid[j] = A.bf16 ? __uint_as_float(static_cast<uint32_t>(u) << 16) : __half2float(__ushort_as_half(u));
+  }
+  __syncthreads();
+  // up projection + bias + skip + residual
+  float s1 = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const uint4* w4 = reinterpret_cast<const uint4*>(wu + static_cast<size_t>(i) * rp);
+    float acc = 0.f;
+    for (int c = 0; c < rp / 8; ++c) {
+      float f[8];
+      unpack8(__ldg(w4 + c), f, A.bf16);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
+    }
+    const float v = acc + bu[i] + a[i] + ld16(hrow, i, A.bf16);
+    y[i] = v;
+    s1 += v;
+  }
+  const float mean = block_sum_t(s1, red) / d;
+  float s2 = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float t = y[i] - mean;
+    s2 += t * t;
+  }
+  const float inv = 1.0f / sqrtf(block_sum_t(s2, red) / d + 1e-5f);
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    A.x16[static_cast<long long>(b) * d + i] = st16((y[i] - mean) * inv * A.ln_g[i] + A.ln_b[i], A.bf16);
+}
+
+}  // namespace
+
+void launch_lm_gather(const void* y16, const float* h32, const float* gamma, const float* beta,
+                      const int* lens, int n_req, int S, int d, int precision, float* out32,
+                      void* out16, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  const size_t smem = static_cast<size_t>(d) * sizeof(double);
+  lm_gather_kernel<<<n_req, 256, smem, stream>>>(static_cast<const uint16_t*>(y16), h32, gamma,
+                                                 beta, lens, S, d, precision, out32,
+                                                 static_cast<uint16_t*>(out16));
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_lm_argmax(const LmArgmaxArgs& a, int n_req, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  lm_argmax_kernel<<<n_req, kArgThreads, 0, stream>>>(a);
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_attn_decode(const AttnDecodeArgs& a, int n_req, int heads, int max_keys,
+                        cudaStream_t stream) {
+  if (n_req <= 0) return;
+  const size_t smem = (static_cast<size_t>((max_keys + 3) & ~3) + 4 * 64) * sizeof(float);
+  if (smem > 48 * 1024) {
+    HMI_CUDA(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  }
+  attn_decode_kernel<<<dim3(heads, n_req), 128, smem, stream>>>(a);
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_adapter_rows_ln(const AdapterRowsArgs& a, int n_req, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  HMI_CHECK(a.d % 8 == 0 && a.r_pad % 8 == 0, HMI_CONFIG_ERROR, "adapter rows: d, r_pad % 8");
+  const size_t smem = static_cast<size_t>(2 * a.d + a.r_pad) * sizeof(float);
+  adapter_rows_ln_kernel<<<n_req, 256, smem, stream>>>(a);
+  HMI_CUDA(cudaGetLastError());
+}
+
+}  // namespace hmi_b200

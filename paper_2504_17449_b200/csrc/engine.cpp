@@ -41,6 +41,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "decode.hpp"
 #include "gemm.hpp"
 #include "kernels.hpp"
 #include "slot_pool.hpp"
@@ -214,7 +215,7 @@ struct Ctx {
   std::mutex mu;
 
   std::vector<LayerDev> layers;
-  AttnPlan attn;
+  std::vector<AttnPlan> attn;  // per layer when the prompt KV cache is kept, else one
   // activations
   DevBuf<uint16_t> h16, qkv16, ctx16, a16, mid16, x16, ffn16;
   DevBuf<float> y32, h32;
@@ -272,6 +273,32 @@ struct Ctx {
   DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
   static constexpr int kStatsLd = kStatsStride;
   int stats1_bn = 0, stats2_bn = 0, stats1_n = 0, stats2_n = 0;
+  // causal generation: each layer's prompt q|k|v stays in qkv16 (KV cache); the generated
+  // rows' k|v go to kv_tail [L][max_batch][max_new][2d]
+  bool kv = false;
+  int Bp = 0;  // max_batch rounded up to 128 (rows of the single-row decode GEMMs)
+  DevBuf<uint16_t> qkv_dec, kv_tail, hdec16;
+  DevBuf<float> hdec32, lm_logits;
+  DevBuf<uint32_t> gen_tokens;
+  DevBuf<int32_t> gen_pos, gen_out;
+  DevBuf<float> gen_logit;
+  int gen_stride = 0;
+  struct DecPlans {
+    GemmPlan qkv, oproj, ffn1, ffn2;
+  };
+  std::vector<DecPlans> dec;
+  // wide lm heads (kind 2, labels > max_labels): 16-bit [V_pad][d] GEMM operand + padded bias
+  struct LmHead {
+    int V = 0, V_pad = 0;
+    uint16_t* w16 = nullptr;
+    float* bias = nullptr;
+    GemmPlan plan;
+  };
+  std::map<int, LmHead> lm_heads;
+  uint16_t* qkv_at(int l) const {
+    return qkv16.p + (kv ? static_cast<size_t>(l) * max_rows * 3 * d : 0);
+  }
+  void build_lm_plan(LmHead& h);
   // profiling
   bool prof = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -345,7 +372,10 @@ struct Ctx {
              const uint32_t* tokens_dev, uint32_t stride, const uint32_t* lens_host,
              const uint32_t* lens_dev, uint32_t max_len, float* d_scores_out,
              int32_t* d_labels_out, std::vector<PoolRecord>* records,
-             std::vector<int32_t>* record_layer);
+             std::vector<int32_t>* record_layer, uint32_t n_new = 0);
+  void decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, int wide_head);
+  void launch_lm_head(uint32_t n_req, int S, const LmHead& lm, int wide_head, bool gen,
+                      float* scores, int32_t* labels);
 };
 
 Ctx::~Ctx() {
@@ -357,6 +387,12 @@ Ctx::~Ctx() {
   }
   d_stats1.free();
   d_stats2.free();
+  qkv_dec.free(); kv_tail.free(); hdec16.free(); hdec32.free(); lm_logits.free();
+  gen_tokens.free(); gen_pos.free(); gen_out.free(); gen_logit.free();
+  for (auto& [id, h] : lm_heads) {
+    if (h.w16) cudaFree(h.w16);
+    if (h.bias) cudaFree(h.bias);
+  }
   for (auto& s : stg) {
     for (void* p : {static_cast<void*>(s.inst), static_cast<void*>(s.tokens),
                     static_cast<void*>(s.lens), static_cast<void*>(s.delta),
@@ -411,7 +447,9 @@ void Ctx::convert_adapter(const float* src, uint8_t* dst) const {
 }
 
 void Ctx::build_plans() {
-  attn = make_attention_plan(qkv16.p, ctx16.p, max_rows, d, static_cast<int>(opt.precision));
+  attn.clear();
+  for (int l = 0; l < (kv ? L : 1); ++l)
+    attn.push_back(make_attention_plan(qkv_at(l), ctx16.p, max_rows, d, static_cast<int>(opt.precision)));
   const int sms = device_sm_count();
   {  // statistics producers' N tiles fix the number of partials per row
     const int mt = max_rows / 128;
@@ -438,7 +476,7 @@ void Ctx::build_plans() {
     s.b = w.wqkv; s.N = 3 * d; s.groups = 1; s.b_ld = d; s.b_group_stride_bytes = size_t(3) * d * d * 2;
     s.bias = w.bqkv; s.bias_group_stride = 0; s.tile_slot = nullptr;
     s.res0 = s.res1 = nullptr; s.res_ld = 0;
-    s.c = qkv16.p; s.c_ld = 3 * d; s.epi = 0; s.cta2 = true;
+    s.c = qkv_at(l); s.c_ld = 3 * d; s.epi = 0; s.cta2 = true;
     s.bn = pick_bn(3 * d, m_tiles, sms, true);
     w.qkv = make_gemm_plan(s);
     // O projection
@@ -489,7 +527,7 @@ void Ctx::build_plans() {
         q.a = h16.p; q.a_ld = d; q.K = d;
         q.b = w.wqkv_f; q.N = 3 * d; q.groups = 1; q.b_ld = d;
         q.b_group_stride_bytes = size_t(3) * d * d * 2;
-        q.bias = w.bqkv_f; q.c = qkv16.p; q.c_ld = 3 * d; q.epi = kEpiFoldLN; q.cta2 = true;
+        q.bias = w.bqkv_f; q.c = qkv_at(l); q.c_ld = 3 * d; q.epi = kEpiFoldLN; q.cta2 = true;
         q.a_stats = d_stats2.p; q.a_stats_n = stats2_n; q.colsum = w.cs_qkv; q.inv_n = inv_d;
         q.bn = pick_bn(3 * d, m_tiles, sms, true);
         w.qkv = make_gemm_plan(q);
@@ -570,6 +608,46 @@ void Ctx::build_plans() {
       w.ffn2_ln = best_ln_plan(g, m_tiles);
     }
   }
+  // single-row decode steps: unfolded weights, explicit LayerNorms, 1-CTA tiles
+  dec.clear();
+  if (kv) {
+    const int mt = Bp / 128;
+    for (int l = 0; l < L; ++l) {
+      LayerDev& w = layers[l];
+      DecPlans dp;
+      GemmSpec s;
+      s.precision = prec;
+      s.a_rows = Bp;
+      s.a = h16.p; s.a_ld = d; s.K = d;
+      s.b = w.wqkv; s.N = 3 * d; s.b_ld = d; s.b_group_stride_bytes = size_t(3) * d * d * 2;
+      s.bias = w.bqkv; s.c = qkv_dec.p; s.c_ld = 3 * d; s.epi = 0;
+      s.bn = pick_bn(3 * d, mt, sms);
+      dp.qkv = make_gemm_plan(s);
+      s.a = ctx16.p; s.b = w.wo; s.N = d; s.b_group_stride_bytes = size_t(d) * d * 2;
+      s.bias = w.bo; s.c = a16.p; s.c_ld = d; s.bn = pick_bn(d, mt, sms);
+      dp.oproj = make_gemm_plan(s);
+      s.a = x16.p; s.b = w.w1; s.N = f; s.b_group_stride_bytes = size_t(f) * d * 2;
+      s.bias = w.b1; s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.bn = pick_bn(f, mt, sms);
+      dp.ffn1 = make_gemm_plan(s);
+      s.a = ffn16.p; s.a_ld = f; s.K = f; s.b = w.w2; s.N = d; s.b_ld = f;
+      s.b_group_stride_bytes = size_t(d) * f * 2; s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
+      s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, mt, sms);
+      dp.ffn2 = make_gemm_plan(s);
+      dec.push_back(dp);
+    }
+  }
+}
+
+void Ctx::build_lm_plan(LmHead& h) {
+  GemmSpec s;
+  s.precision = static_cast<int>(opt.precision);
+  s.a_rows = Bp;
+  s.a = hdec16.p; s.a_ld = d; s.K = d;
+  s.b = h.w16; s.N = h.V_pad; s.b_ld = d; s.b_group_stride_bytes = static_cast<size_t>(h.V_pad) * d * 2;
+  s.bias = h.bias; s.c = lm_logits.p; s.c_ld = static_cast<int>(lm_logits.n / Bp);
+  s.epi = kEpiOutF32;
+  s.bn = pick_bn(h.V_pad, Bp / 128, device_sm_count());
+  h.plan = make_gemm_plan(s);
 }
 
 void Ctx::upload_plot_hash() {
@@ -599,9 +677,12 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
                 const uint32_t* tokens_dev, uint32_t stride, const uint32_t* lens_host,
                 const uint32_t* lens_dev, uint32_t max_len, float* d_scores_out,
                 int32_t* d_labels_out, std::vector<PoolRecord>* records,
-                std::vector<int32_t>* record_layer) {
+                std::vector<int32_t>* record_layer, uint32_t n_new) {
   HMI_CHECK(n_req >= 1 && n_req <= opt.max_batch, HMI_DIMENSION_ERROR,
             "batch size must be in [1, max_batch]");
+  const bool gen = n_new > 0;
+  HMI_CHECK(!gen || (kv && n_new <= opt.max_new_tokens), HMI_CONFIG_ERROR,
+            "generation needs max_new_tokens >= n_new (causal model)");
   const bool sync_mode = opt.pipeline_mode == 0;
   const bool fine = opt.pipeline_mode == 2;
   reap(sync_mode);
@@ -615,6 +696,20 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     }
     tasks[i] = static_cast<uint32_t>(h_inst_task[k]);
   }
+  // wide lm heads of this batch (at most one; generation needs every request on it)
+  int wide_head = -1;
+  for (uint32_t i = 0; i < n_req; ++i) {
+    const int hd = h_inst_head[inst[i]];
+    const bool wide = lm_heads.count(hd) != 0;
+    if (wide) {
+      HMI_CHECK(wide_head < 0 || wide_head == hd, HMI_CONFIG_ERROR,
+                "a batch may use at most one wide lm head");
+      wide_head = hd;
+    }
+    HMI_CHECK(!gen || wide, HMI_CONFIG_ERROR, "generation needs every request bound to a wide lm head");
+  }
+  HMI_CHECK(!gen || lm_heads.at(wide_head).V <= static_cast<int>(cfg.vocab_size), HMI_CONFIG_ERROR,
+            "generation: the lm head emits ids outside the vocabulary");
   if (lens_host) {
     max_len = 0;
     for (uint32_t i = 0; i < n_req; ++i) {
@@ -815,12 +910,13 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     const bool last = l == L - 1;
     timed(P_QKV, s, [&] { launch_gemm(w.qkv, rows, s); });
     timed(P_ATTN, s, [&] {
+      const AttnPlan& ap = attn[kv ? l : 0];
       if (S == 128 && attn_tc) {
-        launch_attention_tc(attn, d_lens.p, static_cast<int>(n_req), heads, causal, s);
+        launch_attention_tc(ap, d_lens.p, static_cast<int>(n_req), heads, causal, s);
       } else if (S == 128) {
-        launch_attention_s128(attn, d_lens.p, static_cast<int>(n_req), heads, causal, s);
+        launch_attention_s128(ap, d_lens.p, static_cast<int>(n_req), heads, causal, s);
       } else {
-        launch_attention(qkv16.p, ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal,
+        launch_attention(qkv_at(l), ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal,
                          prec, s);
       }
     });
@@ -850,7 +946,12 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   H.offset = d_head_off.p;
   H.labels = d_head_labels.p;
   H.kind = d_head_kind.p;
-  timed(P_HEAD, s, [&] {
+  float* scores_dst = d_scores_out ? d_scores_out : d_scores.p;
+  int32_t* labels_dst = d_labels_out ? d_labels_out : d_labels.p;
+  if (wide_head >= 0 && !gen) {
+    HMI_CUDA(cudaMemsetAsync(scores_dst, 0, static_cast<size_t>(n_req) * opt.max_labels * 4, s));
+  }
+  if (!gen) timed(P_HEAD, s, [&] {
     if (ln_mode == 0) {  // the head applies the last layer's LN2 to its pre-norm row
       H.y16 = h16.p;
       H.ln_g = layers[L - 1].ln2g;
@@ -862,9 +963,13 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
       }
     }
     launch_head(H, h32.p, d_req_head.p, d_lens.p, static_cast<int>(n_req), S, d,
-                static_cast<int>(opt.max_labels), d_scores_out ? d_scores_out : d_scores.p,
-                d_labels_out ? d_labels_out : d_labels.p, d_tags.p, s);
+                static_cast<int>(opt.max_labels), scores_dst, labels_dst, d_tags.p, s);
   });
+  if (wide_head >= 0) {
+    const LmHead& lm = lm_heads.at(wide_head);
+    timed(P_HEAD, s, [&] { launch_lm_head(n_req, S, lm, wide_head, gen, scores_dst, labels_dst); });
+    if (gen) decode_steps(n_req, n_new, S, lm, wide_head);
+  }
   if (!d_scores_out) {
     timed(P_D2H, s, [&] {
       HMI_CUDA(cudaMemcpyAsync(st.scores, d_scores.p, static_cast<size_t>(n_req) * opt.max_labels * sizeof(float),
@@ -877,10 +982,153 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   st.busy = true;
   inflight.push_back(Inflight{st.done, si, uniq});
   last_n = n_req;
-  n_launches += (delta.empty() ? 0 : 1) + 3 + (ln_mode == 1 ? 9ull : 7ull) * L;
+  n_launches += (delta.empty() ? 0 : 1) + 2 + (gen ? 0 : 1) + (ln_mode == 1 ? 9ull : 7ull) * L;
+  if (wide_head >= 0) n_launches += 3 + (gen ? (n_new - 1ull) * (3 + 7ull * L) : 0);
   ++n_batches;
   last_S = static_cast<uint32_t>(S);
   return si;
+}
+
+// Wide lm head over the final row of each request (apply_head lm_logits, model.cpp:151-168):
+// gather (+ f64 LayerNorm of pre-norm rows), tcgen05 logits GEMM, top-8 + f64 rescoring.
+void Ctx::launch_lm_head(uint32_t n_req, int S, const LmHead& lm, int wide_head, bool gen,
+                         float* scores, int32_t* labels) {
+  cudaStream_t s = compute;
+  const int prec = static_cast<int>(opt.precision);
+  const int Mp = static_cast<int>((n_req + 127) / 128 * 128);
+  launch_lm_gather(ln_mode == 0 ? h16.p : nullptr, h32.p, layers[L - 1].ln2g, layers[L - 1].ln2b,
+                   d_lens.p, static_cast<int>(n_req), S, d, prec, hdec32.p, hdec16.p, s);
+  launch_gemm(lm.plan, Mp, s);
+  LmArgmaxArgs a;
+  a.logits = lm_logits.p;
+  a.ld = static_cast<int>(lm_logits.n / Bp);
+  a.V = lm.V;
+  a.h32 = hdec32.p;
+  a.d = d;
+  a.w = d_head_arena.p + h_head_off[wide_head];
+  a.bias = a.w + static_cast<size_t>(d) * lm.V;
+  if (gen) {
+    // the prompt's tokens start the generated sequences; token 1 lands at position len
+    HMI_CUDA(cudaMemcpy2DAsync(gen_tokens.p, static_cast<size_t>(gen_stride) * 4, d_tokens.p,
+                               static_cast<size_t>(S) * 4, static_cast<size_t>(S) * 4, n_req,
+                               cudaMemcpyDeviceToDevice, s));
+    HMI_CUDA(cudaMemcpyAsync(gen_pos.p, d_lens.p, n_req * 4, cudaMemcpyDeviceToDevice, s));
+    a.gen_tokens = gen_tokens.p;
+    a.tok_stride = gen_stride;
+    a.gen_pos = gen_pos.p;
+    a.advance = 0;
+    a.out_tokens = gen_out.p;
+    a.out_logits = gen_logit.p;
+    a.out_ld = static_cast<int>(opt.max_new_tokens);
+    a.step = 0;
+  } else {
+    a.req_head = d_req_head.p;
+    a.head = wide_head;
+    a.labels_out = labels;
+    a.scores_out = scores;
+    a.scores_ld = static_cast<int>(opt.max_labels);
+  }
+  launch_lm_argmax(a, static_cast<int>(n_req), s);
+}
+
+// Generated tokens 2..n_new: one causal row per request per step through every layer,
+// keys / values of earlier rows read from the cache (prompt rows: qkv_at(l); generated
+// rows: kv_tail). Each step: K5 (decode row) -> per layer QKV, cached attention, O,
+// per-row adapter + LN1, FFN1, FFN2 (+res), LN2 -> lm GEMM -> argmax / append.
+void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, int wide_head) {
+  cudaStream_t s = compute;
+  const int prec = static_cast<int>(opt.precision);
+  const int n = static_cast<int>(n_req);
+  const int Mp = (n + 127) / 128 * 128;
+  const int T = static_cast<int>(opt.max_new_tokens);
+  PlotDev P;
+  P.slots = d_slots.p;
+  P.mask = h_slots.empty() ? 0 : h_slots.size() - 1;
+  P.parent = d_parent.p;
+  P.max_versions = static_cast<int>(h_parent.size());
+  P.reps = d_reps.p;
+  P.ngram = ngram;
+  P.d = d;
+  P.max_depth = 1;
+  for (size_t v = 0; v < h_parent.size(); ++v) {
+    if (h_parent[v] == -2) continue;
+    int depth = 1;
+    for (int32_t u = h_parent[v]; u >= 0; u = h_parent[u]) ++depth;
+    P.max_depth = std::max(P.max_depth, depth);
+  }
+  LmArgmaxArgs am;
+  am.logits = lm_logits.p;
+  am.ld = static_cast<int>(lm_logits.n / Bp);
+  am.V = lm.V;
+  am.h32 = hdec32.p;
+  am.d = d;
+  am.w = d_head_arena.p + h_head_off[wide_head];
+  am.bias = am.w + static_cast<size_t>(d) * lm.V;
+  am.gen_tokens = gen_tokens.p;
+  am.tok_stride = gen_stride;
+  am.gen_pos = gen_pos.p;
+  am.advance = 1;
+  am.out_tokens = gen_out.p;
+  am.out_logits = gen_logit.p;
+  am.out_ld = T;
+  for (uint32_t k = 1; k < n_new; ++k) {
+    timed(P_RETRIEVE, s, [&] {
+      launch_retrieve(P, gen_tokens.p, d_lens.p, d_req_version.p, n, S, 1, h16.p, prec, nullptr,
+                      nullptr, nullptr, d_err.p, s, gen_pos.p, gen_stride);
+    });
+    for (int l = 0; l < L; ++l) {
+      LayerDev& w = layers[l];
+      DecPlans& dp = dec[l];
+      const bool last = l == L - 1;
+      timed(P_QKV, s, [&] { launch_gemm(dp.qkv, Mp, s); });
+      timed(P_ATTN, s, [&] {
+        AttnDecodeArgs a;
+        a.qkv_new = qkv_dec.p;
+        a.qkv_prefill = qkv_at(l);
+        a.S = S;
+        a.tail = kv_tail.p + static_cast<size_t>(l) * opt.max_batch * T * 2 * d;
+        a.tail_cap = T;
+        a.lens = d_lens.p;
+        a.gen_pos = gen_pos.p;
+        a.ctx = ctx16.p;
+        a.d = d;
+        a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d / heads)));
+        a.bf16 = prec;
+        launch_attn_decode(a, n, heads, S + static_cast<int>(n_new), s);
+      });
+      timed(P_OPROJ, s, [&] { launch_gemm(dp.oproj, Mp, s); });
+      timed(P_AD_UP, s, [&] {
+        AdapterRowsArgs a;
+        a.a16 = a16.p;
+        a.h16 = h16.p;
+        a.req_task = d_req_task.p;
+        a.slot_of = d_slot_of.p;
+        a.layers = L;
+        a.layer = l;
+        a.arena = arena.p;
+        a.slot_bytes = slot_bytes;
+        a.d = d;
+        a.r_pad = r_pad;
+        a.ln_g = w.ln1g;
+        a.ln_b = w.ln1b;
+        a.x16 = x16.p;
+        a.err = d_err.p;
+        a.bf16 = prec;
+        launch_adapter_rows_ln(a, n, s);
+      });
+      timed(P_FFN1, s, [&] { launch_gemm(dp.ffn1, Mp, s); });
+      timed(P_FFN2, s, [&] { launch_gemm(dp.ffn2, Mp, s); });
+      timed(P_LN2, s, [&] {
+        launch_layernorm(y32.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p, last ? hdec32.p : nullptr,
+                         n, d, prec, s);
+      });
+    }
+    timed(P_HEAD, s, [&] {
+      launch_gemm(lm.plan, Mp, s);
+      am.step = static_cast<int>(k);
+      launch_lm_argmax(am, n, s);
+    });
+  }
 }
 
 }  // namespace hmi_b200
@@ -1066,7 +1314,23 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
 
     // ---- activations
     const size_t R = c.max_rows;
-    c.h16.alloc(R * d); c.qkv16.alloc(R * 3 * d); c.ctx16.alloc(R * d); c.a16.alloc(R * d);
+    c.kv = c.opt.max_new_tokens > 0;
+    HMI_CHECK(!c.kv || cfg->mode == 1, HMI_CONFIG_ERROR,
+              "max_new_tokens needs a causal model (encoder rows see later tokens)");
+    c.Bp = static_cast<int>((c.opt.max_batch + 127) / 128 * 128);
+    c.h16.alloc(R * d); c.qkv16.alloc(R * 3 * d * (c.kv ? c.L : 1)); c.ctx16.alloc(R * d); c.a16.alloc(R * d);
+    c.hdec16.alloc(static_cast<size_t>(c.Bp) * d);
+    c.hdec32.alloc(static_cast<size_t>(c.Bp) * d);
+    if (c.kv) {
+      const size_t Bm = c.opt.max_batch, T = c.opt.max_new_tokens;
+      c.qkv_dec.alloc(static_cast<size_t>(c.Bp) * 3 * d);
+      c.kv_tail.alloc(static_cast<size_t>(c.L) * Bm * T * 2 * d);
+      c.gen_stride = c.S_max + static_cast<int>(T);
+      c.gen_tokens.alloc(Bm * c.gen_stride);
+      c.gen_pos.alloc(Bm);
+      c.gen_out.alloc(Bm * T);
+      c.gen_logit.alloc(Bm * T);
+    }
     c.mid16.alloc(R * c.r_pad); c.x16.alloc(R * d); c.ffn16.alloc(R * f);
     c.y32.alloc(R * d); c.h32.alloc(R * d);
     const size_t B = c.opt.max_batch;
@@ -1306,7 +1570,8 @@ int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, ui
     HMI_CHECK(head_idx < c.h_head_off.size(), HMI_CONFIG_ERROR, "head index exceeds max_heads");
     HMI_CHECK(kind <= 2, HMI_CONFIG_ERROR, "head kind must be 0, 1 or 2");
     HMI_CHECK(labels >= 1, HMI_CONFIG_ERROR, "output head needs at least one label");
-    HMI_CHECK(labels <= c.opt.max_labels, HMI_CONFIG_ERROR, "head labels exceed max_labels");
+    const bool wide = kind == 2 && labels > c.opt.max_labels;  // vocabulary-wide lm head
+    HMI_CHECK(labels <= c.opt.max_labels || wide, HMI_CONFIG_ERROR, "head labels exceed max_labels");
     if (c.h_head_kind[head_idx] >= 0) throw HmiError(HMI_CONFLICT_ERROR, "head already registered");
     const size_t n = static_cast<size_t>(c.d) * labels + labels;
     if (c.head_floats + n > c.d_head_arena.n) {
@@ -1329,6 +1594,29 @@ int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, ui
     HMI_CUDA(cudaMemcpy(c.d_head_off.p + head_idx, &c.h_head_off[head_idx], 8, cudaMemcpyHostToDevice));
     HMI_CUDA(cudaMemcpy(c.d_head_labels.p + head_idx, &c.h_head_labels[head_idx], 4, cudaMemcpyHostToDevice));
     HMI_CUDA(cudaMemcpy(c.d_head_kind.p + head_idx, &c.h_head_kind[head_idx], 4, cudaMemcpyHostToDevice));
+    if (wide) {
+      // 16-bit K-major copy [V_pad][d] for the tcgen05 logits GEMM; padded columns are zero
+      Ctx::LmHead h;
+      h.V = static_cast<int>(labels);
+      h.V_pad = static_cast<int>((labels + 255) / 256 * 256);
+      const size_t dd = static_cast<size_t>(c.d);
+      std::vector<uint16_t> wt(static_cast<size_t>(h.V_pad) * dd, 0);
+      for (size_t i = 0; i < dd; ++i)
+        for (size_t j = 0; j < labels; ++j) wt[j * dd + i] = f2h(w[i * labels + j], static_cast<int>(c.opt.precision));
+      std::vector<float> bp(h.V_pad, 0.f);
+      std::memcpy(bp.data(), b, labels * 4);
+      HMI_CUDA(cudaMalloc(&h.w16, wt.size() * 2));
+      HMI_CUDA(cudaMalloc(&h.bias, bp.size() * 4));
+      HMI_CUDA(cudaMemcpy(h.w16, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
+      HMI_CUDA(cudaMemcpy(h.bias, bp.data(), bp.size() * 4, cudaMemcpyHostToDevice));
+      const size_t need = static_cast<size_t>(c.Bp) * h.V_pad;
+      if (c.lm_logits.n < need) {
+        c.lm_logits.alloc(need);
+        for (auto& [id, o] : c.lm_heads) c.build_lm_plan(o);  // logits buffer moved
+      }
+      c.build_lm_plan(h);
+      c.lm_heads[static_cast<int>(head_idx)] = h;
+    }
   });
 }
 
@@ -1424,6 +1712,33 @@ int hmi_gpu_infer_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instan
     if (c.prof) c.prof_collect();
     c.reap(false);
     if (want) fill_trace(recs, tag, trace, trace_cap, evicted, evicted_cap, n_trace);
+    if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
+  });
+}
+
+int hmi_gpu_generate(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                     const uint32_t* tokens, uint32_t stride, const uint32_t* lens,
+                     uint32_t n_new, int32_t* out_tokens, float* out_logits) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    HMI_CHECK(n_new >= 1 && out_tokens, HMI_CONFIG_ERROR, "generate: n_new >= 1 and out_tokens required");
+    const int si = c.submit(n_req, instance_idx, tokens, nullptr, stride, lens, nullptr, 0, nullptr,
+                            nullptr, nullptr, nullptr, n_new);
+    Staging& st = c.stg[si];
+    HMI_CUDA(cudaEventSynchronize(st.done));
+    const size_t T = c.opt.max_new_tokens;
+    HMI_CUDA(cudaMemcpy2D(out_tokens, n_new * 4, c.gen_out.p, T * 4, n_new * 4, n_req,
+                          cudaMemcpyDeviceToHost));
+    if (out_logits) {
+      HMI_CUDA(cudaMemcpy2D(out_logits, n_new * 4, c.gen_logit.p, T * 4, n_new * 4, n_req,
+                            cudaMemcpyDeviceToHost));
+    }
+    const int err = *st.err;
+    if (c.prof) c.prof_collect();
+    c.reap(false);
     if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
   });
 }

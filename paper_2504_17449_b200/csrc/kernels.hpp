@@ -47,7 +47,8 @@ struct PlotDev {
 void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* lens,
                      const int* req_version, int n_req, int S, int causal, void* h16,
                      int precision, double* h64_debug, int32_t* gather, int32_t* levels,
-                     int32_t* err, cudaStream_t stream);
+                     int32_t* err, cudaStream_t stream, const int32_t* dec_pos = nullptr,
+                     int tok_stride = 0);
 
 // K6: routing instance -> (version, task, head) and task -> per-layer HBM slot.
 void launch_route(const uint32_t* instance_idx, int n_req, const int32_t* inst_version,

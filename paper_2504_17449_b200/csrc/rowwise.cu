@@ -117,17 +117,21 @@ __global__ void __launch_bounds__(256, 6) retrieve_kernel(PlotDev P, const uint3
                                                        int bf16, double* __restrict__ h64,
                                                        int32_t* __restrict__ gather,
                                                        int32_t* __restrict__ levels,
-                                                       int32_t* __restrict__ err) {
+                                                       int32_t* __restrict__ err,
+                                                       const int32_t* __restrict__ dec_pos,
+                                                       int tok_stride) {
   constexpr int kMaxWin = kRetrieveChunk + kMaxNgram;
   __shared__ int32_t wrow[kMaxWin * kMaxNgram];  // rep row per (window, offset)
   __shared__ int32_t wlev[kMaxWin * kMaxNgram];  // sub-gram length
   const int n = P.ngram;
   const int b = blockIdx.x;
-  const int p0 = blockIdx.y * kRetrieveChunk;
-  const int p1 = p0 + kRetrieveChunk < S ? p0 + kRetrieveChunk : S;
-  const int len = lens[b];
+  // decode mode (dec_pos != null): the single causal row dec_pos[b] of a sequence
+  // extended by generated tokens; output row b
+  const int p0 = dec_pos ? dec_pos[b] : blockIdx.y * kRetrieveChunk;
+  const int p1 = dec_pos ? p0 + 1 : (p0 + kRetrieveChunk < S ? p0 + kRetrieveChunk : S);
+  const int len = dec_pos ? p0 + 1 : lens[b];
   const int version = req_version[b];
-  const uint32_t* tok = tokens + static_cast<long long>(b) * S;
+  const uint32_t* tok = tokens + static_cast<long long>(b) * (dec_pos ? tok_stride : S);
   const int hl = (n - 1) / 2, hr = n - 1 - hl;
   // windows this chunk of positions needs (encoder: centred windows covering them;
   // causal: the window ending at each position)
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(256, 6) retrieve_kernel(PlotDev P, const uint3
   const int d = P.d;
   const int V = d / 128;  // float4 per lane
   for (int p = p0 + warp; p < p1; p += nwarps) {
-    const long long orow = static_cast<long long>(b) * S + p;
+    const long long orow = dec_pos ? static_cast<long long>(b) : static_cast<long long>(b) * S + p;
     int32_t rows[kMaxNgram];
     int32_t levs[kMaxNgram];
     int cnt = 0;
@@ -407,6 +411,7 @@ __global__ void __launch_bounds__(256) head_kernel(HeadDev H, const float* __res
   const float* W = H.arena + H.offset[hid];
   const float* B = W + static_cast<long long>(d) * nl;
   const int len = lens[b];
+  if (kind == 2 && nl > max_labels) return;  // wide lm head: served by the lm GEMM path
   if (kind == 1) {
     // token_tag: rows < valid_len, argmax per row
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -566,15 +571,17 @@ void launch_layernorm(const float* y, const float* gamma, const float* beta, voi
 void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* lens,
                      const int* req_version, int n_req, int S, int causal, void* h16,
                      int precision, double* h64_debug, int32_t* gather, int32_t* levels,
-                     int32_t* err, cudaStream_t stream) {
+                     int32_t* err, cudaStream_t stream, const int32_t* dec_pos, int tok_stride) {
   if (n_req <= 0) return;
   HMI_CHECK(plot.d % 128 == 0, HMI_CONFIG_ERROR, "retrieve: d must be a multiple of 128");
-  dim3 grid(n_req, (S + kRetrieveChunk - 1) / kRetrieveChunk);
+  HMI_CHECK(!dec_pos || causal, HMI_CONFIG_ERROR, "retrieve: decode rows need causal mode");
+  dim3 grid(n_req, dec_pos ? 1 : (S + kRetrieveChunk - 1) / kRetrieveChunk);
   const int n = plot.ngram;
   const size_t smem = static_cast<size_t>(kRetrieveChunk + kMaxNgram) * (n * (n + 1) / 2) *
                       plot.max_depth * sizeof(int32_t);
   retrieve_kernel<<<grid, 256, smem, stream>>>(plot, tokens, lens, req_version, S, causal, h16,
-                                                precision, h64_debug, gather, levels, err);
+                                                precision, h64_debug, gather, levels, err,
+                                                dec_pos, tok_stride);
   HMI_CUDA(cudaGetLastError());
 }
 

@@ -75,14 +75,14 @@ class GpuEngine:
                  precision: int = 0, max_batch: int = 256, max_seq: int = 128,
                  bottleneck: int = 64, max_labels: int = 8, pipeline_mode: int = MODE_FINE,
                  pool_bytes: int = 0, max_tasks: int = 1024, max_instances: int = 0,
-                 max_heads: int = 0, max_versions: int = 64):
+                 max_heads: int = 0, max_versions: int = 64, max_new_tokens: int = 0):
         self.cfg = cfg
         self.max_labels = max_labels
         self.max_batch = max_batch
         self.max_seq = max_seq
         opts = Options(precision, max_batch, max_seq, bottleneck, max_labels, pipeline_mode,
                        pool_bytes, max_tasks, max_instances or max_tasks, max_heads or max_tasks,
-                       max_versions)
+                       max_versions, max_new_tokens, 0)
         hi = np.ascontiguousarray(higher_f32, np.float32)
         assert hi.size == cfg.higher_layers * layer_floats(cfg), "higher weights size"
         h = ctypes.c_void_p()
@@ -166,6 +166,21 @@ class GpuEngine:
         check(_native.lib().hmi_gpu_infer_batch_device(
             self.h, inst.shape[0], _p(inst, ctypes.c_uint32), ctypes.c_void_p(d_tokens), stride,
             ctypes.c_void_p(d_lens), max_len, ctypes.c_void_p(d_scores), ctypes.c_void_p(d_labels)))
+
+    def generate(self, instance_idx, tokens, lens, n_new: int):
+        """Greedy continuation of causal prompts through a wide lm head
+        (hmi_gpu_generate): returns (tokens [n, n_new] int32, logits [n, n_new] f32)."""
+        inst = np.ascontiguousarray(instance_idx, np.uint32)
+        toks = np.ascontiguousarray(tokens, np.uint32)
+        ln = np.ascontiguousarray(lens, np.uint32)
+        n = inst.shape[0]
+        out = np.zeros((n, n_new), np.int32)
+        logit = np.zeros((n, n_new), np.float32)
+        check(_native.lib().hmi_gpu_generate(self.h, n, _p(inst, ctypes.c_uint32),
+                                             _p(toks, ctypes.c_uint32), toks.shape[1],
+                                             _p(ln, ctypes.c_uint32), n_new,
+                                             _p(out, ctypes.c_int32), _p(logit, ctypes.c_float)))
+        return out, logit
 
     def synchronize(self) -> None:
         check(_native.lib().hmi_gpu_synchronize(self.h))

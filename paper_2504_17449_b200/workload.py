@@ -54,6 +54,7 @@ class Workload:
     alpha: float = 50.0
     p_noise: float = 0.05
     pool_fraction: float = 1.0   # HBM slot pool as a fraction of all tenants' adapters
+    gen_tokens: int = 0          # causal generation: tokens generated per request (C3)
 
     def flops_per_request(self) -> int:
         """Algorithmic FLOPs: F_layer = 2L(4d^2 + 2df + 2dr) + 4L^2 d,
@@ -63,6 +64,17 @@ class Workload:
         layer = 2 * L * (4 * d * d + 2 * d * f + 2 * d * r) + attn
         return self.higher_layers * layer + 2 * d * self.labels
 
+    def generate_flops_per_request(self) -> int:
+        """Prompt forward + lm head, then one single-row step per further token at
+        context c: layers * (2 (4d^2 + 2df + 2dr) + 4 c d) + 2 d V."""
+        L, d, f, r = self.seq, self.hidden_size, self.ffn_size, self.r
+        total = self.flops_per_request()
+        for k in range(1, self.gen_tokens):
+            c = L + k  # keys of the row at position L + k - 1
+            total += self.higher_layers * (2 * (4 * d * d + 2 * d * f + 2 * d * r) + 4 * c * d)
+            total += 2 * d * self.labels
+        return total
+
 
 CONFIGS = {
     # C1 tiny hBERT (4 layers = 2 PLOT + 2 higher), 16 tenants, batch 32
@@ -70,8 +82,9 @@ CONFIGS = {
                    batch=32, domain_vocab=300, domain_tokens=8192, root_tokens=4096),
     # C2 hBERT-base (12 layers = 6 PLOT + 6 higher), 1,000 tenants, 8 domains, batch 256
     "c2": Workload("hBERT-base", 768, 12, 6, 6, 3072, 30522),
-    # C3 hGPT-2 small (causal) -- prompt path; lm head handled as a cls-width head here
-    "c3": Workload("hGPT-2-small", 768, 12, 6, 6, 3072, 50257, mode=1, head_kind=2, labels=8),
+    # C3 hGPT-2 small (causal): prompt 128 + 32 greedy tokens, one shared vocabulary lm head
+    "c3": Workload("hGPT-2-small", 768, 12, 6, 6, 3072, 50257, mode=1, head_kind=2,
+                   labels=50257, gen_tokens=32),
     # C4 hBERT-base, 10,000 tenants swapped through a bounded HBM slot pool
     "c4": Workload("hBERT-base-10k-swap", 768, 12, 6, 6, 3072, 30522, n_tenants=10000,
                    pool_fraction=0.6),

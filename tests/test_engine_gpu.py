@@ -219,3 +219,102 @@ def test_base_parity(n_req):
     assert err <= TOL
     assert (res.labels == ref_labels).mean() >= 0.999
     w.eng.close()
+
+
+@pytest.fixture(scope="module")
+def gpt():
+    """hGPT-style tiny causal model, one vocabulary-wide lm head (1024 > max_labels) shared
+    by every instance, KV cache for 12 generated tokens."""
+    cfg = oracle.Config(256, 4, 2, 2, 1024, 1024, 1, 3, 11)
+    w = World(cfg, n_tasks=8, r=16, labels=cfg.vocab_size, head_kind=E.HEAD_LM, max_batch=16,
+              shared_head=True, max_new_tokens=12, max_labels=8)
+    yield w
+    w.eng.close()
+
+
+def test_wide_lm_head_infer_batch(gpt):
+    """The wide lm head through infer_batch: label = argmax over the vocabulary,
+    scores[:, 0] = its logit (tcgen05 logits GEMM + f64 rescoring of the top-8)."""
+    inst, toks, lens = gpt.requests(51, 16, 120, min_len=1)
+    res = gpt.eng.infer_batch(inst, toks, lens)
+    ref_scores, ref_labels, _ = gpt.oracle_batch(inst, toks, lens)
+    assert (res.labels == ref_labels).mean() >= 0.999
+    top = ref_scores[np.arange(len(inst)), ref_labels]
+    rel = np.abs(res.scores[:, 0] - top) / np.abs(ref_scores).max(axis=1)
+    assert rel.max() <= TOL
+    assert (res.scores[:, 1:8] == 0).all()
+
+
+def test_generate_teacher_forced(gpt):
+    """Greedy generation with the KV cache: every generated token is checked against
+    the oracle's full causal forward over prompt + the tokens generated before it
+    (teacher forcing), so one near-tie cannot cascade through the comparison."""
+    n, n_new = 12, 12
+    inst, toks, lens = gpt.requests(53, n, 116, min_len=2)
+    lens[:3] = [2, 3, 116]
+    gen, logit = gpt.eng.generate(inst, toks, lens, n_new)
+    assert ((gen >= 0) & (gen < gpt.cfg.vocab_size)).all()
+    # the first token is what infer_batch predicts for the prompt
+    res = gpt.eng.infer_batch(inst, toks, lens)
+    assert np.array_equal(gen[:, 0], res.labels)
+    seqs, meta = [], []
+    for i in range(n):
+        for k in range(n_new):
+            seq = np.concatenate([toks[i, :lens[i]], gen[i, :k].astype(np.uint32)])
+            seqs.append(seq)
+            meta.append((i, k))
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(16) as ex:
+        out = list(ex.map(lambda s: gpt.oracle_one(int(inst[meta[s][0]]), seqs[s], len(seqs[s])),
+                          range(len(seqs))))
+    agree, worst_gap, worst_err = 0, 0.0, 0.0
+    for (i, k), (scores, label, _) in zip(meta, out):
+        scale = np.abs(scores).max()
+        g = int(gen[i, k])
+        agree += int(g == label)
+        worst_gap = max(worst_gap, (scores[label] - scores[g]) / scale)   # 0 when equal
+        worst_err = max(worst_err, abs(float(logit[i, k]) - scores[g]) / scale)
+    rate = agree / len(meta)
+    print(f"generate: argmax agreement {rate:.4f}, worst near-tie gap {worst_gap:.2e}, "
+          f"worst logit err {worst_err:.2e}")
+    assert worst_err <= TOL
+    assert worst_gap <= TOL          # any disagreement is a near tie within tolerance
+    assert rate >= 0.97
+
+
+def test_generate_errors(gpt):
+    inst, toks, lens = gpt.requests(55, 4, 40)
+    from paper_2504_17449_b200._native import ConfigError
+    with pytest.raises(ConfigError):
+        gpt.eng.generate(inst, toks, lens, 13)  # > max_new_tokens
+
+
+def test_generate_gpt2_small_shapes():
+    """C3 shapes: hGPT-2 small (d=768, 12 heads, 6 higher layers, ffn 3072, r=64) with the
+    50,257-token lm head shared by every tenant; teacher-forced against the oracle."""
+    w = World(oracle.GPT2S, n_tasks=6, r=64, labels=oracle.GPT2S.vocab_size,
+              head_kind=E.HEAD_LM, max_batch=6, shared_head=True, max_new_tokens=3,
+              max_labels=8, branches=tuple((0, 60) for _ in range(4)), n_hot=64, n_bi=400,
+              n_tri=400)
+    inst, toks, lens = w.requests(57, 6, 128, min_len=100)
+    gen, logit = w.eng.generate(inst, toks, lens, 3)
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = [(i, k) for i in range(6) for k in range(3)]
+
+    def run(j):
+        i, k = j
+        seq = np.concatenate([toks[i, :lens[i]], gen[i, :k].astype(np.uint32)])
+        return w.oracle_one(int(inst[i]), seq, len(seq))
+
+    with ThreadPoolExecutor(32) as ex:
+        out = list(ex.map(run, jobs))
+    agree = 0
+    for (i, k), (scores, label, _) in zip(jobs, out):
+        scale = np.abs(scores).max()
+        g = int(gen[i, k])
+        agree += int(g == label)
+        assert (scores[label] - scores[g]) / scale <= TOL
+        assert abs(float(logit[i, k]) - scores[g]) / scale <= TOL
+    print(f"C3 generate argmax agreement {agree / len(jobs):.4f}")
+    assert agree / len(jobs) >= 0.94
+    w.eng.close()

@@ -19,7 +19,8 @@ class World:
     def __init__(self, cfg: oracle.Config, n_tasks: int, r: int, labels: int, *,
                  head_kind: int = 0, branches=((0, 40), (0, 40), (1, 30)), max_batch=32,
                  max_seq=128, pool_bytes=0, pipeline_mode=E.MODE_FINE, precision=0,
-                 table_seed=1, n_hot=24, n_bi=80, n_tri=60, engine=True):
+                 table_seed=1, n_hot=24, n_bi=80, n_tri=60, engine=True, shared_head=False,
+                 max_new_tokens=0, max_labels=None):
         self.cfg, self.r, self.labels, self.head_kind = cfg, r, labels, head_kind
         self.higher = oracle.generate_higher(cfg)
         self.tables, self.hot = make_tree(table_seed, cfg.vocab_size, cfg.hidden_size,
@@ -29,8 +30,10 @@ class World:
         for t in self.tables:
             self.tree.add_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
         self.adapters = [oracle.generate_adapter(cfg, r, ADAPTER_SEED + t) for t in range(n_tasks)]
-        self.heads = [oracle.generate_head(cfg.hidden_size, labels, HEAD_SEED + t)
-                      for t in range(n_tasks)]
+        # shared_head: one (vocabulary-wide lm) head bound to every instance
+        self.heads = [oracle.generate_head(cfg.hidden_size, labels, HEAD_SEED + (0 if shared_head else t))
+                      for t in range(1 if shared_head else n_tasks)]
+        self.shared_head = shared_head
         self.n_versions = len(self.tables)
         # instance i -> (version i % n_versions, task i, head i)
         self.inst_version = np.arange(n_tasks) % self.n_versions
@@ -40,16 +43,19 @@ class World:
                                 cfg.ffn_size, cfg.vocab_size, cfg.mode, cfg.max_fragment,
                                 cfg.seed)
             self.eng = E.GpuEngine(mc, self.higher, precision=precision, max_batch=max_batch,
-                                   max_seq=max_seq, bottleneck=r, max_labels=labels,
+                                   max_seq=max_seq, bottleneck=r,
+                                   max_labels=labels if max_labels is None else max_labels,
                                    pipeline_mode=pipeline_mode, pool_bytes=pool_bytes,
-                                   max_tasks=n_tasks, max_versions=max(8, self.n_versions))
+                                   max_tasks=n_tasks, max_versions=max(8, self.n_versions),
+                                   max_new_tokens=max_new_tokens)
             for t in self.tables:
                 self.eng.upload_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
             for t in range(n_tasks):
                 self.eng.register_task(t, self.adapters[t])
-                w, b = self.heads[t]
-                self.eng.register_head(t, head_kind, w, b)
-                self.eng.bind_instance(t, int(self.inst_version[t]), t, t)
+                if not shared_head or t == 0:
+                    w, b = self.heads[t]
+                    self.eng.register_head(t, head_kind, w, b)
+                self.eng.bind_instance(t, int(self.inst_version[t]), t, 0 if shared_head else t)
 
     def requests(self, seed, n, max_len, min_len=1, p_hot=0.9):
         toks, lens = make_requests(seed, n, self.hot, self.cfg.vocab_size, max_len,
@@ -58,7 +64,7 @@ class World:
         return inst.astype(np.uint32), toks, lens
 
     def oracle_one(self, inst, tokens, length):
-        w, b = self.heads[inst]
+        w, b = self.heads[0 if self.shared_head else inst]
         return oracle.infer_one(self.cfg, self.higher, self.tree, int(self.inst_version[inst]),
                                 tokens[:length], self.adapters[inst], self.r, w, b,
                                 head_kind=self.head_kind)
