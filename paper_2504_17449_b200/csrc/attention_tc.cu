@@ -6,17 +6,19 @@
 // S = Q K^T / sqrt(64) over keys j < limit (valid_len, or i + 1 when causal), softmax,
 // ctx = P V. One persistent CTA per SM walks (request, head) items, double-buffered:
 //
-//   warp 0 (lane 0): TMA   Q, K, V tiles (128 x 64 16-bit, SWIZZLE_128B) -> smem[buf]
-//   warp 1 (lane 0): MMA   S[buf] = Q K^T   tcgen05 M=128 N=128 K=64 -> TMEM
-//                          O[buf] = P V     tcgen05 M=128 N=64 K=128, V as MN-major B
+//   warp 0 (lane 0): TMA   Q, K, V tiles (128 x 64 16-bit, SWIZZLE_128B) -> smem stage
+//                          (kStages items in flight)
+//   warp 1 (lane 0): MMA   S[buf] = Q K^T   tcgen05 M=128 N=128 K=64 -> TMEM; issued one item
+//                          ahead of O[buf] = P V (M=128 N=64 K=128, V as MN-major B), so the
+//                          two softmax groups run concurrently
 //   warps 2..9     : softmax, two groups of 4 warps (group g serves buffer g, i.e. every
 //                    other item, so two items' softmax overlap); one query row per
 //                    thread: TMEM S row -> mask / max / exp2 / sum -> 16-bit P row into
-//                    swizzled smem (UMMA A operand); epilogue: TMEM O row * 1/sum ->
+//                    swizzled smem over the consumed Q, K tiles (UMMA A operand); epilogue: TMEM O row * 1/sum ->
 //                    16-bit -> smem -> TMA store
 //
-// Barriers per buffer: load_full (TMA tx), load_empty (MMA commit after P.V),
-// s_full (MMA commit), p_full (4 softmax warps), o_full (MMA commit), o_empty (4 warps).
+// Barriers per load stage: load_full (TMA tx), load_empty (MMA commit after P.V); per TMEM
+// buffer: s_full (MMA commit), p_full (4 softmax warps), o_full (MMA commit), o_empty (4 warps).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -31,9 +33,10 @@ namespace {
 
 constexpr int kTcThreads = 320;  // TMA warp, MMA warp, 2 groups x 4 softmax warps
 constexpr int kT = 128 * 128;                // one 128 x 64 16-bit tile (bytes)
-constexpr int kBufBytes = 3 * kT + 2 * kT;   // Q, K, V + P (128 x 128 16-bit as two tiles)
+constexpr int kStages = 4;                   // Q, K, V load stages (items in flight)
+constexpr int kBufBytes = 3 * kT;            // Q, K, V; P (128 x 128 16-bit) overwrites Q, K
 constexpr int kOStage = kT;                  // output staging tile
-constexpr int kSmem = 1024 + 2 * kBufBytes + 2 * kOStage + 256;
+constexpr int kSmem = 1024 + kStages * kBufBytes + 2 * kOStage + 256;
 
 // Shared-memory descriptor of an MN-major SWIZZLE_128B operand whose MN extent is one
 // 128-byte atom (64 x 16-bit): 8-row K groups are 1024 B apart.
@@ -68,23 +71,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
     const int* __restrict__ lens, int n_items, int heads, int d, int causal, float scale_log2) {
   extern __shared__ uint8_t raw[];
   uint8_t* base = raw + ((1024 - (smem_u32(raw) & 1023)) & 1023);
-  uint8_t* ostg = base + 2 * kBufBytes;
+  uint8_t* ostg = base + kStages * kBufBytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(ostg + 2 * kOStage);
-  uint64_t* load_full = bar;        // [2]
-  uint64_t* load_empty = bar + 2;   // [2]
-  uint64_t* s_full = bar + 4;       // [2]
-  uint64_t* p_full = bar + 6;       // [2]
-  uint64_t* o_full = bar + 8;       // [2]
-  uint64_t* o_empty = bar + 10;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* load_full = bar;                  // [kStages]
+  uint64_t* load_empty = bar + kStages;       // [kStages]
+  uint64_t* s_full = bar + 2 * kStages;       // [2]
+  uint64_t* p_full = s_full + 2;              // [2]
+  uint64_t* o_full = s_full + 4;              // [2]
+  uint64_t* o_empty = s_full + 6;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_qkv);
     tma_prefetch_desc(&map_ctx);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kStages; ++b) {
       mbar_init(&load_full[b], 1);
       mbar_init(&load_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 4);
       mbar_init(&o_full[b], 1);
@@ -104,8 +109,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
     if (lane == 0) {
       int k = 0;
       for (int item = my_first; item < n_items; item += step, ++k) {
-        const int b = k & 1;
-        const uint32_t ph = (k >> 1) & 1;
+        const int b = k % kStages;
+        const uint32_t ph = (k / kStages) & 1;
         mbar_wait(&load_empty[b], ph ^ 1);
         const int req = item / heads, h = item - req * heads;
         uint8_t* dst = base + b * kBufBytes;
@@ -119,24 +124,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
     if (lane == 0) {
       const uint32_t id_s = idesc_f16(128, 128, kBf16 ? 1u : 0u);
       const uint32_t id_o = idesc_f16(128, 64, kBf16 ? 1u : 0u) | (1u << 16);  // B MN-major
-      int k = 0;
-      for (int item = my_first; item < n_items; item += step, ++k) {
-        const int b = k & 1;
-        const uint32_t ph = (k >> 1) & 1;
-        uint8_t* buf = base + b * kBufBytes;
-        mbar_wait(&load_full[b], ph);
+      const int n_mine = my_first < n_items ? (n_items - 1 - my_first) / step + 1 : 0;
+      auto issue_s = [&](int k) {  // S[k & 1] = Q K^T of this CTA's k-th item
+        const int st = k % kStages;
+        mbar_wait(&load_full[st], (k / kStages) & 1);
         tc_fence_after();
-        // S[b] = Q K^T (K = 64 = 4 x 16; +32 B inside the swizzle atom per step)
+        uint8_t* buf = base + st * kBufBytes;
         const uint64_t qd = sdesc_k_sw128(smem_u32(buf));
         const uint64_t kd = sdesc_k_sw128(smem_u32(buf + kT));
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) umma_f16(tmem + b * 128, qd + 2 * kk, kd + 2 * kk, id_s, kk);
-        umma_commit(&s_full[b]);
+        for (int kk = 0; kk < 4; ++kk) {  // K = 64 = 4 x 16; +32 B inside the swizzle atom per step
+          umma_f16(tmem + (k & 1) * 128, qd + 2 * kk, kd + 2 * kk, id_s, kk);
+        }
+        umma_commit(&s_full[k & 1]);
+      };
+      if (n_mine > 0) issue_s(0);
+      for (int k = 0; k < n_mine; ++k) {
+        const int b = k & 1;
+        const uint32_t ph = (k >> 1) & 1;
+        // S of the next item first: its TMEM buffer was released by p_full(k - 1), waited below
+        // in the previous iteration, so both softmax groups have work
+        if (k + 1 < n_mine) issue_s(k + 1);
         // O[b] = P V once the softmax wrote P and the epilogue released O[b]
         mbar_wait(&p_full[b], ph);
         mbar_wait(&o_empty[b], ph ^ 1);
         tc_fence_after();
-        const uint32_t p0 = smem_u32(buf + 3 * kT), vb = smem_u32(buf + 2 * kT);
+        uint8_t* buf = base + (k % kStages) * kBufBytes;
+        const uint32_t p0 = smem_u32(buf), vb = smem_u32(buf + 2 * kT);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // 16 keys per step
           const uint64_t pd = sdesc_k_sw128(p0 + (kk >> 2) * kT) + 2 * (kk & 3);
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
           umma_f16(tmem + 256 + b * 64, pd, vd, id_o, kk);
         }
         umma_commit(&o_full[b]);
-        umma_commit(&load_empty[b]);  // Q, K, V, P of buffer b consumed
+        umma_commit(&load_empty[k % kStages]);  // Q, K, V, P of this stage consumed
       }
     }
   } else {
@@ -220,8 +234,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
         s[j] = exp2f(s[j] - mb);
         l += s[j];
       }
-      // P row r -> two SWIZZLE_128B K-major tiles (keys 0-63, 64-127) of buffer b
-      uint8_t* P = base + b * kBufBytes + 3 * kT;
+      // P row r -> two SWIZZLE_128B K-major tiles (keys 0-63, 64-127) over the stage's Q, K
+      // (both consumed: s_full committed after the S MMA read them)
+      uint8_t* P = base + (k % kStages) * kBufBytes;
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         uint4 v;

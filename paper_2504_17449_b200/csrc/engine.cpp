@@ -42,6 +42,7 @@
 #include <vector>
 
 #include "decode.hpp"
+#include "adapter.hpp"
 #include "gemm.hpp"
 #include "kernels.hpp"
 #include "slot_pool.hpp"
@@ -94,6 +95,7 @@ struct LayerDev {
   float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
   GemmPlan qkv, oproj, ad_down, ad_up, ffn1, ffn2;
   GemmPlan ad_up_ln, ffn2_ln;  // LayerNorm fused into the epilogue (cluster row reduction)
+  AdapterPlan adapter;         // fused down + up + skip + residual (adapter.cu), folded LN mode
   // LayerNorm folding (default mode): gamma folded into the consumer's weights, beta.W into
   // its bias, and the per-column sums of the folded 16-bit weights for the mean correction
   void* mem_fold = nullptr;
@@ -126,9 +128,12 @@ struct Inflight {
   std::vector<uint32_t> tasks;
 };
 
-// N tile with the least wave quantisation; `pair`: units are 256-row CTA-pair tiles
-// scheduled over sms/2 clusters (cta_group::2 kernel).
-int pick_bn(int N, int m_tiles, int sms, bool pair = false) {
+// N tile with the best (wave quantisation x per-tile efficiency); `pair`: units are 256-row
+// CTA-pair tiles scheduled over sms/2 clusters (cta_group::2 kernel); `min_bn`: narrowest tile
+// allowed. Per-tile efficiency of the pair kernel is measured (profiles/r01_gemm_sweep.txt:
+// 256-wide pair tiles run 1.07-1.19x faster than 192-wide ones at equal wave counts; the
+// 1-CTA kernel is less sensitive).
+int pick_bn(int N, int m_tiles, int sms, bool pair = false, int min_bn = 64) {
   int best = -1;
   double best_eff = -1;
   if (pair) {
@@ -136,10 +141,11 @@ int pick_bn(int N, int m_tiles, int sms, bool pair = false) {
     sms /= 2;
   }
   for (int bn : {256, 192, 128, 64}) {
-    if (N % bn || (pair && bn < 128)) continue;
+    if (N % bn || (pair && bn < 128) || bn < min_bn) continue;
     const long tiles = static_cast<long>(N / bn) * m_tiles;
     const long waves = (tiles + sms - 1) / sms;
-    const double eff = static_cast<double>(tiles) / (waves * sms);
+    const double w = !pair ? 1.0 : bn == 256 ? 1.0 : bn == 192 ? 0.85 : 0.7;
+    const double eff = w * static_cast<double>(tiles) / (waves * sms);
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = bn;
@@ -270,6 +276,9 @@ struct Ctx {
   // (HMI_LN_MODE=unfused), 2 cluster-reduced GEMM epilogues (HMI_LN_MODE=cluster)
   int ln_mode = 0;
   bool attn_tc = true;  // tcgen05 attention for padded length 128 (HMI_ATTN=mma selects mma.sync)
+  // one fused adapter kernel per layer (folded LN mode, r <= 64); HMI_ADAPTER=gemm selects the
+  // two grouped GEMMs
+  bool adapter_fused = true;
   DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
   static constexpr int kStatsLd = kStatsStride;
   int stats1_bn = 0, stats2_bn = 0, stats1_n = 0, stats2_n = 0;
@@ -453,9 +462,11 @@ void Ctx::build_plans() {
   const int sms = device_sm_count();
   {  // statistics producers' N tiles fix the number of partials per row
     const int mt = max_rows / 128;
-    stats1_bn = pick_bn(d, mt, sms);
-    stats2_bn = pick_bn(d, mt, sms, true);
-    stats1_n = 2 * (d / stats1_bn);
+    // each producer N tile emits two partials per row: at most kStatsLd of them
+    const int min_bn = (2 * d + kStatsLd - 1) / kStatsLd;
+    stats1_bn = pick_bn(d, mt, sms, false, min_bn);
+    stats2_bn = pick_bn(d, mt, sms, true, min_bn);
+    stats1_n = adapter_fused ? 2 : 2 * (d / stats1_bn);
     stats2_n = 2 * (d / stats2_bn);
     HMI_CHECK(stats1_n <= kStatsLd && stats2_n <= kStatsLd, HMI_CONFIG_ERROR,
               "hidden size too wide for the LayerNorm statistics buffer");
@@ -552,6 +563,21 @@ void Ctx::build_plans() {
         }
         u.bn = stats1_bn;
         w.ad_up = make_gemm_plan(u);
+        if (adapter_fused) {
+          AdapterSpec as;
+          as.a = a16.p; as.h = h16.p; as.out = x16.p;
+          as.arena = arena.p; as.slot_bytes = slot_bytes;
+          as.off_wu = off_wu; as.off_bd = off_bd; as.off_bu = off_bu;
+          as.n_slots = static_cast<int>(n_slots); as.d = d; as.r_pad = r_pad;
+          as.rows = max_rows; as.precision = prec;
+          as.tile_slot = u.tile_slot;
+          as.stats_out = d_stats1.p; as.stats_ld = kStatsLd;
+          if (prev) {
+            as.r_stats = d_stats2.p; as.r_stats_n = stats2_n;
+            as.r_gamma = prev->ln2g; as.r_beta = prev->ln2b;
+          }
+          w.adapter = make_adapter_plan(as);
+        }
       }
       {  // FFN1 on LN1(y1)
         GemmSpec g;
@@ -922,9 +948,13 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     });
     timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
     if (fine) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
-    timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
+    if (ln_mode == 0 && adapter_fused) {
+      timed(P_AD_UP, s, [&] { launch_adapter(w.adapter, rows, s); });
+    } else {
+      timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
+    }
     if (ln_mode == 0) {
-      timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
+      if (!adapter_fused) timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
       timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
       timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
     } else if (ln_mode == 2) {
@@ -1399,6 +1429,8 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       c.ln_mode = m == "unfused" ? 1 : m == "cluster" ? 2 : 0;
     }
     if (const char* env = std::getenv("HMI_ATTN")) c.attn_tc = std::string(env) != "mma";
+    c.adapter_fused = c.r_pad == 64 && c.d % 128 == 0;
+    if (const char* env = std::getenv("HMI_ADAPTER")) c.adapter_fused &= std::string(env) != "gemm";
     c.d_stats1.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.d_stats2.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.build_plans();

@@ -125,6 +125,37 @@ def test_layernorm_placements_agree(c1, monkeypatch, mode):
     assert np.abs(folded.scores - other.scores).max() < 1e-2
 
 
+BASE_SMALL = dict(n_tasks=4, r=64, labels=8, max_batch=4, branches=tuple((0, 60) for _ in range(2)),
+                  n_hot=64, n_bi=400, n_tri=400)
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "base"])
+def test_adapter_fused_matches_grouped_gemms(c1, monkeypatch, cfg):
+    """The fused adapter kernel (down + ReLU + up + skip + LN2-residual in one launch) and the
+    two tenant-grouped GEMMs it replaces give the same logits; both meet the tolerance."""
+    if cfg == "tiny":
+        w1 = c1
+        inst, toks, lens = c1.requests(29, 16, 128)
+    else:
+        w1 = World(oracle.BASE, **BASE_SMALL)
+        inst, toks, lens = w1.requests(31, 4, 128, min_len=1)
+    fused = w1.eng.infer_batch(inst, toks, lens)
+    monkeypatch.setenv("HMI_ADAPTER", "gemm")
+    if cfg == "tiny":
+        w2 = World(oracle.TINY, n_tasks=16, r=16, labels=8, max_batch=32)
+    else:
+        w2 = World(oracle.BASE, **BASE_SMALL)
+    grouped = w2.eng.infer_batch(inst, toks, lens)
+    w2.eng.close()
+    ref_scores, ref_labels, _ = w1.oracle_batch(inst, toks, lens)
+    assert logit_error(fused.scores, ref_scores) <= TOL
+    assert (fused.labels == ref_labels).mean() >= 0.999
+    scale = np.abs(grouped.scores).max()
+    assert np.abs(fused.scores - grouped.scores).max() / scale < 2e-3
+    if cfg != "tiny":
+        w1.eng.close()
+
+
 @pytest.mark.parametrize("causal", [0, 1])
 def test_attention_tc_matches_mma(monkeypatch, causal):
     """tcgen05 attention (default for padded length 128) vs the mma.sync kernel."""
