@@ -42,10 +42,11 @@ constexpr int kStages = 3;
 constexpr int kStageBytes = 24576;     // A 128 x 64 (16 KB) + Wd 64 x 64 (8 KB); or Wu 128 x 64
 constexpr int kResSlots = 3;
 constexpr int kResBytes = 32768;       // a box + h box, 128 rows x 64 columns each
+constexpr int kVecBytes = 768;         // per residual slot: the chunk's 64 bu, gamma, beta floats
 constexpr int kBox = 16384;
 constexpr int kUpN = 128;              // y chunk width
-constexpr int kSmem =
-    1024 + kStages * kStageBytes + kBox /*mid*/ + kResSlots * kResBytes + 8 * 4096 /*staging*/ + 256;
+constexpr int kSmem = 1024 + kStages * kStageBytes + kBox /*mid*/ + kResSlots * kResBytes +
+                     8 * 4096 /*staging*/ + kResSlots * kVecBytes + 256;
 
 template <bool kBf16>
 __device__ __forceinline__ float2 unpack2(uint32_t w) {
@@ -75,7 +76,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* ring = base;
   uint8_t* midA = ring + kStages * kStageBytes;
   uint8_t* res = midA + kBox;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(res + kResSlots * kResBytes + 8 * 4096);
+  uint8_t* vec = res + kResSlots * kResBytes + 8 * 4096;  // [kResSlots][kVecBytes]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vec + kResSlots * kVecBytes);
   uint64_t* full = bar;                          // [kStages]
   uint64_t* empty = bar + kStages;               // [kStages]
   uint64_t* res_full = bar + 2 * kStages;        // [kResSlots]
@@ -159,13 +161,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_once = policy_evict_first();
       uint32_t slot = 0, phase = 0, jg = 0;
       for (int mt = blockIdx.x; mt < args.num_m_tiles; mt += gridDim.x) {
+        const long long grp = __ldg(&args.tile_slot[mt]);
         for (int j = 0; j < n_res; ++j, ++jg) {
           mbar_wait(&res_empty[slot], phase ^ 1);
           res_tag[slot] = jg;
           uint8_t* rs = res + slot * kResBytes;
-          mbar_arrive_expect_tx(&res_full[slot], 2 * kBox);
+          const bool ln = args.r_stats != nullptr;
+          mbar_arrive_expect_tx(&res_full[slot], 2 * kBox + (ln ? 768 : 256));
           tma_load_2d_hint(rs, &maps.a, &res_full[slot], j * 64, mt * 128, pol_once);
           tma_load_2d_hint(rs + kBox, &maps.h, &res_full[slot], j * 64, mt * 128, pol_once);
+          uint8_t* vs = vec + slot * kVecBytes;
+          bulk_load(vs, args.bu + grp * args.slot_floats + j * 64, 256, &res_full[slot]);
+          if (ln) {
+            bulk_load(vs + 256, args.r_gamma + j * 64, 256, &res_full[slot]);
+            bulk_load(vs + 512, args.r_beta + j * 64, 256, &res_full[slot]);
+          }
           if (++slot == kResSlots) { slot = 0; phase ^= 1; }
         }
       }
@@ -263,8 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(mid_full);
       }
       // ---- E2: y chunks. Residual chunk j = 2c + half of this tile lives in ring slot
-      // (tile_j0 + j) % kResSlots; it is released as soon as a + LN(h) is in registers.
-      const float* bup = args.bu + static_cast<long long>(grp) * args.slot_floats;
+      // (tile_j0 + j) % kResSlots; it is released as soon as bu + a + LN(h) is in registers.
       float s1 = 0.f, s2 = 0.f;
       for (int c = 0; c < n_up; ++c, ++u) {
         const uint32_t b = u & 1;
@@ -272,6 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t j = tile_j0 + 2 * c + half;
         const uint32_t slot = j % kResSlots;
         const uint8_t* rs = res + slot * kResBytes;
+        const float* s_bu = reinterpret_cast<const float*>(vec + slot * kVecBytes);
+        const float* s_g = s_bu + 64;
+        const float* s_b = s_bu + 128;
         float v[64];
         if (lane == 0) {
           while (res_tag[slot] != j) {
@@ -291,14 +303,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int i = 8 * k + 2 * e;
             const float2 fa = unpack2<kBf16>(wa[e]);
             const float2 fh = unpack2<kBf16>(wh[e]);
+            const float2 bu2 = *reinterpret_cast<const float2*>(s_bu + i);
             if (args.r_stats != nullptr) {
-              const float2 g = __ldg(reinterpret_cast<const float2*>(args.r_gamma + col0 + i));
-              const float2 be = __ldg(reinterpret_cast<const float2*>(args.r_beta + col0 + i));
-              v[i] = fa.x + ((fh.x - rst.x) * rst.y * g.x + be.x);
-              v[i + 1] = fa.y + ((fh.y - rst.x) * rst.y * g.y + be.y);
+              const float2 g = *reinterpret_cast<const float2*>(s_g + i);
+              const float2 be = *reinterpret_cast<const float2*>(s_b + i);
+              v[i] = bu2.x + fa.x + ((fh.x - rst.x) * rst.y * g.x + be.x);
+              v[i + 1] = bu2.y + fa.y + ((fh.y - rst.x) * rst.y * g.y + be.y);
             } else {
-              v[i] = fa.x + fh.x;
-              v[i + 1] = fa.y + fh.y;
+              v[i] = bu2.x + fa.x + fh.x;
+              v[i + 1] = bu2.y + fa.y + fh.y;
             }
           }
         }
@@ -312,13 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x32(tmem + lane_off + 128 + b * kUpN + half * 64 + 32 * hh, t);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bup + col0 + 32 * hh + i));
-            v[32 * hh + i] += __uint_as_float(t[i]) + b4.x;
-            v[32 * hh + i + 1] += __uint_as_float(t[i + 1]) + b4.y;
-            v[32 * hh + i + 2] += __uint_as_float(t[i + 2]) + b4.z;
-            v[32 * hh + i + 3] += __uint_as_float(t[i + 3]) + b4.w;
-          }
+          for (int i = 0; i < 32; ++i) v[32 * hh + i] += __uint_as_float(t[i]);
         }
         tc_fence_before();
         __syncwarp();
@@ -369,6 +376,10 @@ AdapterPlan make_adapter_plan(const AdapterSpec& s) {
   HMI_CHECK(s.d % kUpN == 0 && s.d >= kUpN, HMI_CONFIG_ERROR,
             "fused adapter: hidden size must be a multiple of 128");
   HMI_CHECK(s.rows % 128 == 0, HMI_CONFIG_ERROR, "fused adapter: rows must be a multiple of 128");
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  HMI_CHECK(al16(s.arena + s.off_bu) && s.slot_bytes % 16 == 0 &&
+                (s.r_stats == nullptr || (al16(s.r_gamma) && al16(s.r_beta))),
+            HMI_CONFIG_ERROR, "fused adapter: bias / LayerNorm vectors must be 16-byte aligned");
   const CUtensorMapDataType t16 =
       s.precision == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   AdapterPlan p;
