@@ -241,6 +241,8 @@ def config_dict(wl, args, world_size):
         "seq_len": wl.seq,
         "parallelism": f"tenant-sharded x{world_size} (no collectives)",
         "pipeline": args.mode,
+        "hbm_slot_pool": f"{args.pool_fraction if args.pool_fraction is not None else wl.pool_fraction:.2f}"
+                         " of this GPU's tenants",
         "l2": "flushed (256 MiB write) before every timed step",
     }
 
@@ -266,7 +268,8 @@ def bench_ours(args, wl):
     higher = E.generate_higher(mc)
     my_tenants = [t for t in range(wl.n_tenants) if t % world_size == rank]
     ref_layer_bytes = (wl.hidden_size * wl.r * 2 + wl.r + wl.hidden_size) * 4
-    pool_bytes = int(max(wl.batch, wl.pool_fraction * len(my_tenants))) * wl.higher_layers * ref_layer_bytes
+    frac = args.pool_fraction if args.pool_fraction is not None else wl.pool_fraction
+    pool_bytes = int(max(wl.batch, frac * len(my_tenants))) * wl.higher_layers * ref_layer_bytes
     eng = E.GpuEngine(mc, higher, device=local, precision=args.precision, max_batch=wl.batch,
                       max_seq=wl.seq, bottleneck=wl.r, max_labels=wl.labels, pipeline_mode=mode,
                       pool_bytes=pool_bytes, max_tasks=wl.n_tenants,
@@ -280,8 +283,10 @@ def bench_ours(args, wl):
         eng.bind_instance(t, world.tenant_version(t), t, t)
 
     K, W = args.steps, args.warmup
+    # W warm-up batches, K timed device-resident batches, K fresh batches for the e2e pass
+    # (fresh so a swapping pool sees the same miss rate in both passes)
     batches = [world.requests(10_000 * (rank + 1) + s, wl.batch, tenants=my_tenants)
-               for s in range(W + K)]
+               for s in range(W + 2 * K)]
     dev = torch.device("cuda", local)
     d_tok = [torch.from_numpy(b[1].astype(np.int32)).to(dev) for b in batches]
     d_len = [torch.from_numpy(b[2].astype(np.int32)).to(dev) for b in batches]
@@ -351,7 +356,7 @@ def bench_ours(args, wl):
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for k in range(K):
-        inst, toks, lens = batches[W + k]
+        inst, toks, lens = batches[W + K + k]
         eng.infer_batch(inst, toks, lens)
     b.record(stream)
     torch.cuda.synchronize()
@@ -511,6 +516,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--mode", default="fine", choices=["sync", "coarse", "fine"])
     ap.add_argument("--precision", type=int, default=0)
+    ap.add_argument("--pool-fraction", type=float, default=None,
+                    help="HBM slot pool as a fraction of this rank's tenants (C4 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="timed device region only (for ncu)")
     args = ap.parse_args()

@@ -2,7 +2,7 @@
 """Summarise an `ncu --set full` capture of one C2 layer into profiles/ (text + json).
 
 The capture (tools_profile.sh) holds, in launch order: retrieve, then higher
-layers 0 and 1 (gemm_qkv, attention, gemm_oproj, adapter_down, adapter_up,
+layers 0 and 1 (gemm_qkv, attention, gemm_oproj, adapter (fused down+up),
 gemm_ffn1, gemm_ffn2 each; layer 1's QKV is the LN-folded variant). Keys
 without a suffix are layer 1 (the steady-state layer).
 """
@@ -13,14 +13,14 @@ import subprocess
 import sys
 
 # LayerNorm folded (default engine mode): retrieval, then layer 0 and layer 1
-LAYER = ["gemm_qkv", "attention", "gemm_oproj", "adapter_down", "adapter_up", "gemm_ffn1",
-         "gemm_ffn2"]
+LAYER = ["gemm_qkv", "attention", "gemm_oproj", "adapter_up", "gemm_ffn1", "gemm_ffn2"]
 ORDER = ["retrieve"] + [f"{k}@L0" for k in LAYER] + LAYER
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
            "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed",
            "smsp__cycles_active.avg", "sm__cycles_elapsed.avg.per_second"]
 
 
