@@ -279,8 +279,6 @@ struct Ctx {
   // one fused adapter kernel per layer (folded LN mode, r <= 64); HMI_ADAPTER=gemm selects the
   // two grouped GEMMs
   bool adapter_fused = true;
-  // shared-weight GEMMs: CTA pairs per cluster (2 = B tile multicast across two pairs)
-  int gemm_mc = 1;
   DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
   static constexpr int kStatsLd = kStatsStride;
   int stats1_bn = 0, stats2_bn = 0, stats1_n = 0, stats2_n = 0;
@@ -489,7 +487,7 @@ void Ctx::build_plans() {
     s.b = w.wqkv; s.N = 3 * d; s.groups = 1; s.b_ld = d; s.b_group_stride_bytes = size_t(3) * d * d * 2;
     s.bias = w.bqkv; s.bias_group_stride = 0; s.tile_slot = nullptr;
     s.res0 = s.res1 = nullptr; s.res_ld = 0;
-    s.c = qkv_at(l); s.c_ld = 3 * d; s.epi = 0; s.cta2 = true; s.mc = gemm_mc;
+    s.c = qkv_at(l); s.c_ld = 3 * d; s.epi = 0; s.cta2 = true;
     s.bn = pick_bn(3 * d, m_tiles, sms, true);
     w.qkv = make_gemm_plan(s);
     // O projection
@@ -519,7 +517,7 @@ void Ctx::build_plans() {
     s.b = w.w1; s.N = f; s.groups = 1; s.b_ld = d; s.b_group_stride_bytes = size_t(f) * d * 2;
     s.bias = w.b1; s.bias_group_stride = 0; s.tile_slot = nullptr;
     s.res0 = s.res1 = nullptr;
-    s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.cta2 = true; s.mc = gemm_mc;
+    s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.cta2 = true;
     s.bn = pick_bn(f, m_tiles, sms, true);
     w.ffn1 = make_gemm_plan(s);
     // FFN2 + residual: y = ffn . W2 + b2 + x
@@ -540,7 +538,7 @@ void Ctx::build_plans() {
         q.a = h16.p; q.a_ld = d; q.K = d;
         q.b = w.wqkv_f; q.N = 3 * d; q.groups = 1; q.b_ld = d;
         q.b_group_stride_bytes = size_t(3) * d * d * 2;
-        q.bias = w.bqkv_f; q.c = qkv_at(l); q.c_ld = 3 * d; q.epi = kEpiFoldLN; q.cta2 = true; q.mc = gemm_mc;
+        q.bias = w.bqkv_f; q.c = qkv_at(l); q.c_ld = 3 * d; q.epi = kEpiFoldLN; q.cta2 = true;
         q.a_stats = d_stats2.p; q.a_stats_n = stats2_n; q.colsum = w.cs_qkv; q.inv_n = inv_d;
         q.bn = pick_bn(3 * d, m_tiles, sms, true);
         w.qkv = make_gemm_plan(q);
@@ -587,7 +585,7 @@ void Ctx::build_plans() {
         g.a_rows = max_rows;
         g.a = x16.p; g.a_ld = d; g.K = d;
         g.b = w.w1_f; g.N = f; g.groups = 1; g.b_ld = d; g.b_group_stride_bytes = size_t(f) * d * 2;
-        g.bias = w.b1_f; g.c = ffn16.p; g.c_ld = f; g.epi = kEpiRelu | kEpiFoldLN; g.cta2 = true; g.mc = gemm_mc;
+        g.bias = w.b1_f; g.c = ffn16.p; g.c_ld = f; g.epi = kEpiRelu | kEpiFoldLN; g.cta2 = true;
         g.a_stats = d_stats1.p; g.a_stats_n = stats1_n; g.colsum = w.cs_1; g.inv_n = inv_d;
         g.bn = pick_bn(f, m_tiles, sms, true);
         w.ffn1 = make_gemm_plan(g);
@@ -599,7 +597,7 @@ void Ctx::build_plans() {
         g.a = ffn16.p; g.a_ld = f; g.K = f;
         g.b = w.w2; g.N = d; g.groups = 1; g.b_ld = f; g.b_group_stride_bytes = size_t(d) * f * 2;
         g.bias = w.b2; g.res0 = x16.p; g.res_ld = d; g.c = h16.p; g.c_ld = d;
-        g.epi = kEpiRes1 | kEpiRes0LN | kEpiStats; g.cta2 = true; g.mc = gemm_mc;
+        g.epi = kEpiRes1 | kEpiRes0LN | kEpiStats; g.cta2 = true;
         g.stats_out = d_stats2.p; g.stats_ld = kStatsLd;
         g.r_stats = d_stats1.p; g.r_stats_n = stats1_n; g.r_gamma = w.ln1g; g.r_beta = w.ln1b;
         g.inv_n = inv_d;
@@ -1433,7 +1431,6 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     if (const char* env = std::getenv("HMI_ATTN")) c.attn_tc = std::string(env) != "mma";
     c.adapter_fused = c.r_pad == 64 && c.d % 128 == 0;
     if (const char* env = std::getenv("HMI_ADAPTER")) c.adapter_fused &= std::string(env) != "gemm";
-    if (const char* env = std::getenv("HMI_GEMM_MC")) c.gemm_mc = std::atoi(env) == 2 ? 2 : 1;
     c.d_stats1.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.d_stats2.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.build_plans();

@@ -17,14 +17,10 @@ namespace {
 
 using KernelFn = void (*)(GemmMaps, GemmArgs);
 
-// pair kernels come in two cluster shapes; g_mc selects which one kernel_ptr returns
-thread_local int g_mc = 1;
-
 template <int BN, int EPI, bool C2>
 KernelFn kernel_ptr() {
   if constexpr (C2) {
-    if (g_mc == 2) return reinterpret_cast<KernelFn>(&gemm2_tcgen05_kernel<BN, EPI, 2>);
-    return reinterpret_cast<KernelFn>(&gemm2_tcgen05_kernel<BN, EPI, 1>);
+    return reinterpret_cast<KernelFn>(&gemm2_tcgen05_kernel<BN, EPI>);
   } else {
     return reinterpret_cast<KernelFn>(&gemm_tcgen05_kernel<BN, EPI>);
   }
@@ -127,17 +123,14 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
     p.cluster_n = s.N / s.bn;
   }
   p.two_cta = c2;
-  p.mc = c2 ? s.mc : 1;
-  g_mc = p.mc;
   p.fn = reinterpret_cast<void*>(pick_kernel(s.bn, epi, c2, &p.smem_bytes));
-  g_mc = 1;
   HMI_CHECK(p.fn != nullptr, HMI_CONFIG_ERROR, "gemm: unsupported epilogue");
   const CUtensorMapDataType t16 =
       s.precision == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   p.maps.a = make_tmap_2d(s.a, t16, s.K, s.a_rows, s.a_ld * 2ull, kBlockK, kBlockM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
   p.maps.b = make_tmap_3d(s.b, t16, s.K, s.N, s.groups, s.b_ld * 2ull, s.b_group_stride_bytes,
-                         kBlockK, c2 ? s.bn / (2 * p.mc) : s.bn, CU_TENSOR_MAP_SWIZZLE_128B);
+                         kBlockK, c2 ? s.bn / 2 : s.bn, CU_TENSOR_MAP_SWIZZLE_128B);
   const bool f32 = (s.epi & kEpiOutF32) != 0 && !ln;
   p.maps.c = make_tmap_2d(s.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : t16, s.N, s.a_rows,
                          s.c_ld * (f32 ? 4ull : 2ull), f32 ? 32 : 64, 32,
@@ -186,15 +179,15 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.idesc = idesc_f16(c2 ? 2 * kBlockM : kBlockM, s.bn, s.precision == 1 ? 1u : 0u);
   p.max_rows = s.a_rows;
   if (c2) {
-    // co-resident clusters of 2 * mc CTAs (GPCs need not divide evenly into clusters)
+    // co-resident CTA pairs (GPCs need not divide evenly into clusters)
     HMI_CUDA(cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * p.mc * (device_sm_count() / (2 * p.mc)));
+    cfg.gridDim = dim3(2 * (device_sm_count() / 2));
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2 * p.mc;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -202,12 +195,12 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, p.fn, &cfg) != cudaSuccess || n <= 0) {
       cudaGetLastError();
-      n = device_sm_count() / (2 * p.mc);
+      n = device_sm_count() / 2;
     }
     p.max_clusters = n;
     if (std::getenv("HMI_DEBUG_PLAN")) {
-      std::fprintf(stderr, "gemm plan: pair kernel bn=%d mc=%d smem=%d max_clusters=%d\n", s.bn,
-                   p.mc, p.smem_bytes, n);
+      std::fprintf(stderr, "gemm plan: pair kernel bn=%d smem=%d max_clusters=%d\n", s.bn,
+                   p.smem_bytes, n);
     }
   }
   if (ln) {
@@ -280,7 +273,7 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
     return;
   }
   if (p.two_cta) {
-    const int rows = 2 * p.mc;  // M tiles per cluster unit
+    const int rows = 2;  // M tiles per pair unit
     const int units = (a.num_m_tiles + rows - 1) / rows * a.num_n_tiles;
     const int clusters = p.max_clusters > 0 ? p.max_clusters : device_sm_count() / rows;
     grid = rows * (units < clusters ? units : clusters);
@@ -304,8 +297,7 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
                                   const uint16_t* res1, int epi, int bn, int precision,
                                   void* out, float* elapsed_ms) {
   const bool cta2 = (epi & 256) != 0;  // probe flag: request the cta_group::2 kernel
-  const int mc = (epi & 4096) != 0 ? 2 : 1;  // probe flag: clusters of two pairs (B multicast)
-  epi &= ~(256 | 4096);
+  epi &= ~256;
   using namespace hmi_b200;
   void *dA = nullptr, *dB = nullptr, *dBias = nullptr, *dC = nullptr, *dSlot = nullptr,
        *dR0 = nullptr, *dR1 = nullptr;
@@ -343,7 +335,7 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
     s.tile_slot = static_cast<const int*>(dSlot);
     s.res0 = dR0; s.res1 = dR1; s.res_ld = N;
     s.c = dC; s.c_ld = N;
-    s.epi = epi; s.bn = bn; s.precision = precision; s.cta2 = cta2; s.mc = mc;
+    s.epi = epi; s.bn = bn; s.precision = precision; s.cta2 = cta2;
     GemmPlan p = make_gemm_plan(s);
     HMI_CUDA(cudaEventCreate(&e0));
     HMI_CUDA(cudaEventCreate(&e1));

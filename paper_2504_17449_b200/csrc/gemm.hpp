@@ -76,7 +76,6 @@ struct GemmSpec {
   int bn = 256;                      // N tile
   int precision = 0;                 // 0 fp16, 1 bf16
   bool cta2 = false;                 // cta_group::2 pair kernel (shared weights only)
-  int mc = 1;                        // pair kernel: CTA pairs per cluster (2 = B multicast)
   const float* ln_gamma = nullptr;   // kEpiLN
   const float* ln_beta = nullptr;
   void* c2 = nullptr;                // kEpiOut2F32: f32 copy [a_rows][c2_ld]
@@ -100,7 +99,6 @@ struct GemmPlan {
   int smem_bytes = 0;
   int max_rows = 0;
   bool two_cta = false;
-  int mc = 1;
   int cluster_n = 1;     // kEpiLN: CTAs per cluster along N (= N / BN)
   int max_clusters = 0;  // kEpiLN: co-resident clusters (cudaOccupancyMaxActiveClusters)
 };

@@ -702,15 +702,8 @@ struct Gemm2Smem {
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
 };
 
-// MC = CTA pairs per cluster. MC = 2: a cluster of 4 CTAs computes a 512 x BN block as two
-// pairs that share the B tile: CTA (pair p, rank r) TMA-loads quarter p of B half r and
-// multicasts it to CTA (0, r) and (1, r), halving B's L2 -> SM traffic (the shared GEMMs run
-// at the L2 throughput cap with unicast operands). Multicast bytes complete on each
-// destination's own full barrier; in a pair's rank-1 CTA a relay thread (warp 1) forwards
-// that completion to the pair leader's full barrier, which the MMA issuer waits on. Each
-// stage's empty barrier waits for both pairs' MMA commits.
-template <int BN, int EPI, int MC>
-__global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kGemmThreads, 1)
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm2_tcgen05_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args) {
   const CUtensorMap& map_a = maps.a;
   const CUtensorMap& map_b = maps.b;
@@ -719,7 +712,6 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kGemmThreads, 1
   constexpr int kStages = L::kStages;
   static_assert(kStages >= 3, "smem budget too small");
   static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "BN");
-  static_assert(MC == 1 || MC == 2, "MC");
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -736,15 +728,11 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kGemmThreads, 1
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t crank = cluster_ctarank();
-  const uint32_t rank = crank & 1;          // rank inside the pair
-  const uint32_t pair = crank >> 1;         // pair inside the cluster
-  const uint32_t leader = crank & ~1u;      // this pair's leader (cluster rank)
-  constexpr int kRows = 2 * MC;             // M tiles per unit
-  const int n_groups = (args.num_m_tiles + kRows - 1) / kRows;
-  const int num_units = n_groups * args.num_n_tiles;
-  const int cluster = blockIdx.x / (2 * MC);
-  const int n_clusters = gridDim.x / (2 * MC);
+  const uint32_t rank = cluster_ctarank();
+  const int n_pairs = (args.num_m_tiles + 1) / 2;
+  const int num_units = n_pairs * args.num_n_tiles;
+  const int cluster = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
   const int num_kb = args.K / kBlockK;
 
   if (warp == 0 && lane == 0) {
@@ -752,8 +740,8 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kGemmThreads, 1
     tma_prefetch_desc(&map_b);
     tma_prefetch_desc(&map_c);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], (MC == 2 && rank == 0) ? 2 : 1);  // MC = 2: + the peer's relay
-      mbar_init(&empty[s], MC);  // one commit per pair sharing the stage's B
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -768,63 +756,31 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kGemmThreads, 1
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (all CTAs)
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_first();
       const uint64_t pol_b = policy_evict_last();
       uint32_t stage = 0, phase = 0;
-      const uint32_t leader_full0 = mapa_shared(smem_u32(&full[0]), leader);
       for (int u = cluster; u < num_units; u += n_clusters) {
-        const int mg = u / args.num_n_tiles;
-        const int nt = u - mg * args.num_n_tiles;
-        const int mt = kRows * mg + static_cast<int>(crank);
+        const int mp = u / args.num_n_tiles;
+        const int nt = u - mp * args.num_n_tiles;
+        const int mt = 2 * mp + static_cast<int>(rank);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if constexpr (MC == 1) {
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
-          } else {
-            // leader: both A tiles + its B half (two multicast quarters); rank 1: its B half
-            mbar_arrive_expect_tx(&full[stage],
-                                  rank == 0 ? 2 * L::kABytes + L::kBBytes : L::kBBytes);
-          }
-          const uint32_t leader_full = leader_full0 + stage * 8;
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
+          const uint32_t leader_full = mapa_shared(smem_u32(&full[stage]), 0);
           tma_load_2d_2sm(sA + stage * L::kABytes, &map_a, leader_full, kb * kBlockK,
                           mt * kBlockM, pol_a);
-          if constexpr (MC == 1) {
-            tma_load_3d_2sm(sB + stage * L::kBBytes, &map_b, leader_full, kb * kBlockK,
-                            nt * BN + static_cast<int>(rank) * (BN / 2), 0, pol_b);
-          } else {
-            // quarter `pair` of B half `rank`, to CTA `rank` of both pairs
-            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
-            tma_load_3d_mc(sB + stage * L::kBBytes + pair * (L::kBBytes / 2), &map_b,
-                           &full[stage], kb * kBlockK,
-                           nt * BN + static_cast<int>(rank) * (BN / 2) +
-                               static_cast<int>(pair) * (BN / 4),
-                           0, mask, pol_b);
-          }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1 && MC == 2 && rank == 1) {
-    // ------------------------------------------------------------ relay (pair rank 1)
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      const uint32_t leader_full0 = mapa_shared(smem_u32(&full[0]), leader);
-      for (int u = cluster; u < num_units; u += n_clusters) {
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          mbar_arrive_cluster(leader_full0 + stage * 8);
+          tma_load_3d_2sm(sB + stage * L::kBBytes, &map_b, leader_full, kb * kBlockK,
+                          nt * BN + static_cast<int>(rank) * (BN / 2), 0, pol_b);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (pair leaders)
+    // ------------------------------------------------------------ MMA issuer (leader only)
     if (rank == 0 && lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      const uint16_t pair_mask = static_cast<uint16_t>(0x3u << crank);
-      const uint16_t stage_mask = MC == 1 ? 0x3 : 0xF;
       for (int u = cluster; u < num_units; u += n_clusters) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -838,25 +794,25 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kGemmThreads, 1
           for (int k = 0; k < kBlockK / 16; ++k) {
             umma_f16_2cta(d_tmem, a_desc + 2 * k, b_desc + 2 * k, args.idesc, (kb | k) != 0);
           }
-          umma_commit_2cta_mc(&empty[stage], stage_mask);
+          umma_commit_2cta_mc(&empty[stage], 0x3);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit_2cta_mc(&tfull[acc], pair_mask);
+        umma_commit_2cta_mc(&tfull[acc], 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (all CTAs)
+    // ------------------------------------------------------------ epilogue (both CTAs)
     const uint32_t q = warp & 3;
     const int half = static_cast<int>(warp - 2) >> 2;
     uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
     uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0;
     for (int u = cluster; u < num_units; u += n_clusters) {
-      const int mg = u / args.num_n_tiles;
-      const int nt = u - mg * args.num_n_tiles;
-      const int mt = kRows * mg + static_cast<int>(crank);
+      const int mp = u / args.num_n_tiles;
+      const int nt = u - mp * args.num_n_tiles;
+      const int mt = 2 * mp + static_cast<int>(rank);
       float2 a_st, r_st;
       epi_row_stats<EPI>(args, mt, q, lane, a_st, r_st);
       mbar_wait(&tfull[acc], acc_phase);
@@ -865,7 +821,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kGemmThreads, 1
                              lane, a_st, r_st, nullptr);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), leader));
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }

@@ -343,20 +343,6 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* smem_dst, const CUtensorMa
       : "memory");
 }
 
-// Multicast TMA: the box lands at the same smem offset in every CTA of `mask`, and each
-// destination's transaction bytes complete on the mbarrier at `bar`'s offset in that CTA.
-__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map,
-                                               uint64_t* bar, int32_t x, int32_t y, int32_t z,
-                                               uint16_t mask, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "h"(mask),
-      "l"(policy)
-      : "memory");
-}
-
 // ---------------------------------------------------------------------------
 // UMMA descriptors
 // ---------------------------------------------------------------------------
