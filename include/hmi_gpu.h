@@ -170,6 +170,18 @@ int hmi_gpu_infer_batch_device(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t*
  * bound to the same wide lm head. out_tokens / out_logits: [n_req x n_new]
  * (out_logits nullable: the chosen token's f64-rescored logit).
  * Errors: n_new > max_new_tokens or encoder mode -> CONFIG.                  */
+/* Asynchronous form of hmi_gpu_infer_batch for pipelined serving: the batch is enqueued
+ * (inputs staged in pinned memory, H2D / compute / D2H on the context's streams) and a ticket
+ * returned at once; hmi_gpu_wait_batch blocks until that batch finished and copies its
+ * scores [n_req x max_labels] and labels out. At most 4 batches may be outstanding
+ * (HMI_CAPACITY_ERROR beyond). Replaces nothing in the reference, whose scheduler drains
+ * one batch at a time; it is how a serving loop overlaps batch k+1's host
+ * work and copies with batch k's compute. */
+int hmi_gpu_submit_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                         const uint32_t* tokens, uint32_t stride, const uint32_t* lens,
+                         uint64_t* ticket);
+int hmi_gpu_wait_batch(hmi_gpu_ctx* ctx, uint64_t ticket, float* scores, int32_t* labels);
+
 int hmi_gpu_generate(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
                      const uint32_t* tokens, uint32_t stride, const uint32_t* lens,
                      uint32_t n_new, int32_t* out_tokens, float* out_logits);

@@ -118,6 +118,8 @@ def _sig(L):
                                       P(LoadRecord), u32, u32p, u32, u32p]
     L.hmi_gpu_infer_batch_device.argtypes = [vp, u32, u32p, vp, u32, vp, u32, vp, vp]
     L.hmi_gpu_generate.argtypes = [vp, u32, u32p, u32p, u32, u32p, u32, i32p, f32p]
+    L.hmi_gpu_submit_batch.argtypes = [vp, u32, u32p, u32p, u32, u32p, u64p]
+    L.hmi_gpu_wait_batch.argtypes = [vp, u64, f32p, i32p]
     L.hmi_gpu_synchronize.argtypes = [vp]
     L.hmi_gpu_stream.argtypes = [vp]
     L.hmi_gpu_stream.restype = vp

@@ -120,6 +120,10 @@ struct Staging {
   int32_t* err = nullptr;
   cudaEvent_t done = nullptr;
   bool busy = false;
+  // asynchronous submission (hmi_gpu_submit_batch): results held here until collected
+  bool held = false;
+  uint64_t ticket = 0;
+  uint32_t n_req = 0;
 };
 
 struct Inflight {
@@ -260,6 +264,7 @@ struct Ctx {
   size_t chunk_left = 0;
   uint64_t bytes_copied = 0;
   uint64_t n_launches = 0, n_batches = 0, n_copies = 0;
+  uint64_t next_ticket = 0;
   std::vector<void*> cp_dst, cp_src;
   std::vector<size_t> cp_size;
   bool use_batch_copy = std::getenv("HMI_BATCH_COPY") == nullptr ||
@@ -706,6 +711,8 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
                 std::vector<int32_t>* record_layer, uint32_t n_new) {
   HMI_CHECK(n_req >= 1 && n_req <= opt.max_batch, HMI_DIMENSION_ERROR,
             "batch size must be in [1, max_batch]");
+  HMI_CHECK(!stg[stg_next].held, HMI_CAPACITY_ERROR,
+            "too many outstanding submitted batches: wait on the oldest ticket first");
   const bool gen = n_new > 0;
   HMI_CHECK(!gen || (kv && n_new <= opt.max_new_tokens), HMI_CONFIG_ERROR,
             "generation needs max_new_tokens >= n_new (causal model)");
@@ -1012,7 +1019,8 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   st.busy = true;
   inflight.push_back(Inflight{st.done, si, uniq});
   last_n = n_req;
-  n_launches += (delta.empty() ? 0 : 1) + 2 + (gen ? 0 : 1) + (ln_mode == 1 ? 9ull : 7ull) * L;
+  const uint64_t per_layer = ln_mode == 1 ? 9ull : (ln_mode == 0 && adapter_fused) ? 6ull : 7ull;
+  n_launches += (delta.empty() ? 0 : 1) + 2 + (gen ? 0 : 1) + per_layer * L;
   if (wide_head >= 0) n_launches += 3 + (gen ? (n_new - 1ull) * (3 + 7ull * L) : 0);
   ++n_batches;
   last_S = static_cast<uint32_t>(S);
@@ -1744,6 +1752,46 @@ int hmi_gpu_infer_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instan
     if (c.prof) c.prof_collect();
     c.reap(false);
     if (want) fill_trace(recs, tag, trace, trace_cap, evicted, evicted_cap, n_trace);
+    if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
+  });
+}
+
+int hmi_gpu_submit_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_idx,
+                         const uint32_t* tokens, uint32_t stride, const uint32_t* lens,
+                         uint64_t* ticket) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(ticket != nullptr, HMI_CONFIG_ERROR, "null ticket");
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    const int si = c.submit(n_req, instance_idx, tokens, nullptr, stride, lens, nullptr, 0, nullptr,
+                            nullptr, nullptr, nullptr);
+    Staging& st = c.stg[si];
+    st.held = true;
+    st.ticket = ++c.next_ticket;
+    st.n_req = n_req;
+    *ticket = st.ticket;
+  });
+}
+
+int hmi_gpu_wait_batch(hmi_gpu_ctx* ctx, uint64_t ticket, float* scores, int32_t* labels) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    Staging* st = nullptr;
+    for (Staging& x : c.stg)
+      if (x.held && x.ticket == ticket) st = &x;
+    HMI_CHECK(st != nullptr, HMI_CONFIG_ERROR, "unknown or already collected ticket");
+    HMI_CUDA(cudaEventSynchronize(st->done));
+    st->held = false;
+    const int err = *st->err;
+    if (scores) std::memcpy(scores, st->scores, static_cast<size_t>(st->n_req) * c.opt.max_labels * 4);
+    if (labels) std::memcpy(labels, st->labels, st->n_req * 4);
+    if (c.prof) c.prof_collect();
+    c.reap(false);
     if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
   });
 }

@@ -78,6 +78,7 @@ class GpuEngine:
                  max_heads: int = 0, max_versions: int = 64, max_new_tokens: int = 0):
         self.cfg = cfg
         self.max_labels = max_labels
+        self._pending: dict[int, int] = {}
         self.max_batch = max_batch
         self.max_seq = max_seq
         opts = Options(precision, max_batch, max_seq, bottleneck, max_labels, pipeline_mode,
@@ -159,6 +160,27 @@ class GpuEngine:
                               "bytes": r.bytes,
                               "evicted": [int(x) for x in ev[r.evicted_offset:r.evicted_offset + r.n_evicted]]})
         return BatchResult(scores, labels, tags, trace)
+
+    def submit_batch(self, instance_idx, tokens, lens) -> int:
+        """Enqueue a batch (host buffers) and return its ticket at once (hmi_gpu_submit_batch)."""
+        inst = np.ascontiguousarray(instance_idx, np.uint32)
+        toks = np.ascontiguousarray(tokens, np.uint32)
+        ln = np.ascontiguousarray(lens, np.uint32)
+        t = ctypes.c_uint64(0)
+        check(_native.lib().hmi_gpu_submit_batch(self.h, inst.shape[0], _p(inst, ctypes.c_uint32),
+                                                 _p(toks, ctypes.c_uint32), toks.shape[1],
+                                                 _p(ln, ctypes.c_uint32), ctypes.byref(t)))
+        self._pending[t.value] = inst.shape[0]
+        return t.value
+
+    def wait_batch(self, ticket: int) -> BatchResult:
+        """Block until a submitted batch finished; its scores and labels (hmi_gpu_wait_batch)."""
+        n = self._pending.pop(ticket)
+        scores = np.zeros((n, self.max_labels), np.float32)
+        labels = np.zeros(n, np.int32)
+        check(_native.lib().hmi_gpu_wait_batch(self.h, ticket, _p(scores, ctypes.c_float),
+                                               _p(labels, ctypes.c_int32)))
+        return BatchResult(scores, labels, None, [])
 
     def infer_batch_device(self, instance_idx, d_tokens: int, stride: int, d_lens: int,
                            max_len: int, d_scores: int, d_labels: int) -> None:

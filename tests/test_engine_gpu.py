@@ -86,6 +86,23 @@ def test_c1_permutation_and_batch_independence(c1):
     assert np.array_equal(single.scores[0], a.scores[0])
 
 
+def test_submit_wait_pipelined_matches_sync(c1):
+    """hmi_gpu_submit_batch / hmi_gpu_wait_batch (up to four batches in flight) return
+    exactly what the synchronous call returns; a fifth outstanding batch is refused."""
+    from paper_2504_17449_b200._native import CapacityError
+
+    reqs = [c1.requests(100 + k, 8 + 4 * k, 128) for k in range(5)]
+    sync = [c1.eng.infer_batch(*r) for r in reqs]
+    tickets = [c1.eng.submit_batch(*r) for r in reqs[:4]]
+    with pytest.raises(CapacityError):
+        c1.eng.submit_batch(*reqs[4])
+    outs = [c1.eng.wait_batch(t) for t in tickets]
+    t4 = c1.eng.submit_batch(*reqs[4])
+    outs.append(c1.eng.wait_batch(t4))
+    for a, b in zip(sync, outs):
+        assert np.array_equal(a.scores, b.scores) and np.array_equal(a.labels, b.labels)
+
+
 def test_c1_swap_small_pool_bit_identical(c1):
     """A pool holding only 3 tasks forces evictions and reloads every batch; outputs
     are bit-identical to the all-resident run and the trace obeys the LRU law."""
