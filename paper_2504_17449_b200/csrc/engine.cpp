@@ -465,15 +465,14 @@ void Ctx::build_plans() {
   for (int l = 0; l < (kv ? L : 1); ++l)
     attn.push_back(make_attention_plan(qkv_at(l), ctx16.p, max_rows, d, static_cast<int>(opt.precision)));
   const int sms = device_sm_count();
-  {  // statistics producers' N tiles fix the number of partials per row
+  {  // GEMM statistics producers emit one partial per 64-column group of the row; the fused
+     // adapter one per column half
     const int mt = max_rows / 128;
-    // each producer N tile emits two partials per row: at most kStatsLd of them
-    const int min_bn = (2 * d + kStatsLd - 1) / kStatsLd;
-    stats1_bn = pick_bn(d, mt, sms, false, min_bn);
-    stats2_bn = pick_bn(d, mt, sms, true, min_bn);
-    stats1_n = adapter_fused ? 2 : 2 * (d / stats1_bn);
-    stats2_n = 2 * (d / stats2_bn);
-    HMI_CHECK(stats1_n <= kStatsLd && stats2_n <= kStatsLd, HMI_CONFIG_ERROR,
+    stats1_bn = pick_bn(d, mt, sms);
+    stats2_bn = pick_bn(d, mt, sms, true);
+    stats1_n = adapter_fused ? 2 : d / 64;
+    stats2_n = d / 64;
+    HMI_CHECK(d % 64 == 0 && d / 64 <= kStatsLd, HMI_CONFIG_ERROR,
               "hidden size too wide for the LayerNorm statistics buffer");
   }
   const int m_tiles = max_rows / 128;

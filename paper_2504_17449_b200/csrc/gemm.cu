@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "gemm_tcgen05.cuh"
@@ -145,6 +146,22 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
     p.maps.r1 = make_tmap_2d(s.res1, t16, s.N, s.a_rows, s.res_ld * 2ull, 64, 128,
                              CU_TENSOR_MAP_SWIZZLE_128B);
   }
+  p.precision = s.precision;
+  p.bn = s.bn;
+  p.tail_enabled = std::getenv("HMI_GEMM_TAIL") == nullptr ||
+                   std::string(std::getenv("HMI_GEMM_TAIL")) != "0";
+  if (c2) {
+    // wave-tail sub-tile widths must stay multiples of 64 columns (the epilogue's store chunk)
+    const int g = s.bn / 64;
+    p.tail_s0 = g % 2 == 0 ? 2 : g % 3 == 0 ? 3 : 0;
+    p.tail_s1 = g % 4 == 0 ? 4 : p.tail_s0;
+    if (p.tail_s0) {
+      p.maps.r0 = make_tmap_3d(s.b, t16, s.K, s.N, s.groups, s.b_ld * 2ull, s.b_group_stride_bytes,
+                               kBlockK, s.bn / (2 * p.tail_s0), CU_TENSOR_MAP_SWIZZLE_128B);
+      p.maps.r1 = make_tmap_3d(s.b, t16, s.K, s.N, s.groups, s.b_ld * 2ull, s.b_group_stride_bytes,
+                               kBlockK, s.bn / (2 * p.tail_s1), CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+  }
   if (s.epi & kEpiOut2F32) {
     HMI_CHECK(s.c2 != nullptr, HMI_CONFIG_ERROR, "gemm: f32 copy output missing");
     p.maps.c2 = make_tmap_2d(s.c2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, s.N, s.a_rows, s.c2_ld * 4ull,
@@ -172,7 +189,7 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.r_gamma = s.r_gamma;
   p.args.r_beta = s.r_beta;
   p.args.inv_n = s.inv_n;
-  if (s.epi & kEpiStats) HMI_CHECK(s.stats_out && s.stats_ld == kStatsStride && 2 * (s.N / s.bn) <= kStatsStride, HMI_CONFIG_ERROR, "gemm: stats buffer");
+  if (s.epi & kEpiStats) HMI_CHECK(s.stats_out && s.stats_ld == kStatsStride && s.N % 64 == 0 && s.N / 64 <= kStatsStride, HMI_CONFIG_ERROR, "gemm: stats buffer");
   if (s.epi & kEpiFoldLN) HMI_CHECK(s.a_stats && s.colsum && s.inv_n > 0.f, HMI_CONFIG_ERROR, "gemm: fold args");
   if (s.epi & (kEpiRes0LN | kEpiRes1LN))
     HMI_CHECK(s.r_stats && s.r_gamma && s.r_beta && s.inv_n > 0.f, HMI_CONFIG_ERROR, "gemm: residual LN args");
@@ -272,11 +289,31 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
     HMI_CUDA(cudaLaunchKernelEx(&cfg, fn, p.maps, a));
     return;
   }
+  a.n_main = 0;
+  a.tail_split = 1;
+  a.idesc_tail = a.idesc;
+  a.tail_r1 = 0;
   if (p.two_cta) {
     const int rows = 2;  // M tiles per pair unit
     const int units = (a.num_m_tiles + rows - 1) / rows * a.num_n_tiles;
     const int clusters = p.max_clusters > 0 ? p.max_clusters : device_sm_count() / rows;
     grid = rows * (units < clusters ? units : clusters);
+    // the last partial wave of R units runs as R x S narrower sub-tiles (R x S <= clusters)
+    const int R = units > clusters ? units % clusters : 0;
+    if (p.tail_enabled && R > 0 && p.tail_s0) {
+      int S = 1;
+      if (p.tail_s1 > 1 && R * p.tail_s1 <= clusters) {
+        S = p.tail_s1;
+        a.tail_r1 = 1;
+      } else if (R * p.tail_s0 <= clusters) {
+        S = p.tail_s0;
+      }
+      if (S > 1) {
+        a.tail_split = S;
+        a.n_main = units - R;
+        a.idesc_tail = idesc_f16(2 * kBlockM, p.bn / S, p.precision == 1 ? 1u : 0u);
+      }
+    }
   } else {
     const int tiles = a.num_m_tiles * a.num_n_tiles;
     grid = tiles < device_sm_count() ? tiles : device_sm_count();
@@ -297,7 +334,8 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
                                   const uint16_t* res1, int epi, int bn, int precision,
                                   void* out, float* elapsed_ms) {
   const bool cta2 = (epi & 256) != 0;  // probe flag: request the cta_group::2 kernel
-  epi &= ~256;
+  const bool no_tail = (epi & 8192) != 0;  // probe flag: no wave-tail sub-tiles
+  epi &= ~(256 | 8192);
   using namespace hmi_b200;
   void *dA = nullptr, *dB = nullptr, *dBias = nullptr, *dC = nullptr, *dSlot = nullptr,
        *dR0 = nullptr, *dR1 = nullptr;
@@ -337,6 +375,7 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
     s.c = dC; s.c_ld = N;
     s.epi = epi; s.bn = bn; s.precision = precision; s.cta2 = cta2;
     GemmPlan p = make_gemm_plan(s);
+    if (no_tail) p.tail_enabled = false;
     HMI_CUDA(cudaEventCreate(&e0));
     HMI_CUDA(cudaEventCreate(&e1));
     launch_gemm(p, M, 0);  // warm-up / first launch

@@ -34,6 +34,13 @@ struct GemmArgs {
   const float* r_gamma;        // LayerNorm applied on the fly to that residual
   const float* r_beta;
   float inv_n;                 // 1 / (row width the statistics cover)
+  // pair kernel wave-tail split: units [0, n_main) run whole; each of the remaining units is
+  // cut into tail_split narrower N sub-tiles (MMA N = BN / tail_split, idesc_tail) so the last
+  // partial wave spreads over more SMs. Per-element K order is unchanged (bit-identical).
+  int n_main;
+  int tail_split;
+  uint32_t idesc_tail;
+  int tail_r1;                 // tail B boxes through maps.r1 (else maps.r0)
 };
 
 // Epilogue flags
@@ -46,7 +53,8 @@ constexpr int kEpiLN = 32;    // LayerNorm over the row (cluster of N/BN CTAs), 
 constexpr int kEpiOut2F32 = 64;  // with kEpiLN: also write an f32 copy through map_c2
 constexpr int kEpiResTma = 128;  // with kEpiLN: residual tiles TMA-prefetched into smem
 // LayerNorm folding: LN(y) is never materialised; its consumers apply it.
-constexpr int kEpiStats = 256;   // write per-row partial (sum, sumsq) of the output
+constexpr int kEpiStats = 256;   // write per-row partial (sum, sumsq) of the output, one per
+                                 // 64-column group (16-bit outputs only)
 constexpr int kStatsStride = 16; // float2 entries per row of a partial-statistics buffer
 constexpr int kEpiFoldLN = 512;  // A is pre-norm y: out = inv*(acc - mean*colsum) + bias
 constexpr int kEpiRes0LN = 1024; // residual res0 is pre-norm: add LN(res0) (r_* args)
@@ -99,6 +107,9 @@ struct GemmPlan {
   int smem_bytes = 0;
   int max_rows = 0;
   bool two_cta = false;
+  int tail_s0 = 0, tail_s1 = 0;  // pair kernel: tail splits served by maps.r0 / maps.r1 (0: none)
+  bool tail_enabled = true;      // HMI_GEMM_TAIL=0 disables the wave-tail split
+  int precision = 0, bn = 0;
   int cluster_n = 1;     // kEpiLN: CTAs per cluster along N (= N / BN)
   int max_clusters = 0;  // kEpiLN: co-resident clusters (cudaOccupancyMaxActiveClusters)
 };

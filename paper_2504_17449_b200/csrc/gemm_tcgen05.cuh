@@ -175,24 +175,25 @@ __device__ __forceinline__ void epi_row_stats(const GemmArgs& args, int mt, uint
 // row statistics; kEpiRes{0,1}LN normalise a pre-norm residual on the fly; kEpiStats
 // emits this thread's partial row (sum, sumsq) for the next consumer.
 template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, int grp,
-                                              const GemmArgs& args, const CUtensorMap* map_c,
-                                              uint8_t* stg, uint32_t& sbuf, uint32_t q,
-                                              int half, uint32_t lane, float2 a_st,
-                                              float2 r_st, const uint8_t* res_smem) {
+__device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_base, int ncols,
+                                              int grp, const GemmArgs& args,
+                                              const CUtensorMap* map_c, uint8_t* stg,
+                                              uint32_t& sbuf, uint32_t q, int half,
+                                              uint32_t lane, float2 a_st, float2 r_st,
+                                              const uint8_t* res_smem) {
   constexpr bool kResTma = (EPI & kEpiResTma) != 0;  // residual tiles staged in smem by TMA
   constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
   constexpr bool kBf16 = (EPI & kEpiBf16) != 0;  // 16-bit tensors are bf16 (else fp16)
   constexpr int kCW = kOutF32 ? 32 : 64;         // output columns per 128-byte staging row
   static_assert(BN % kCW == 0, "BN must be a multiple of the store chunk");
-  const float* bias = args.bias + grp * args.bias_slot_stride + nt * BN;
+  static_assert((EPI & kEpiStats) == 0 || !kOutF32, "row statistics need 16-bit outputs");
+  const float* bias = args.bias + grp * args.bias_slot_stride + col_base;
   const int row0 = mt * kBlockM + static_cast<int>(q) * 32;
   const int row = row0 + static_cast<int>(lane);
   const bool row_ok = row < args.M;
   const uint32_t t_row = t_acc + ((q * 32) << 16);
-  float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
-  for (int c = half * kCW; c < BN; c += 2 * kCW) {
+  for (int c = half * kCW; c < ncols; c += 2 * kCW) {
     float v[kCW];
 #pragma unroll
     for (int j = 0; j < kCW / 32; ++j) {
@@ -203,7 +204,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
       for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
     }
     if constexpr ((EPI & kEpiFoldLN) != 0) {
-      const float* cs = args.colsum + nt * BN + c;
+      const float* cs = args.colsum + col_base + c;
 #pragma unroll
       for (int i = 0; i < kCW; i += 4) {
         const float4 c4 = __ldg(reinterpret_cast<const float4*>(cs + i));
@@ -219,7 +220,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
       v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
     }
     if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
-      const int col = nt * BN + c;
+      const int col = col_base + c;
       if constexpr (kResTma) {
         const int row_local = static_cast<int>(q) * 32 + static_cast<int>(lane);
         float r[kCW];
@@ -253,11 +254,16 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
 #pragma unroll
       for (int i = 0; i < kCW; ++i) v[i] = fmaxf(v[i], 0.0f);
     }
-    if constexpr ((EPI & kEpiStats) != 0) {
+    if constexpr ((EPI & kEpiStats) != 0) {  // partial of this 64-column group
+      float s1 = 0.f, s2 = 0.f;
 #pragma unroll
       for (int i = 0; i < kCW; ++i) {
         s1 += v[i];
         s2 += v[i] * v[i];
+      }
+      if (row_ok) {
+        args.stats_out[static_cast<long long>(row) * args.stats_ld + (col_base + c) / 64] =
+            make_float2(s1, s2);
       }
     }
     uint32_t packed[32];  // one 128-byte row per thread
@@ -283,14 +289,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int nt, in
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0 && mt < args.num_m_tiles) {
-      tma_store_2d(map_c, buf, nt * BN + c, row0);
+      tma_store_2d(map_c, buf, col_base + c, row0);
       tma_store_commit();
-    }
-  }
-  if constexpr ((EPI & kEpiStats) != 0) {
-    if (row_ok) {
-      args.stats_out[static_cast<long long>(row) * args.stats_ld + nt * 2 + half] =
-          make_float2(s1, s2);
     }
   }
 }
@@ -649,8 +649,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                   kRT ? sRes : nullptr, kRT ? res_empty : nullptr);
       } else {
         if constexpr (kRT) mbar_wait(res_full, iter & 1);
-        epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, stg, sbuf, q,
-                               half, lane, a_st, r_st, sRes);
+        epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt * BN, BN, grp, args, &map_c, stg,
+                               sbuf, q, half, lane, a_st, r_st, sRes);
         if constexpr (kRT) {  // residual tiles consumed: the producer may stage the next tile's
           __syncwarp();
           if (lane == 0) mbar_arrive(res_empty);
@@ -689,6 +689,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // to both CTAs' empty / tmem-full barriers; both CTAs' epilogues drain their
 // own 128 TMEM lanes and arrive on the leader's tmem-empty barrier.
 // ===========================================================================
+// Pair-kernel work unit v: a 256 x BN tile, or (in the wave tail) one of tail_split
+// sub-tiles of width BN / tail_split.
+struct PairUnit {
+  int mp, col0, width;
+  bool tail;
+};
+
+template <int BN>
+__device__ __forceinline__ PairUnit pair_unit(const GemmArgs& a, int v) {
+  PairUnit p;
+  int u = v, sub = 0;
+  p.tail = a.tail_split > 1 && v >= a.n_main;
+  if (p.tail) {
+    const int t = v - a.n_main;
+    u = a.n_main + t / a.tail_split;
+    sub = t - (t / a.tail_split) * a.tail_split;
+  }
+  p.mp = u / a.num_n_tiles;
+  const int nt = u - p.mp * a.num_n_tiles;
+  p.width = p.tail ? BN / a.tail_split : BN;
+  p.col0 = nt * BN + sub * p.width;
+  return p;
+}
+
+__device__ __forceinline__ int pair_units_total(const GemmArgs& a, int num_units) {
+  return a.tail_split > 1 ? a.n_main + (num_units - a.n_main) * a.tail_split : num_units;
+}
+
 template <int BN>
 struct Gemm2Smem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;          // this CTA's 128 rows of A
@@ -731,6 +759,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const int n_pairs = (args.num_m_tiles + 1) / 2;
   const int num_units = n_pairs * args.num_n_tiles;
+  const int total = pair_units_total(args, num_units);
   const int cluster = blockIdx.x >> 1;
   const int n_clusters = gridDim.x >> 1;
   const int num_kb = args.K / kBlockK;
@@ -761,18 +790,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_a = policy_evict_first();
       const uint64_t pol_b = policy_evict_last();
       uint32_t stage = 0, phase = 0;
-      for (int u = cluster; u < num_units; u += n_clusters) {
-        const int mp = u / args.num_n_tiles;
-        const int nt = u - mp * args.num_n_tiles;
-        const int mt = 2 * mp + static_cast<int>(rank);
+      for (int v = cluster; v < total; v += n_clusters) {
+        const PairUnit pu = pair_unit<BN>(args, v);
+        const int mt = 2 * pu.mp + static_cast<int>(rank);
+        // wave-tail sub-tiles load B through the narrower-box maps r0 / r1
+        const CUtensorMap* mb = !pu.tail ? &map_b : args.tail_r1 ? &maps.r1 : &maps.r0;
+        const uint32_t bytes = 2 * (L::kABytes + (pu.width / 2) * kBlockK * 2);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
           const uint32_t leader_full = mapa_shared(smem_u32(&full[stage]), 0);
           tma_load_2d_2sm(sA + stage * L::kABytes, &map_a, leader_full, kb * kBlockK,
                           mt * kBlockM, pol_a);
-          tma_load_3d_2sm(sB + stage * L::kBBytes, &map_b, leader_full, kb * kBlockK,
-                          nt * BN + static_cast<int>(rank) * (BN / 2), 0, pol_b);
+          tma_load_3d_2sm(sB + stage * L::kBBytes, mb, leader_full, kb * kBlockK,
+                          pu.col0 + static_cast<int>(rank) * (pu.width / 2), 0, pol_b);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -781,7 +812,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ MMA issuer (leader only)
     if (rank == 0 && lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int u = cluster; u < num_units; u += n_clusters) {
+      for (int v = cluster; v < total; v += n_clusters) {
+        const uint32_t idesc = args.tail_split > 1 && v >= args.n_main ? args.idesc_tail : args.idesc;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -792,7 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           const uint64_t b_desc = sdesc_k_sw128(smem_u32(sB + stage * L::kBBytes));
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k) {
-            umma_f16_2cta(d_tmem, a_desc + 2 * k, b_desc + 2 * k, args.idesc, (kb | k) != 0);
+            umma_f16_2cta(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
           }
           umma_commit_2cta_mc(&empty[stage], 0x3);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -809,16 +841,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
     uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0;
-    for (int u = cluster; u < num_units; u += n_clusters) {
-      const int mp = u / args.num_n_tiles;
-      const int nt = u - mp * args.num_n_tiles;
-      const int mt = 2 * mp + static_cast<int>(rank);
+    for (int v = cluster; v < total; v += n_clusters) {
+      const PairUnit pu = pair_unit<BN>(args, v);
+      const int mt = 2 * pu.mp + static_cast<int>(rank);
       float2 a_st, r_st;
       epi_row_stats<EPI>(args, mt, q, lane, a_st, r_st);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt, 0, args, &map_c, stg, sbuf, q, half,
-                             lane, a_st, r_st, nullptr);
+      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, pu.col0, pu.width, 0, args, &map_c, stg,
+                             sbuf, q, half, lane, a_st, r_st, nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));

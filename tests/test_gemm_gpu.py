@@ -173,3 +173,25 @@ def test_gemm_throughput_qkv_shape():
     ref = a[:256].astype(np.float64) @ b[0].astype(np.float64).T
     assert np.abs(out[:256] - ref).max() / np.abs(ref).max() < 2e-3
     assert tflops > 100
+
+
+@pytest.mark.parametrize("M,N,K,bn,epi", [(32768, 768, 3072, 256, 2), (32768, 768, 768, 256, 0),
+                                           (5120, 768, 768, 192, 8), (20480, 256, 256, 128, 1)])
+def test_gemm_cta_pair_wave_tail_split_bit_identical(M, N, K, bn, epi):
+    """The pair kernel's last partial wave runs as narrower N sub-tiles (MMA N = BN/2..BN/4);
+    every output element keeps its K order, so results are bit-identical to whole tiles."""
+    rng = np.random.default_rng(M + N + K)
+    a = rng.standard_normal((M, K)).astype(np.float16)
+    b = rng.uniform(-0.05, 0.05, (1, N, K)).astype(np.float16)
+    bias = rng.uniform(-0.1, 0.1, (1, N)).astype(np.float32)
+    r0 = rng.standard_normal((M, N)).astype(np.float16) if epi & 2 else None
+    split, _ = _probe(a, b, bias, res0=r0, epi=epi | 256, bn=bn)
+    whole, _ = _probe(a, b, bias, res0=r0, epi=epi | 256 | 8192, bn=bn)
+    assert np.array_equal(split, whole)
+    for rows in (slice(0, 256), slice(M - 256, M)):  # first wave and the split tail
+        ref = a[rows].astype(np.float64) @ b[0].astype(np.float64).T + bias[0]
+        if epi & 2:
+            ref += r0[rows]
+        if epi & 1:
+            ref = np.maximum(ref, 0)
+        assert np.abs(split[rows] - ref).max() / np.abs(ref).max() < 2e-3
