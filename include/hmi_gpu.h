@@ -246,6 +246,50 @@ int hmi_pool_op(hmi_pool* pool, int op, uint32_t n, const uint32_t* tasks, uint3
                 uint32_t evicted_cap, int32_t* n_trace);
 int hmi_pool_stats(hmi_pool* pool, uint64_t* out);
 
+/* ---- GPU PLOT builder --------------------------
+ * The reference's offline table construction: build_root / derive_branch
+ * (proj/src/plot/table.cpp:29-104) select keys exactly (std::map order, the PLT1
+ * entry order; frequencies as the reference counts them) and each key's
+ * representation is lower_stack_forward (proj/src/transformer/model.cpp:96-118),
+ * computed on the GPU with the serving path's tcgen05 GEMM. A table can be handed
+ * to hmi_gpu_upload_table as is (key_len, keys, reps).
+ *   token_emb [vocab x d], pos_emb [max_fragment x d], lower_f32 = lower layers in
+ *   the HMI1 per-layer order (as higher_f32 of hmi_gpu_create); max_rows bounds the
+ *   rows per GPU pass (0: 16384). Errors: BUILD (empty corpus, no lower stack, domain
+ *   model shape != root), CONFIG (alpha outside [0, 100]), DIMENSION (fragment length),
+ *   VOCABULARY (token id).                                                    */
+typedef struct hmi_plot_builder hmi_plot_builder;
+typedef struct hmi_plot_table hmi_plot_table;
+int hmi_plot_builder_create(int device, const hmi_model_config* cfg, const float* token_emb,
+                            const float* pos_emb, const float* lower_f32, uint32_t precision,
+                            uint32_t max_rows, hmi_plot_builder** out);
+int hmi_plot_builder_destroy(hmi_plot_builder* b);
+/* lower_stack_forward of n fragments (fragment i: key_len[i] tokens at keys[i * max_fragment]);
+ * reps rows (sum key_len x d, f32) in fragment order */
+int hmi_plot_forward(hmi_plot_builder* b, uint32_t n, const uint32_t* key_len,
+                     const uint32_t* keys, float* reps);
+/* corpus = n_seq sequences of seq_lens[s] tokens, concatenated in `tokens` */
+int hmi_plot_build_root(hmi_plot_builder* b, uint32_t n_seq, const uint32_t* seq_lens,
+                        const uint32_t* tokens, hmi_plot_table** out);
+int hmi_plot_derive_branch(hmi_plot_builder* domain_model, const hmi_plot_table* root,
+                           uint32_t n_seq, const uint32_t* seq_lens, const uint32_t* tokens,
+                           double alpha_percent, hmi_plot_table** out);
+/* key selection only (no representations; host-only, no GPU needed) */
+int hmi_plot_select_root(uint32_t ngram, uint32_t vocab, uint32_t n_seq, const uint32_t* seq_lens,
+                         const uint32_t* tokens, hmi_plot_table** out);
+int hmi_plot_select_branch(uint32_t ngram, uint32_t n_seq, const uint32_t* seq_lens,
+                           const uint32_t* tokens, double alpha_percent, hmi_plot_table** out);
+/* a table from arrays (e.g. a PLT1 body, plot_io.cpp:26-31); freq and reps nullable */
+int hmi_plot_table_create(uint32_t ngram, uint32_t d, uint32_t n, const uint32_t* key_len,
+                          const uint32_t* keys, const uint64_t* freq, const float* reps,
+                          hmi_plot_table** out);
+int hmi_plot_table_info(const hmi_plot_table* t, uint32_t* n_entries, uint64_t* n_rows,
+                        uint32_t* has_reps);
+/* key_len [n], keys [n x max_fragment] (zero padded), freq [n], reps [n_rows x d] (nullable) */
+int hmi_plot_table_read(const hmi_plot_table* t, uint32_t* key_len, uint32_t* keys,
+                        uint64_t* freq, float* reps);
+int hmi_plot_table_free(hmi_plot_table* t);
+
 /* ---- standalone kernel probe (K1/K2 GEMM) ------------------------------ */
 /* C[M x N] = epi(A[M x K] . B[g]^T + bias[g]) for a device-side tcgen05 GEMM,
  * host buffers in/out, used by the parity tests of the GEMM kernel alone.

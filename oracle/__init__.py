@@ -111,6 +111,8 @@ def orc() -> ctypes.CDLL:
         L.orc_higher_forward.argtypes = [ctypes.c_void_p, f32p, f64p, ctypes.c_size_t,
                                          ctypes.c_size_t, f32p, ctypes.c_uint32, f32p, f32p,
                                          ctypes.c_uint32, ctypes.c_int, f64p, i32p, i32p]
+        L.orc_lower_forward.argtypes = [ctypes.c_void_p, f32p, f32p, f32p, u32p, ctypes.c_size_t,
+                                         f64p]
         L.orc_infer_one.argtypes = [ctypes.c_void_p, f32p, ctypes.c_void_p, ctypes.c_uint32,
                                     u32p, ctypes.c_uint32, ctypes.c_uint32, f32p,
                                     ctypes.c_uint32, f32p, f32p, ctypes.c_uint32, ctypes.c_int,
@@ -274,6 +276,65 @@ def higher_forward(cfg: Config, higher: np.ndarray, h: np.ndarray, valid_len: in
                                   ptr(scores, f64p), ctypes.byref(label), ptr(tags, i32p))
     assert rc == 0
     return scores, label.value, tags[:valid_len], h
+
+
+def lower_forward(cfg: Config, model: dict, tokens) -> np.ndarray:
+    """lower_stack_forward (model.cpp:96-118) of one fragment: [len x d] f64 PLOT rep rows.
+    `model` is generate_model(cfg, lower=True)."""
+    tokens = np.ascontiguousarray(tokens, np.uint32)
+    out = np.empty((len(tokens), cfg.hidden_size), np.float64)
+    rc = orc().orc_lower_forward(ctypes.byref(cfg.c()), ptr(model["token_embedding"], f32p),
+                                 ptr(model["position_embedding"], f32p), ptr(model["lower"], f32p),
+                                 ptr(tokens, u32p), len(tokens), ptr(out, f64p))
+    assert rc == 0, rc
+    return out
+
+
+def _kgram_counts(corpus, k: int) -> dict:
+    """count_kgrams (table.cpp:16-27): occurrences of every k-gram over the corpus."""
+    counts: dict = {}
+    for seq in corpus:
+        seq = [int(x) for x in seq]
+        for i in range(len(seq) - k + 1):
+            key = tuple(seq[i:i + k])
+            counts[key] = counts.get(key, 0) + 1
+    return counts
+
+
+def plot_select_root(corpus, ngram: int, vocab: int) -> list:
+    """build_root's entries (table.cpp:29-58) as (key, freq) in std::map key order: every
+    k-gram (k = 1..ngram) with its count, then every vocabulary uni-gram absent from the
+    corpus with frequency 1. Python tuple order = std::vector<uint32_t> lexicographic order."""
+    if len(corpus) == 0:
+        raise ValueError("cannot build a table from an empty corpus")
+    entries: dict = {}
+    for k in range(1, ngram + 1):
+        for key, n in _kgram_counts(corpus, k).items():
+            entries.setdefault(key, n)
+    for t in range(vocab):
+        entries.setdefault((t,), 1)
+    return sorted(entries.items())
+
+
+def plot_select_branch(corpus, ngram: int, alpha_percent: float) -> list:
+    """derive_branch's entries (table.cpp:60-104): the corpus' ngram-grams by count
+    descending (ties in key order, stable sort) until cumulative * 10000 >= round(alpha *
+    100) * total; returned in key order."""
+    if not 0.0 <= alpha_percent <= 100.0:
+        raise ValueError("alpha_percent must be in [0, 100]")
+    alpha_centi = int(np.floor(alpha_percent * 100.0 + 0.5))  # std::llround, alpha >= 0
+    counts = _kgram_counts(corpus, ngram)
+    total = sum(counts.values())
+    if total == 0 or alpha_centi == 0:
+        return []
+    order = sorted(sorted(counts.items()), key=lambda kv: -kv[1])
+    out, cum = [], 0
+    for key, n in order:
+        cum += n
+        out.append((key, n))
+        if cum * 10000 >= alpha_centi * total:
+            break
+    return sorted(out)
 
 
 def infer_one(cfg: Config, higher, tree: OracleTree, version: int, tokens, adapters, r: int,

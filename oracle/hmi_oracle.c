@@ -31,6 +31,7 @@
 
 #define ORC_OK 0
 #define ORC_DIMENSION 1
+#define ORC_VOCABULARY 2
 #define ORC_ROUTING 5
 #define ORC_CONFIG 6
 #define ORC_BUILD 7
@@ -356,6 +357,29 @@ int orc_higher_forward(const orc_config* c, const float* higher, double* h, size
       tags[i] = argmax(tmp, labels);
     }
     free(tmp);
+  }
+  return ORC_OK;
+}
+
+/*
+ * lower_stack_forward, model.cpp:96-118: h[i] = token_emb[t_i] + position_emb[i] (fragment-local
+ * positions), then every lower layer (layer_forward without an adapter, all keys valid).
+ *   tok_emb [vocab x d], pos_emb [max_fragment x d], lower = lower_layers x layer_floats
+ *   out [len x d] doubles (the PLOT rep of the fragment)
+ */
+int orc_lower_forward(const orc_config* c, const float* tok_emb, const float* pos_emb,
+                      const float* lower, const uint32_t* tokens, size_t len, double* out) {
+  if (len == 0 || len > c->max_fragment) return ORC_DIMENSION;
+  const size_t d = c->hidden_size;
+  for (size_t i = 0; i < len; ++i) {
+    if (tokens[i] >= c->vocab_size) return ORC_VOCABULARY;
+    for (size_t j = 0; j < d; ++j) {
+      out[i * d + j] = (double)tok_emb[(size_t)tokens[i] * d + j] + (double)pos_emb[i * d + j];
+    }
+  }
+  const size_t lf = orc_layer_floats(c);
+  for (uint32_t l = 0; l < c->lower_layers; ++l) {
+    layer_forward(out, lower + l * lf, NULL, 0, c, len, len);
   }
   return ORC_OK;
 }

@@ -118,6 +118,18 @@ def _sig(L):
                                       P(LoadRecord), u32, u32p, u32, u32p]
     L.hmi_gpu_infer_batch_device.argtypes = [vp, u32, u32p, vp, u32, vp, u32, vp, vp]
     L.hmi_gpu_generate.argtypes = [vp, u32, u32p, u32p, u32, u32p, u32, i32p, f32p]
+    L.hmi_plot_builder_create.argtypes = [ctypes.c_int, P(ModelConfig), f32p, f32p, f32p, u32, u32,
+                                          P(vp)]
+    L.hmi_plot_builder_destroy.argtypes = [vp]
+    L.hmi_plot_forward.argtypes = [vp, u32, u32p, u32p, f32p]
+    L.hmi_plot_build_root.argtypes = [vp, u32, u32p, u32p, P(vp)]
+    L.hmi_plot_derive_branch.argtypes = [vp, vp, u32, u32p, u32p, ctypes.c_double, P(vp)]
+    L.hmi_plot_select_root.argtypes = [u32, u32, u32, u32p, u32p, P(vp)]
+    L.hmi_plot_select_branch.argtypes = [u32, u32, u32p, u32p, ctypes.c_double, P(vp)]
+    L.hmi_plot_table_create.argtypes = [u32, u32, u32, u32p, u32p, u64p, f32p, P(vp)]
+    L.hmi_plot_table_info.argtypes = [vp, u32p, u64p, u32p]
+    L.hmi_plot_table_read.argtypes = [vp, u32p, u32p, u64p, f32p]
+    L.hmi_plot_table_free.argtypes = [vp]
     L.hmi_gpu_submit_batch.argtypes = [vp, u32, u32p, u32p, u32, u32p, u64p]
     L.hmi_gpu_wait_batch.argtypes = [vp, u64, f32p, i32p]
     L.hmi_gpu_synchronize.argtypes = [vp]
