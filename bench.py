@@ -514,6 +514,84 @@ def bench_generate(args, wl):
     eng.close()
 
 
+def bench_plot(args):
+    """GPU PLOT builder: lower_stack_forward of the C2 root table's
+    keys (the vocabulary uni-gram backstop + every 2/3-gram of the root corpus, build_root's key
+    set, table.cpp:29-58) through hmi_plot_forward, host keys in / host f32 reps out. A step =
+    the whole root table. Side measurement; the headline is C2 serving."""
+    import torch
+
+    world_size, rank, local = dist_setup()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    from paper_2504_17449_b200 import engine as E
+    from paper_2504_17449_b200 import plot
+    from paper_2504_17449_b200.workload import CONFIGS, World
+
+    wl = CONFIGS["c2"]
+    world = World(wl)
+    root = world.tables[0]
+    key_len, keys = root["key_len"], root["keys"]
+    rows = int(key_len.sum())
+    mc = E.model_config(wl.hidden_size, wl.heads, wl.lower_layers, wl.higher_layers, wl.ffn_size,
+                        wl.vocab_size, wl.mode, wl.max_fragment, wl.model_seed)
+    b = plot.GpuPlotBuilder(mc, max_rows=32768)
+    for _ in range(args.warmup):
+        b.forward(key_len[:4096], keys[:4096])
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms0, _ = b.stats()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        reps = b.forward(key_len, keys)
+    secs = time.perf_counter() - t0
+    ms1, _ = b.stats()
+    clk = clocks.stop()
+    d, f = wl.hidden_size, wl.ffn_size
+    flops_row = 2 * (4 * d * d + 2 * d * f) * wl.lower_layers
+    value = args.steps * rows / ((ms1 - ms0) / 1e3)   # device time of the GPU passes
+    e2e = args.steps * rows / secs                    # host keys in -> host f32 reps out
+    _, peak_burst, peak_sust, peak_src = peaks()
+    achieved = value * flops_row / 1e12
+    line = {
+        "metric": "PLOT build: lower-stack rows/s (C2 root table: 30,522 uni-grams + corpus 2/3-grams)",
+        "value": value, "unit": "rows/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp16 operands, fp32 accumulate", "data": "synthetic corpus",
+        "config": {"workload": f"hBERT-base lower stack ({wl.lower_layers} layers, d={d}), "
+                               f"{len(key_len)} keys / {rows} rows per step",
+                   "l2": "inputs (rows x d activations per layer) exceed L2"},
+        "e2e": {"value": e2e, "unit": "rows/s", "h2d_bytes_per_step": int(keys.nbytes + key_len.nbytes),
+                "d2h_bytes_per_step": int(reps.nbytes)},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sust, "unit": "TFLOP/s",
+                     "frac": achieved / peak_sust, "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained; all lower-stack kernels of the step",
+                     "flops_per_row": flops_row},
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        import oracle
+        from concurrent.futures import ThreadPoolExecutor
+
+        cfg = oracle.Config(wl.hidden_size, wl.heads, wl.lower_layers, wl.higher_layers,
+                            wl.ffn_size, wl.vocab_size, wl.mode, wl.max_fragment, wl.model_seed)
+        m = oracle.generate_model(cfg, lower=True)
+        threads = os.cpu_count() or 1
+        sample = list(range(0, len(key_len), max(1, len(key_len) // (4 * threads))))[:4 * threads]
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda i: oracle.lower_forward(cfg, m, keys[i, :key_len[i]]), sample))
+        cs = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": int(key_len[sample].sum()) / cs, "unit": "rows/s",
+                                "cores": threads, "kind": "port",
+                                "sample": f"{len(sample)} root-table fragments through the C oracle's "
+                                          f"lower_stack_forward (bit-exact to the reference's scalar "
+                                          f"kernels), {threads} threads"}
+    print(json.dumps(line), flush=True)
+    b.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -531,6 +609,9 @@ def main():
     args.warmup = max(args.warmup, 3)
     from paper_2504_17449_b200.workload import CONFIGS
 
+    if args.config == "plot":
+        bench_plot(args)
+        return
     wl = CONFIGS[args.config]
     if args.impl == "reference":
         bench_reference(args, wl)

@@ -268,6 +268,9 @@ int hmi_plot_builder_destroy(hmi_plot_builder* b);
  * reps rows (sum key_len x d, f32) in fragment order */
 int hmi_plot_forward(hmi_plot_builder* b, uint32_t n, const uint32_t* key_len,
                      const uint32_t* keys, float* reps);
+/* device time (CUDA events around each GPU pass, H2D of keys to the last LayerNorm) and rows
+ * computed since the builder was created */
+int hmi_plot_builder_stats(hmi_plot_builder* b, double* device_ms, uint64_t* rows);
 /* corpus = n_seq sequences of seq_lens[s] tokens, concatenated in `tokens` */
 int hmi_plot_build_root(hmi_plot_builder* b, uint32_t n_seq, const uint32_t* seq_lens,
                         const uint32_t* tokens, hmi_plot_table** out);

@@ -121,6 +121,7 @@ def _sig(L):
     L.hmi_plot_builder_create.argtypes = [ctypes.c_int, P(ModelConfig), f32p, f32p, f32p, u32, u32,
                                           P(vp)]
     L.hmi_plot_builder_destroy.argtypes = [vp]
+    L.hmi_plot_builder_stats.argtypes = [vp, f64p, u64p]
     L.hmi_plot_forward.argtypes = [vp, u32, u32p, u32p, f32p]
     L.hmi_plot_build_root.argtypes = [vp, u32, u32p, u32p, P(vp)]
     L.hmi_plot_derive_branch.argtypes = [vp, vp, u32, u32p, u32p, ctypes.c_double, P(vp)]

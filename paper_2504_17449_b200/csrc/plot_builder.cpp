@@ -115,7 +115,12 @@ struct PlotBuilder {
   uint32_t* keys_d = nullptr;
   uint16_t *h16 = nullptr, *qkv16 = nullptr, *ctx16 = nullptr, *x16 = nullptr, *ffn16 = nullptr;
   float *y32 = nullptr, *out32 = nullptr;
-  std::vector<float> host_rows;
+  // pinned staging, double-buffered: fragment keys in, f32 rows out
+  uint32_t* keys_pin[2] = {nullptr, nullptr};
+  float* out_pin[2] = {nullptr, nullptr};
+  cudaEvent_t ev0[2] = {}, ev1[2] = {}, done[2] = {};
+  double device_ms = 0.0;
+  uint64_t rows_done = 0;
   cudaStream_t stream = nullptr;
   std::mutex mu;
 
@@ -128,6 +133,12 @@ struct PlotBuilder {
 
   ~PlotBuilder() {
     for (void* p : allocs) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+      if (keys_pin[i]) cudaFreeHost(keys_pin[i]);
+      if (out_pin[i]) cudaFreeHost(out_pin[i]);
+      for (cudaEvent_t e : {ev0[i], ev1[i], done[i]})
+        if (e) cudaEventDestroy(e);
+    }
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -204,13 +215,15 @@ struct PlotBuilder {
     }
   }
 
-  // lower_stack_forward of `cnt` fragments of length k (keys [cnt][ngram] on the host);
-  // their rows (f * k + i) land in host_rows
-  void forward_group(uint32_t k, uint32_t cnt, const uint32_t* keys_host) {
+  // One GPU pass: lower_stack_forward of `cnt` fragments of length k (keys [cnt][ngram] in the
+  // pinned staging buffer `buf`); the f32 rows (f * k + i) are copied back into pinned out[buf]
+  // and done[buf] recorded. Device time between ev0/ev1 accumulates into device_ms.
+  void enqueue_pass(int buf, uint32_t k, uint32_t cnt) {
     const int ngram = static_cast<int>(cfg.max_fragment);
     const int rows = static_cast<int>(cnt * k);
     const int rows_p = (rows + 127) / 128 * 128;
-    HMI_CUDA(cudaMemcpyAsync(keys_d, keys_host, static_cast<size_t>(cnt) * ngram * 4,
+    HMI_CUDA(cudaEventRecord(ev0[buf], stream));
+    HMI_CUDA(cudaMemcpyAsync(keys_d, keys_pin[buf], static_cast<size_t>(cnt) * ngram * 4,
                              cudaMemcpyHostToDevice, stream));
     launch_plot_embed(tok_emb, pos_emb, keys_d, ngram, static_cast<int>(k), static_cast<int>(cnt),
                       rows_p, d, h16, precision, stream);
@@ -228,13 +241,16 @@ struct PlotBuilder {
       launch_layernorm(y32, L.ln2g, L.ln2b, h16, last ? out32 : nullptr, rows_p, d, precision,
                        stream);
     }
-    host_rows.resize(static_cast<size_t>(rows) * d);
-    HMI_CUDA(cudaMemcpyAsync(host_rows.data(), out32, host_rows.size() * 4, cudaMemcpyDeviceToHost,
-                             stream));
-    HMI_CUDA(cudaStreamSynchronize(stream));
+    HMI_CUDA(cudaEventRecord(ev1[buf], stream));
+    HMI_CUDA(cudaMemcpyAsync(out_pin[buf], out32, static_cast<size_t>(rows) * d * 4,
+                             cudaMemcpyDeviceToHost, stream));
+    HMI_CUDA(cudaEventRecord(done[buf], stream));
+    rows_done += static_cast<uint64_t>(rows);
   }
 
-  // reps of n fragments (key_len[i] tokens at keys[i * ngram]) in input order
+  // reps of n fragments (key_len[i] tokens at keys[i * ngram]) in input order. Passes alternate
+  // between two pinned staging buffers: the host scatters pass p's rows into `reps` while the
+  // GPU runs pass p + 1.
   void forward(uint32_t n, const uint32_t* key_len, const uint32_t* keys, float* reps) {
     const uint32_t ngram = cfg.max_fragment;
     std::vector<uint64_t> off(n + 1, 0);
@@ -248,25 +264,43 @@ struct PlotBuilder {
       }
       off[i + 1] = off[i] + key_len[i];
     }
-    std::vector<uint32_t> idx, packed;
+    struct Pass {
+      uint32_t k, cnt;
+      std::vector<uint32_t> frags;
+    };
+    std::vector<Pass> passes;
     for (uint32_t k = 1; k <= ngram; ++k) {
-      idx.clear();
+      std::vector<uint32_t> idx;
       for (uint32_t i = 0; i < n; ++i)
         if (key_len[i] == k) idx.push_back(i);
       const uint32_t per = static_cast<uint32_t>(max_rows) / k;
       for (size_t c0 = 0; c0 < idx.size(); c0 += per) {
         const uint32_t cnt = static_cast<uint32_t>(std::min<size_t>(per, idx.size() - c0));
-        packed.assign(static_cast<size_t>(cnt) * ngram, 0);
-        for (uint32_t j = 0; j < cnt; ++j)
-          std::memcpy(&packed[static_cast<size_t>(j) * ngram],
-                      keys + static_cast<size_t>(idx[c0 + j]) * ngram, ngram * 4);
-        forward_group(k, cnt, packed.data());
-        for (uint32_t j = 0; j < cnt; ++j) {
-          std::memcpy(reps + off[idx[c0 + j]] * d, &host_rows[static_cast<size_t>(j) * k * d],
-                      static_cast<size_t>(k) * d * 4);
-        }
+        passes.push_back({k, cnt, std::vector<uint32_t>(idx.begin() + c0, idx.begin() + c0 + cnt)});
       }
     }
+    auto drain = [&](size_t p) {
+      const int buf = static_cast<int>(p & 1);
+      HMI_CUDA(cudaEventSynchronize(done[buf]));
+      float ms = 0.f;
+      HMI_CUDA(cudaEventElapsedTime(&ms, ev0[buf], ev1[buf]));
+      device_ms += ms;
+      const Pass& ps = passes[p];
+      for (uint32_t j = 0; j < ps.cnt; ++j) {
+        std::memcpy(reps + off[ps.frags[j]] * d, out_pin[buf] + static_cast<size_t>(j) * ps.k * d,
+                    static_cast<size_t>(ps.k) * d * 4);
+      }
+    };
+    for (size_t p = 0; p < passes.size(); ++p) {
+      const int buf = static_cast<int>(p & 1);
+      if (p >= 2) drain(p - 2);  // frees staging buffer `buf`
+      const Pass& ps = passes[p];
+      for (uint32_t j = 0; j < ps.cnt; ++j)
+        std::memcpy(keys_pin[buf] + static_cast<size_t>(j) * ngram,
+                    keys + static_cast<size_t>(ps.frags[j]) * ngram, ngram * 4);
+      enqueue_pass(buf, ps.k, ps.cnt);
+    }
+    for (size_t p = passes.size() >= 2 ? passes.size() - 2 : 0; p < passes.size(); ++p) drain(p);
   }
 
   hmi_plot_table* materialize(const CountMap& sel) {
@@ -366,6 +400,13 @@ int hmi_plot_builder_create(int device, const hmi_model_config* cfg, const float
     b.y32 = b.alloc<float>(R * d);
     b.out32 = b.alloc<float>(R * d);
     HMI_CUDA(cudaMemset(b.ctx16, 0, R * d * 2));
+    for (int i = 0; i < 2; ++i) {
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b.keys_pin[i]), R * cfg->max_fragment * 4, 0));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b.out_pin[i]), R * d * 4, 0));
+      HMI_CUDA(cudaEventCreate(&b.ev0[i]));
+      HMI_CUDA(cudaEventCreate(&b.ev1[i]));
+      HMI_CUDA(cudaEventCreateWithFlags(&b.done[i], cudaEventDisableTiming));
+    }
     const size_t lf = 4 * (d * d + d) + (d * f + f) + (f * d + d) + 4 * d;
     b.layers.resize(cfg->lower_layers);
     for (uint32_t l = 0; l < cfg->lower_layers; ++l) b.upload_layer(lower_f32 + l * lf, b.layers[l]);
@@ -387,6 +428,16 @@ int hmi_plot_forward(hmi_plot_builder* b, uint32_t n, const uint32_t* key_len,
     std::lock_guard<std::mutex> lock(b->impl.mu);
     HMI_CUDA(cudaSetDevice(b->impl.device));
     b->impl.forward(n, key_len, keys, reps);
+  });
+}
+
+int hmi_plot_builder_stats(hmi_plot_builder* b, double* device_ms, uint64_t* rows) {
+  using namespace hmi_b200;
+  return plot_guarded([&] {
+    HMI_CHECK(b != nullptr, HMI_CONFIG_ERROR, "null builder");
+    std::lock_guard<std::mutex> lock(b->impl.mu);
+    if (device_ms) *device_ms = b->impl.device_ms;
+    if (rows) *rows = b->impl.rows_done;
   });
 }
 

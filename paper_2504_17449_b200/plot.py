@@ -129,6 +129,13 @@ class GpuPlotBuilder:
                                              _p(ks, ctypes.c_uint32), _p(out, ctypes.c_float)))
         return out
 
+    def stats(self) -> tuple[float, int]:
+        """(device ms, rows) accumulated over every GPU pass of this builder."""
+        ms = ctypes.c_double(0)
+        rows = ctypes.c_uint64(0)
+        check(_native.lib().hmi_plot_builder_stats(self.h, ctypes.byref(ms), ctypes.byref(rows)))
+        return ms.value, rows.value
+
     def build_root(self, corpus) -> dict:
         n_seq, lens, toks = _corpus(corpus)
         h = ctypes.c_void_p()
