@@ -170,6 +170,23 @@ int hmi_gpu_infer_batch_device(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t*
  * bound to the same wide lm head. out_tokens / out_logits: [n_req x n_new]
  * (out_logits nullable: the chosen token's f64-rescored logit).
  * Errors: n_new > max_new_tokens or encoder mode -> CONFIG.                  */
+/* StageTrace: per (batch, stage, layer) intervals on three
+ * logical workers on one clock (ms since hmi_gpu_trace(ctx, 1)): worker 0 cpu (the host's
+ * submit: routing mirror, DeviceSlotPool decisions, staging), 1 io (the copy stream's adapter
+ * H2D for one layer, stage 1 prefetch), 2 compute (stage 0 retrieve, stage 2 one layer's
+ * compute, stage 3 head + result D2H). hmi_gpu_trace(ctx, 1) clears and starts recording;
+ * hmi_gpu_stage_trace returns the records (n = total, at most cap written). */
+typedef struct hmi_stage_record {
+  uint64_t batch;
+  uint32_t stage;  /* 0 retrieve, 1 prefetch, 2 compute, 3 head, 4 host submit */
+  int32_t layer;   /* higher-stack layer, -1 none */
+  uint32_t worker; /* 0 cpu, 1 io, 2 compute */
+  uint32_t pad;
+  double start_ms, end_ms;
+} hmi_stage_record;
+int hmi_gpu_trace(hmi_gpu_ctx* ctx, int enable);
+int hmi_gpu_stage_trace(hmi_gpu_ctx* ctx, hmi_stage_record* out, uint32_t cap, uint32_t* n);
+
 /* Asynchronous form of hmi_gpu_infer_batch for pipelined serving: the batch is enqueued
  * (inputs staged in pinned memory, H2D / compute / D2H on the context's streams) and a ticket
  * returned at once; hmi_gpu_wait_batch blocks until that batch finished and copies its

@@ -92,6 +92,12 @@ class LoadRecord(ctypes.Structure):
                 ("evicted_offset", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
 
 
+class StageRecord(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_uint64), ("stage", ctypes.c_uint32), ("layer", ctypes.c_int32),
+                ("worker", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("start_ms", ctypes.c_double),
+                ("end_ms", ctypes.c_double)]
+
+
 def declared_symbols(header: str = HEADER_PATH) -> list[str]:
     """Every ``hmi_*`` function declared in the C header."""
     text = open(header).read()
@@ -131,6 +137,8 @@ def _sig(L):
     L.hmi_plot_table_info.argtypes = [vp, u32p, u64p, u32p]
     L.hmi_plot_table_read.argtypes = [vp, u32p, u32p, u64p, f32p]
     L.hmi_plot_table_free.argtypes = [vp]
+    L.hmi_gpu_trace.argtypes = [vp, ctypes.c_int]
+    L.hmi_gpu_stage_trace.argtypes = [vp, ctypes.c_void_p, u32, u32p]
     L.hmi_gpu_submit_batch.argtypes = [vp, u32, u32p, u32p, u32, u32p, u64p]
     L.hmi_gpu_wait_batch.argtypes = [vp, u64, f32p, i32p]
     L.hmi_gpu_synchronize.argtypes = [vp]

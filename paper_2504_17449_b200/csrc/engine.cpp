@@ -29,6 +29,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -54,6 +55,10 @@ void launch_apply_deltas(int32_t* table, const int32_t* pairs, int n, cudaStream
 namespace {
 
 constexpr int kStaging = 4;
+// StageTrace stages / workers (include/hmi_gpu.h hmi_stage_record)
+constexpr int kStageRetrieve = 0, kStagePrefetch = 1, kStageCompute = 2, kStageHead = 3,
+              kStageHost = 4;
+constexpr int kWorkerCpu = 0, kWorkerIo = 1, kWorkerCompute = 2;
 
 enum ProfClass {
   P_H2D = 0, P_ROUTE, P_RETRIEVE, P_QKV, P_ATTN, P_OPROJ, P_AD_DOWN, P_AD_UP, P_LN1, P_FFN1,
@@ -315,6 +320,38 @@ struct Ctx {
   void build_lm_plan(LmHead& h);
   // profiling
   bool prof = false;
+  // StageTrace: per (batch, stage, layer) intervals on three logical
+  // workers, cpu (host submit), io (copy stream), compute (compute stream), one clock whose
+  // origin is `trace_epoch` (recorded on an idle device when tracing is enabled)
+  struct TraceEv {
+    uint64_t batch;
+    int stage, layer, worker;
+    cudaEvent_t a = nullptr, b = nullptr;
+    double host_a = 0, host_b = 0;
+  };
+  bool trace_on = false;
+  cudaEvent_t trace_epoch = nullptr;
+  std::chrono::steady_clock::time_point trace_host0;
+  std::vector<TraceEv> trace_evs;
+  double host_ms() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - trace_host0)
+        .count();
+  }
+  // brackets the work `fn` enqueues on `stream` with a traced interval
+  template <typename F>
+  void traced(int stage, int layer, int worker, cudaStream_t stream, F&& fn) {
+    if (!trace_on) {
+      fn();
+      return;
+    }
+    TraceEv e{n_batches, stage, layer, worker};
+    HMI_CUDA(cudaEventCreate(&e.a));
+    HMI_CUDA(cudaEventCreate(&e.b));
+    HMI_CUDA(cudaEventRecord(e.a, stream));
+    fn();
+    HMI_CUDA(cudaEventRecord(e.b, stream));
+    trace_evs.push_back(e);
+  }
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
   std::vector<cudaEvent_t> prof_free;
   double prof_ms[HMI_PROF_CLASSES] = {};
@@ -710,6 +747,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
                 std::vector<int32_t>* record_layer, uint32_t n_new) {
   HMI_CHECK(n_req >= 1 && n_req <= opt.max_batch, HMI_DIMENSION_ERROR,
             "batch size must be in [1, max_batch]");
+  const double trace_host_a = trace_on ? host_ms() : 0.0;
   HMI_CHECK(!stg[stg_next].held, HMI_CAPACITY_ERROR,
             "too many outstanding submitted batches: wait on the oldest ticket first");
   const bool gen = n_new > 0;
@@ -849,7 +887,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   // ---- copy stream: adapter H2D into HBM slots, one event per layer
   // One cudaMemcpyBatchAsync per layer: a miss-heavy batch issues hundreds of
   // slot-sized copies, and per-call submission cost (not PCIe) bounded them.
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < L; ++l) traced(kStagePrefetch, l, kWorkerIo, copy, [&] {
     const size_t n = loads[l].size();
     if (n != 0) {
       cp_dst.resize(n);
@@ -882,7 +920,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
       n_copies += n;
     }
     HMI_CUDA(cudaEventRecord(ev_layer[l], copy));
-  }
+  });
 
   // ---- compute stream
   cudaStream_t s = compute;
@@ -932,12 +970,14 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   }
   const int causal = cfg.mode == 1 ? 1 : 0;
   const int prec = static_cast<int>(opt.precision);
-  timed(P_RETRIEVE, s, [&] {
-    launch_retrieve(P, d_tokens.p, d_lens.p, d_req_version.p, static_cast<int>(n_req), S, causal,
-                    h16.p, prec, (debug_flags & 1) ? h64.p : nullptr, d_gather.p, d_levels.p,
-                    d_err.p, s);
+  traced(kStageRetrieve, -1, kWorkerCompute, s, [&] {
+    timed(P_RETRIEVE, s, [&] {
+      launch_retrieve(P, d_tokens.p, d_lens.p, d_req_version.p, static_cast<int>(n_req), S, causal,
+                      h16.p, prec, (debug_flags & 1) ? h64.p : nullptr, d_gather.p, d_levels.p,
+                      d_err.p, s);
+    });
   });
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < L; ++l) traced(kStageCompute, l, kWorkerCompute, s, [&] {
     LayerDev& w = layers[l];
     const bool last = l == L - 1;
     timed(P_QKV, s, [&] { launch_gemm(w.qkv, rows, s); });
@@ -976,7 +1016,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
         launch_layernorm(y32.p, w.ln2g, w.ln2b, h16.p, last ? h32.p : nullptr, rows, d, prec, s);
       });
     }
-  }
+  });
   HeadDev H;
   H.arena = d_head_arena.p;
   H.offset = d_head_off.p;
@@ -1015,6 +1055,17 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   }
   HMI_CUDA(cudaMemcpyAsync(st.err, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   HMI_CUDA(cudaEventRecord(st.done, s));
+  if (trace_on) {  // head + D2H (compute), then the host-side submit interval (cpu)
+    TraceEv e{n_batches, kStageHead, -1, kWorkerCompute};
+    HMI_CUDA(cudaEventCreate(&e.a));
+    e.b = nullptr;
+    HMI_CUDA(cudaEventRecord(e.a, s));  // marks the end; start = the last layer's end
+    trace_evs.push_back(e);
+    TraceEv h{n_batches, kStageHost, -1, kWorkerCpu};
+    h.host_a = trace_host_a;
+    h.host_b = host_ms();
+    trace_evs.push_back(h);
+  }
   st.busy = true;
   inflight.push_back(Inflight{st.done, si, uniq});
   last_n = n_req;
@@ -1752,6 +1803,67 @@ int hmi_gpu_infer_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instan
     c.reap(false);
     if (want) fill_trace(recs, tag, trace, trace_cap, evicted, evicted_cap, n_trace);
     if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
+  });
+}
+
+int hmi_gpu_trace(hmi_gpu_ctx* ctx, int enable) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    HMI_CUDA(cudaDeviceSynchronize());
+    for (auto& e : c.trace_evs) {
+      if (e.a) cudaEventDestroy(e.a);
+      if (e.b) cudaEventDestroy(e.b);
+    }
+    c.trace_evs.clear();
+    if (!c.trace_epoch) HMI_CUDA(cudaEventCreate(&c.trace_epoch));
+    c.trace_on = enable != 0;
+    if (c.trace_on) {  // device idle: the epoch event and the host origin coincide
+      HMI_CUDA(cudaEventRecord(c.trace_epoch, c.compute));
+      HMI_CUDA(cudaEventSynchronize(c.trace_epoch));
+      c.trace_host0 = std::chrono::steady_clock::now();
+    }
+  });
+}
+
+int hmi_gpu_stage_trace(hmi_gpu_ctx* ctx, hmi_stage_record* out, uint32_t cap, uint32_t* n) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    HMI_CHECK(c.trace_epoch != nullptr, HMI_CONFIG_ERROR, "tracing was never enabled");
+    HMI_CUDA(cudaDeviceSynchronize());
+    uint32_t k = 0;
+    double prev_end = 0.0;  // compute-stream end of the previous record (head start)
+    for (const auto& e : c.trace_evs) {
+      hmi_stage_record r{};
+      r.batch = e.batch;
+      r.stage = static_cast<uint32_t>(e.stage);
+      r.layer = e.layer;
+      r.worker = static_cast<uint32_t>(e.worker);
+      if (e.worker == kWorkerCpu) {
+        r.start_ms = e.host_a;
+        r.end_ms = e.host_b;
+      } else {
+        float ms = 0.f;
+        HMI_CUDA(cudaEventElapsedTime(&ms, c.trace_epoch, e.a));
+        r.start_ms = ms;
+        if (e.b) {
+          HMI_CUDA(cudaEventElapsedTime(&ms, c.trace_epoch, e.b));
+          r.end_ms = ms;
+        } else {  // head: from the end of the batch's last layer to this mark
+          r.end_ms = r.start_ms;
+          r.start_ms = prev_end;
+        }
+        if (e.worker == kWorkerCompute) prev_end = r.end_ms;
+      }
+      if (k < cap && out) out[k] = r;
+      ++k;
+    }
+    if (n) *n = k;
   });
 }
 

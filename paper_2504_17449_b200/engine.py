@@ -161,6 +161,24 @@ class GpuEngine:
                               "evicted": [int(x) for x in ev[r.evicted_offset:r.evicted_offset + r.n_evicted]]})
         return BatchResult(scores, labels, tags, trace)
 
+    STAGES = ("retrieve", "prefetch", "compute", "head", "host")
+    WORKERS = ("cpu", "io", "compute")
+
+    def trace(self, enable: bool) -> None:
+        """Start (clearing) or stop StageTrace recording (hmi_gpu_trace)."""
+        check(_native.lib().hmi_gpu_trace(self.h, int(enable)))
+
+    def stage_trace(self) -> list:
+        """StageTrace records: dicts {batch, stage, layer, worker, start_ms, end_ms}."""
+        L = _native.lib()
+        n = ctypes.c_uint32(0)
+        check(L.hmi_gpu_stage_trace(self.h, None, 0, ctypes.byref(n)))
+        recs = (_native.StageRecord * max(n.value, 1))()
+        check(L.hmi_gpu_stage_trace(self.h, recs, n.value, ctypes.byref(n)))
+        return [{"batch": int(r.batch), "stage": self.STAGES[r.stage], "layer": int(r.layer),
+                 "worker": self.WORKERS[r.worker], "start_ms": r.start_ms, "end_ms": r.end_ms}
+                for r in recs[:n.value]]
+
     def submit_batch(self, instance_idx, tokens, lens) -> int:
         """Enqueue a batch (host buffers) and return its ticket at once (hmi_gpu_submit_batch)."""
         inst = np.ascontiguousarray(instance_idx, np.uint32)

@@ -103,6 +103,39 @@ def test_submit_wait_pipelined_matches_sync(c1):
         assert np.array_equal(a.scores, b.scores) and np.array_equal(a.labels, b.labels)
 
 
+@pytest.mark.parametrize("mode", [E.MODE_SYNC, E.MODE_COARSE, E.MODE_FINE])
+def test_stage_trace_invariants(mode):
+    """StageTrace: end >= start; intervals of one worker never
+    overlap; a layer's compute starts after that layer's adapter prefetch ends (fine), or after
+    all of the batch's prefetches (sync / coarse); sync also waits for the previous batch."""
+    layer_bytes = (256 * 16 * 2 + 16 + 256) * 4
+    w = World(oracle.TINY, n_tasks=16, r=16, labels=8, max_batch=8,
+              pool_bytes=6 * 2 * layer_bytes + 100, pipeline_mode=mode)
+    w.eng.trace(True)
+    for k in range(4):
+        inst, toks, lens = w.requests(60 + k, 6, 128)
+        w.eng.infer_batch((inst + 5 * k) % 16, toks, lens)
+    recs = w.eng.stage_trace()
+    w.eng.trace(False)
+    w.eng.close()
+    assert len(recs) == 4 * (2 + 2 * 2 + 1)  # per batch: host, retrieve, 2 x (prefetch, compute), head
+    eps = 1e-3
+    for r in recs:
+        assert r["end_ms"] >= r["start_ms"] - eps, r
+    for wk in ("cpu", "io", "compute"):
+        iv = sorted((r["start_ms"], r["end_ms"]) for r in recs if r["worker"] == wk)
+        for (a0, a1), (b0, b1) in zip(iv, iv[1:]):
+            assert b0 >= a1 - eps, (wk, (a0, a1), (b0, b1))
+    for b in {r["batch"] for r in recs}:
+        pre = {r["layer"]: r for r in recs if r["batch"] == b and r["stage"] == "prefetch"}
+        comp = {r["layer"]: r for r in recs if r["batch"] == b and r["stage"] == "compute"}
+        ret = [r for r in recs if r["batch"] == b and r["stage"] == "retrieve"][0]
+        for l, c in comp.items():
+            assert c["start_ms"] >= pre[l]["end_ms"] - eps
+        if mode != E.MODE_FINE:
+            assert ret["start_ms"] >= max(p["end_ms"] for p in pre.values()) - eps
+
+
 def test_c1_swap_small_pool_bit_identical(c1):
     """A pool holding only 3 tasks forces evictions and reloads every batch; outputs
     are bit-identical to the all-resident run and the trace obeys the LRU law."""
