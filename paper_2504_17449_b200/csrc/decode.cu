@@ -145,19 +145,46 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
     v[k] = -INFINITY;
     ix[k] = 0x7fffffff;
   }
-  for (int j = threadIdx.x; j < A.V; j += blockDim.x) {
-    const float x = lg[j];
-    if (x > v[kTopK - 1]) {
-      int k = kTopK - 1;
-      while (k > 0 && x > v[k - 1]) {
-        v[k] = v[k - 1];
-        ix[k] = ix[k - 1];
-        --k;
+  auto consider = [&](float x, int xi) {
+    if (x > v[kTopK - 1]) {  // insert, keeping the earlier index first among equals
+#pragma unroll
+      for (int k = 0; k < kTopK; ++k) {
+        if (x > v[k]) {
+          const float tv = v[k];
+          const int ti = ix[k];
+          v[k] = x;
+          ix[k] = xi;
+          x = tv;
+          xi = ti;
+        }
       }
-      v[k] = x;
-      ix[k] = j;
+    }
+  };
+  // 16 logits in flight per thread: 4 x float4 per round (rows are 16-byte aligned, ld % 4 == 0)
+  const int V4 = A.V & ~3;
+  int j0 = threadIdx.x * 4;
+  for (; j0 + 3 * 4 * kArgThreads < V4; j0 += 4 * 4 * kArgThreads) {
+    float4 x4[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      x4[t] = *reinterpret_cast<const float4*>(lg + j0 + t * 4 * kArgThreads);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int jj = j0 + t * 4 * kArgThreads;
+      consider(x4[t].x, jj);
+      consider(x4[t].y, jj + 1);
+      consider(x4[t].z, jj + 2);
+      consider(x4[t].w, jj + 3);
     }
   }
+  for (; j0 < V4; j0 += 4 * kArgThreads) {
+    const float4 x4 = *reinterpret_cast<const float4*>(lg + j0);
+    consider(x4.x, j0);
+    consider(x4.y, j0 + 1);
+    consider(x4.z, j0 + 2);
+    consider(x4.w, j0 + 3);
+  }
+  for (int j = V4 + static_cast<int>(threadIdx.x); j < A.V; j += kArgThreads) consider(lg[j], j);
 #pragma unroll
   for (int k = 0; k < kTopK; ++k) {
     cv[threadIdx.x * kTopK + k] = v[k];
@@ -199,19 +226,43 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
     }
   }
   __syncthreads();
-  // f64 rescoring of the candidates: h (f32 row) . W[:, j] + b[j] (project_row, model.cpp:130-136)
+  // f64 rescoring of the candidates: h (f32 row) . W[:, j] + b[j] (project_row, model.cpp:130-136),
+  // all candidates in one pass over the row (independent loads), one block reduction
   const float* h = A.h32 + static_cast<long long>(b) * A.d;
+  int cj[kTopK];
+#pragma unroll
+  for (int k = 0; k < kTopK; ++k) cj[k] = cand[k];
+  double acc[kTopK];
+#pragma unroll
+  for (int k = 0; k < kTopK; ++k) acc[k] = 0.0;
+  for (int i = threadIdx.x; i < A.d; i += blockDim.x) {
+    const double hv = static_cast<double>(h[i]);
+    const float* wr = A.w + static_cast<long long>(i) * A.V;
+#pragma unroll
+    for (int k = 0; k < kTopK; ++k) {
+      if (cj[k] >= 0) acc[k] += hv * static_cast<double>(__ldg(wr + cj[k]));
+    }
+  }
+  __shared__ double red8[kTopK][kArgThreads / 32];
+  const int wid = threadIdx.x >> 5, lid = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < kTopK; ++k) {
+    double t = acc[k];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lid == 0) red8[k][wid] = t;
+  }
+  __syncthreads();
   double best = -INFINITY;
   int besti = 0x7fffffff;
+#pragma unroll
   for (int k = 0; k < kTopK; ++k) {
-    const int j = cand[k];
-    if (j < 0) continue;  // uniform across the block
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < A.d; i += blockDim.x)
-      acc += static_cast<double>(h[i]) * static_cast<double>(__ldg(A.w + static_cast<long long>(i) * A.V + j));
-    acc = block_sum_t(acc, red) + static_cast<double>(A.bias[j]);
-    if (acc > best || (acc == best && j < besti)) {
-      best = acc;
+    const int j = cj[k];
+    if (j < 0) continue;
+    double t = 0.0;
+    for (int w = 0; w < kArgThreads / 32; ++w) t += red8[k][w];
+    t += static_cast<double>(A.bias[j]);
+    if (t > best || (t == best && j < besti)) {
+      best = t;
       besti = j;
     }
   }
@@ -233,6 +284,8 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
 // One CTA per (head, request): q of the new row against keys 0..pos.
 __global__ void __launch_bounds__(128) attn_decode_kernel(AttnDecodeArgs A) {
   extern __shared__ float sc[];  // [pos + 1] scores, then 4 x 64 partial contexts
+  __shared__ float qs[64];
+  __shared__ float red[32];
   const int h = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = A.d;
@@ -240,22 +293,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnDecodeArgs A) {
   const int len0 = A.lens[b];
   const int nk = pos + 1;
   const uint16_t* qrow = A.qkv_new + static_cast<long long>(b) * 3 * d;
-  const float scale = A.scale;
-  float q0, q1;
-  {
-    const uint32_t u = reinterpret_cast<const uint32_t*>(qrow + h * 64)[lane];
-    float f[2];
-    if (A.bf16) {
-      f[0] = __uint_as_float(u << 16);
-      f[1] = __uint_as_float(u & 0xffff0000u);
-    } else {
-      const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&u));
-      f[0] = t.x;
-      f[1] = t.y;
-    }
-    q0 = f[0];
-    q1 = f[1];
-  }
+  if (threadIdx.x < 64) qs[threadIdx.x] = ld16(qrow, h * 64 + threadIdx.x, A.bf16);
   // append this row's k, v (head slice) to the generated-rows cache
   uint16_t* trow = A.tail + (static_cast<long long>(b) * A.tail_cap + (pos - len0)) * 2 * d;
   if (threadIdx.x < 64) {
@@ -267,29 +305,36 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnDecodeArgs A) {
           reinterpret_cast<const uint32_t*>(qrow + 2 * d + h * 64)[threadIdx.x - 32];
     }
   }
+  // key / value rows without branches (selects), so unrolled loads issue back to back:
+  // prefill rows j < len0, generated rows len0 <= j < pos, the new row j == pos
+  const uint16_t* pre = A.qkv_prefill + static_cast<long long>(b) * A.S * 3 * d + d + h * 64;
+  const uint16_t* gen = A.tail + static_cast<long long>(b) * A.tail_cap * 2 * d + h * 64 -
+                        static_cast<long long>(len0) * 2 * d;
+  const uint16_t* cur = qrow + d + h * 64;
   auto key_ptr = [&](int j) -> const uint16_t* {
-    if (j == pos) return qrow + d;                         // the new row itself
-    if (j < len0) return A.qkv_prefill + (static_cast<long long>(b) * A.S + j) * 3 * d + d;
-    return A.tail + (static_cast<long long>(b) * A.tail_cap + (j - len0)) * 2 * d;
+    const uint16_t* p = j < len0 ? pre + static_cast<long long>(j) * 3 * d
+                                 : gen + static_cast<long long>(j) * 2 * d;
+    return j == pos ? cur : p;
   };
-  auto val_ptr = [&](int j) -> const uint16_t* {
-    if (j == pos) return qrow + 2 * d;
-    if (j < len0) return A.qkv_prefill + (static_cast<long long>(b) * A.S + j) * 3 * d + 2 * d;
-    return A.tail + (static_cast<long long>(b) * A.tail_cap + (j - len0)) * 2 * d + d;
-  };
-  auto ld2 = [&](const uint16_t* p) -> float2 {
-    const uint32_t u = reinterpret_cast<const uint32_t*>(p + h * 64)[lane];
-    if (A.bf16) return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
-    return __half22float2(*reinterpret_cast<const __half2*>(&u));
-  };
-  for (int j = warp; j < nk; j += 4) {
-    const float2 k = ld2(key_ptr(j));
-    float s = q0 * k.x + q1 * k.y;
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) sc[j] = s * scale;
+  auto val_ptr = [&](int j) -> const uint16_t* { return key_ptr(j) + d; };
+  __syncthreads();
+  // scores: one key per thread (its 64-dim head slice as 8 x 16-byte loads), no shuffles
+  for (int j = threadIdx.x; j < nk; j += blockDim.x) {
+    const uint4* kp = reinterpret_cast<const uint4*>(key_ptr(j));
+    uint4 u[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) u[c] = kp[c];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float f[8];
+      unpack8(u[c], f, A.bf16);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += f[i] * qs[8 * c + i];
+    }
+    sc[j] = s * A.scale;
   }
   __syncthreads();
-  __shared__ float red[32];
   float m = -INFINITY;
   for (int j = threadIdx.x; j < nk; j += blockDim.x) m = fmaxf(m, sc[j]);
   m = block_max_f(m, red);
@@ -300,10 +345,27 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnDecodeArgs A) {
     sum += e;
   }
   sum = block_sum_t(sum, red);  // contains the barrier that publishes sc[]
+  // context: warp w takes keys j = w (mod 4), lane its two dims; 8 keys in flight per warp
   float a0 = 0.f, a1 = 0.f;
-  for (int j = warp; j < nk; j += 4) {
+  int j = warp;
+  for (; j + 28 < nk; j += 32) {
+    uint32_t u[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) u[t] = reinterpret_cast<const uint32_t*>(val_ptr(j + 4 * t))[lane];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float2 v = A.bf16 ? make_float2(__uint_as_float(u[t] << 16), __uint_as_float(u[t] & 0xffff0000u))
+                              : __half22float2(*reinterpret_cast<const __half2*>(&u[t]));
+      const float p = sc[j + 4 * t];
+      a0 += p * v.x;
+      a1 += p * v.y;
+    }
+  }
+  for (; j < nk; j += 4) {
+    const uint32_t u = reinterpret_cast<const uint32_t*>(val_ptr(j))[lane];
+    const float2 v = A.bf16 ? make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u))
+                            : __half22float2(*reinterpret_cast<const __half2*>(&u));
     const float p = sc[j];
-    const float2 v = ld2(val_ptr(j));
     a0 += p * v.x;
     a1 += p * v.y;
   }
