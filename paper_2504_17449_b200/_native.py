@@ -12,7 +12,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhmi_b200.so")
+LIB_PATH = os.environ.get("HMI_LIB_PATH") or os.path.join(_HERE, "_lib", "libhmi_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "hmi_gpu.h")
 
 _lib = None

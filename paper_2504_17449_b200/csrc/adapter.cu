@@ -234,12 +234,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = mt * 128 + r;
       float2 rst = make_float2(0.f, 1.f);
       if (args.r_stats != nullptr) {  // LN2 of the previous layer, applied to h on the fly
-        const float2* p = args.r_stats + static_cast<long long>(row) * args.r_stats_ld;
+        const float4* p = reinterpret_cast<const float4*>(args.r_stats +
+                                                          static_cast<long long>(row) * args.r_stats_ld);
+        float4 q[8];  // r_stats_ld = 16 float2: every partial in one round trip
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          q[i] = 2 * i < args.r_stats_n ? __ldg(p + i) : make_float4(0.f, 0.f, 0.f, 0.f);
         float s1 = 0.f, s2 = 0.f;
-        for (int i = 0; i < args.r_stats_n; ++i) {
-          const float2 v = __ldg(p + i);
-          s1 += v.x;
-          s2 += v.y;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          s1 += q[i].x;
+          s2 += q[i].y;
+          if (2 * i + 1 < args.r_stats_n) {
+            s1 += q[i].z;
+            s2 += q[i].w;
+          }
         }
         const float mean = s1 * args.inv_n;
         const float var = fmaxf(s2 * args.inv_n - mean * mean, 0.0f);
@@ -376,6 +385,8 @@ AdapterPlan make_adapter_plan(const AdapterSpec& s) {
   HMI_CHECK(s.d % kUpN == 0 && s.d >= kUpN, HMI_CONFIG_ERROR,
             "fused adapter: hidden size must be a multiple of 128");
   HMI_CHECK(s.rows % 128 == 0, HMI_CONFIG_ERROR, "fused adapter: rows must be a multiple of 128");
+  HMI_CHECK(s.r_stats == nullptr || (s.stats_ld == 16 && s.r_stats_n <= 16), HMI_CONFIG_ERROR,
+            "fused adapter: statistics rows of 16 float2");
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   HMI_CHECK(al16(s.arena + s.off_bu) && s.slot_bytes % 16 == 0 &&
                 (s.r_stats == nullptr || (al16(s.r_gamma) && al16(s.r_beta))),

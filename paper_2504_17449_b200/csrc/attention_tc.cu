@@ -54,6 +54,14 @@ __device__ __forceinline__ uint32_t sw(int r, int chunk) {
   return static_cast<uint32_t>(r * 128 + ((chunk ^ (r & 7)) << 4));
 }
 
+// 2^x on the MUFU (ex2.approx.ftz: denormal results flush to zero; softmax weights that small
+// vanish against the row's maximum term, which is exactly 1)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <bool kBf16>
 __device__ __forceinline__ uint32_t pk2(float a, float b) {
   if constexpr (kBf16) {
@@ -221,19 +229,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[32 * j + i] = __uint_as_float(t[i]);
       }
-      float mx = -INFINITY;
+      // scale (+ mask keys j >= lim: skipped, model.cpp:48-51), max and sum with four
+      // independent partial chains; exp2 on the MUFU without the denormal fix-up
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if (lim >= 128) {
 #pragma unroll
-      for (int j = 0; j < 128; ++j) {
-        s[j] = j < lim ? s[j] * scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s[j]);
+        for (int j = 0; j < 128; ++j) {
+          s[j] *= scale_log2;
+          m4[j & 3] = fmaxf(m4[j & 3], s[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 128; ++j) {
+          s[j] = j < lim ? s[j] * scale_log2 : -INFINITY;
+          m4[j & 3] = fmaxf(m4[j & 3], s[j]);
+        }
       }
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       const float mb = mx == -INFINITY ? 0.f : mx;
-      float l = 0.f;
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < 128; ++j) {
-        s[j] = exp2f(s[j] - mb);
-        l += s[j];
+        s[j] = ex2_ftz(s[j] - mb);
+        l4[j & 3] += s[j];
       }
+      const float l = (l4[0] + l4[1]) + (l4[2] + l4[3]);
       // P row r -> two SWIZZLE_128B K-major tiles (keys 0-63, 64-127) over the stage's Q, K
       // (both consumed: s_full committed after the S MMA read them)
       uint8_t* P = base + (k % kStages) * kBufBytes;

@@ -86,11 +86,21 @@ __device__ __forceinline__ void add_res16(float* v, const uint16_t* src) {
 // Row (mean, 1/sqrt(var + eps)) of a pre-norm row from P partial (sum, sumsq) entries
 // (layer_norm, ops.cpp:92-116: biased variance, epsilon 1e-5).
 __device__ __forceinline__ float2 row_stats(const float2* part, int n, float inv_n) {
+  // all partials in one round trip: kStatsStride float2 = 8 x 16-byte loads (rows are 128 B)
+  float4 q[kStatsStride / 2];
+#pragma unroll
+  for (int i = 0; i < kStatsStride / 2; ++i) {
+    q[i] = 2 * i < n ? __ldg(reinterpret_cast<const float4*>(part) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float s1 = 0.f, s2 = 0.f;
-  for (int i = 0; i < n; ++i) {
-    const float2 p = __ldg(part + i);
-    s1 += p.x;
-    s2 += p.y;
+#pragma unroll
+  for (int i = 0; i < kStatsStride / 2; ++i) {
+    s1 += q[i].x;
+    s2 += q[i].y;
+    if (2 * i + 1 < n) {
+      s1 += q[i].z;
+      s2 += q[i].w;
+    }
   }
   const float mean = s1 * inv_n;
   const float var = fmaxf(s2 * inv_n - mean * mean, 0.0f);
