@@ -305,10 +305,35 @@ int hmi_plot_table_create(uint32_t ngram, uint32_t d, uint32_t n, const uint32_t
                           hmi_plot_table** out);
 int hmi_plot_table_info(const hmi_plot_table* t, uint32_t* n_entries, uint64_t* n_rows,
                         uint32_t* has_reps);
+int hmi_plot_table_shape(const hmi_plot_table* t, uint32_t* ngram, uint32_t* d);
 /* key_len [n], keys [n x max_fragment] (zero padded), freq [n], reps [n_rows x d] (nullable) */
 int hmi_plot_table_read(const hmi_plot_table* t, uint32_t* key_len, uint32_t* keys,
                         uint64_t* freq, float* reps);
 int hmi_plot_table_free(hmi_plot_table* t);
+
+/* ---- artefact ingest --------------------------
+ * The reference's containers read straight into the f32 layouts above (no f64 round trip);
+ * validation and FormatError cases as the reference readers (io/binary.cpp:62-123):
+ *   PLT1 plot_io.cpp:17-72 · ADP1 adapter_set.cpp:27-75 · HMI1 model_io.cpp:83-115.
+ * Two-phase reads: pass NULL arrays to get the sizes first.                 */
+int hmi_plot_table_load(const char* path, hmi_plot_table** out, uint32_t* version_id,
+                        uint32_t* parent_id, uint32_t* alpha_centi);
+/* PLT1 writer (plot_io.cpp:17-33): entries in key order, reps f32 */
+int hmi_plot_table_save(const hmi_plot_table* t, const char* path, uint32_t version_id,
+                        uint32_t parent_id, const char* domain_label, uint32_t alpha_centi);
+/* body = layers x (W_down [d x r], b_down [r], W_up [r x d], b_up [d]) f32, nullable */
+int hmi_adapter_set_load(const char* path, char* task_id, uint32_t task_id_cap, uint32_t* layers,
+                         uint32_t* d, uint32_t* r, float* body);
+/* config, then (nullable) token_emb [vocab x d], pos_emb [max_fragment x d], lower / higher
+ * layers in the HMI1 per-layer order */
+int hmi_model_load(const char* path, hmi_model_config* cfg, float* token_emb, float* pos_emb,
+                   float* lower_f32, float* higher_f32);
+/* VersionTree::add_branch from a table handle (e.g. a loaded PLT1, or a GPU-built table) */
+int hmi_gpu_upload_plot_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t parent_id,
+                              const hmi_plot_table* t);
+/* AdapterStore::register_set from an ADP1 file (dimensions checked against the context) */
+int hmi_gpu_register_task_file(hmi_gpu_ctx* ctx, uint32_t task_idx, const char* adp1_path);
+int hmi_gpu_check_adapter_dims(hmi_gpu_ctx* ctx, uint32_t layers, uint32_t d, uint32_t r);
 
 /* ---- standalone kernel probe (K1/K2 GEMM) ------------------------------ */
 /* C[M x N] = epi(A[M x K] . B[g]^T + bias[g]) for a device-side tcgen05 GEMM,

@@ -152,6 +152,12 @@ def ref() -> ctypes.CDLL | None:
         L.ref_tree_add_branch.restype = ctypes.c_int64
         L.ref_tree_add_branch.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p, f32p,
                                           u64p]
+        L.ref_plt1_load.argtypes = [ctypes.c_char_p, u32p, u32p, u32p, f32p, u64p]
+        L.ref_adp1_check.argtypes = [ctypes.c_char_p]
+        L.ref_hmi1_check.argtypes = [ctypes.c_char_p]
+        L.ref_model_save.argtypes = [vp, ctypes.c_char_p]
+        L.ref_adapter_save.argtypes = [vp, ctypes.c_char_p]
+        L.ref_plot_persist.argtypes = [vp, ctypes.c_uint32, ctypes.c_char_p]
         L.ref_tree_build_root.restype = vp
         L.ref_tree_build_root.argtypes = [vp, ctypes.c_uint32, u32p, u32p]
         L.ref_tree_derive_branch.restype = ctypes.c_int64

@@ -309,6 +309,35 @@ int ref_plot_persist(void* pt, uint32_t version, const char* path) {
   });
 }
 
+// plot::load (plot_io.cpp:35-72) of a PLT1 file: hdr = {version, parent, ngram, d, count,
+// alpha_centi}; arrays (nullable) in entry order, reps narrowed back to f32. Returns the
+// reference's error class on failure (FormatError -> 9).
+int ref_plt1_load(const char* path, uint32_t* hdr, uint32_t* key_len, uint32_t* keys, float* reps,
+                  uint64_t* freq) {
+  REF_TRY({
+    const plot::PlotTable t = plot::load(path);
+    hdr[0] = t.version_id;
+    hdr[1] = t.parent_id;
+    hdr[2] = t.ngram;
+    hdr[3] = t.hidden_size;
+    hdr[4] = static_cast<uint32_t>(t.entries.size());
+    hdr[5] = t.alpha_centi;
+    size_t e = 0;
+    for (const auto& [k, entry] : t.entries) {
+      if (key_len) key_len[e] = static_cast<uint32_t>(k.size());
+      if (keys)
+        for (uint32_t i = 0; i < t.ngram; ++i) keys[e * t.ngram + i] = i < k.size() ? k[i] : 0;
+      if (freq) freq[e] = entry.freq;
+      if (reps) put(reps, entry.rep);
+      ++e;
+    }
+  });
+}
+
+// load_adapter_set / load_model status only (FormatError -> 9): the reference's verdict on a file
+int ref_adp1_check(const char* path) { REF_TRY((void)adapters::load_adapter_set(path)); }
+int ref_hmi1_check(const char* path) { REF_TRY((void)load_model(path)); }
+
 // retrieve_sequence (retrieval.cpp:82-124) -> len x d doubles, plus the
 // per-window resolve_window levels in the same sweep order (levels[p*n + k]
 // for the k-th window covering p) for gather-index parity.

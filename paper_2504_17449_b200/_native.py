@@ -133,6 +133,15 @@ def _sig(L):
     L.hmi_plot_derive_branch.argtypes = [vp, vp, u32, u32p, u32p, ctypes.c_double, P(vp)]
     L.hmi_plot_select_root.argtypes = [u32, u32, u32, u32p, u32p, P(vp)]
     L.hmi_plot_select_branch.argtypes = [u32, u32, u32p, u32p, ctypes.c_double, P(vp)]
+    cp = ctypes.c_char_p
+    L.hmi_plot_table_shape.argtypes = [vp, u32p, u32p]
+    L.hmi_plot_table_load.argtypes = [cp, P(vp), u32p, u32p, u32p]
+    L.hmi_plot_table_save.argtypes = [vp, cp, u32, u32, cp, u32]
+    L.hmi_adapter_set_load.argtypes = [cp, ctypes.c_char_p, u32, u32p, u32p, u32p, f32p]
+    L.hmi_model_load.argtypes = [cp, P(ModelConfig), f32p, f32p, f32p, f32p]
+    L.hmi_gpu_upload_plot_table.argtypes = [vp, u32, u32, vp]
+    L.hmi_gpu_register_task_file.argtypes = [vp, u32, cp]
+    L.hmi_gpu_check_adapter_dims.argtypes = [vp, u32, u32, u32]
     L.hmi_plot_table_create.argtypes = [u32, u32, u32, u32p, u32p, u64p, f32p, P(vp)]
     L.hmi_plot_table_info.argtypes = [vp, u32p, u64p, u32p]
     L.hmi_plot_table_read.argtypes = [vp, u32p, u32p, u64p, f32p]

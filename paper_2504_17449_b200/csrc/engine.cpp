@@ -1806,6 +1806,20 @@ int hmi_gpu_infer_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instan
   });
 }
 
+int hmi_gpu_check_adapter_dims(hmi_gpu_ctx* ctx, uint32_t layers, uint32_t d, uint32_t r) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(ctx != nullptr, HMI_CONFIG_ERROR, "null context");
+    const Ctx& c = ctx->impl;
+    HMI_CHECK(layers == static_cast<uint32_t>(c.L) && d == static_cast<uint32_t>(c.d) &&
+                  r == static_cast<uint32_t>(c.r),
+              HMI_DIMENSION_ERROR,
+              "adapter set (" + std::to_string(layers) + " layers, d " + std::to_string(d) + ", r " +
+                  std::to_string(r) + ") does not match the model (" + std::to_string(c.L) +
+                  " higher layers, d " + std::to_string(c.d) + ", r " + std::to_string(c.r) + ")");
+  });
+}
+
 int hmi_gpu_trace(hmi_gpu_ctx* ctx, int enable) {
   using namespace hmi_b200;
   return guarded([&] {

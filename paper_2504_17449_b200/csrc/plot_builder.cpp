@@ -547,6 +547,14 @@ int hmi_plot_table_info(const hmi_plot_table* t, uint32_t* n_entries, uint64_t* 
   });
 }
 
+int hmi_plot_table_shape(const hmi_plot_table* t, uint32_t* ngram, uint32_t* d) {
+  return plot_guarded([&] {
+    HMI_CHECK(t != nullptr, HMI_CONFIG_ERROR, "null table");
+    if (ngram) *ngram = t->ngram;
+    if (d) *d = t->d;
+  });
+}
+
 int hmi_plot_table_read(const hmi_plot_table* t, uint32_t* key_len, uint32_t* keys,
                         uint64_t* freq, float* reps) {
   return plot_guarded([&] {

@@ -161,6 +161,23 @@ class GpuEngine:
                               "evicted": [int(x) for x in ev[r.evicted_offset:r.evicted_offset + r.n_evicted]]})
         return BatchResult(scores, labels, tags, trace)
 
+    def upload_plt1(self, path: str) -> tuple[int, int]:
+        """VersionTree::add_branch from a PLT1 file (plot_io.cpp:35-72); (version, parent)."""
+        L = _native.lib()
+        h = ctypes.c_void_p()
+        v, p = ctypes.c_uint32(0), ctypes.c_uint32(0)
+        check(L.hmi_plot_table_load(path.encode(), ctypes.byref(h), ctypes.byref(v), ctypes.byref(p),
+                                    None))
+        try:
+            check(L.hmi_gpu_upload_plot_table(self.h, v.value, p.value, h))
+        finally:
+            L.hmi_plot_table_free(h)
+        return v.value, p.value
+
+    def register_task_file(self, task: int, path: str) -> None:
+        """AdapterStore::register_set from an ADP1 file (adapter_set.cpp:48-75)."""
+        check(_native.lib().hmi_gpu_register_task_file(self.h, task, path.encode()))
+
     STAGES = ("retrieve", "prefetch", "compute", "head", "host")
     WORKERS = ("cpu", "io", "compute")
 

@@ -74,6 +74,67 @@ def table_handle(t: dict, ngram: int, d: int):
     return h
 
 
+def load_plt1(path: str):
+    """A PLT1 file (plot_io.cpp:35-72) -> (table dict, version_id, parent_id, alpha_centi)."""
+    h = ctypes.c_void_p()
+    v, p, a = ctypes.c_uint32(0), ctypes.c_uint32(0), ctypes.c_uint32(0)
+    check(_native.lib().hmi_plot_table_load(path.encode(), ctypes.byref(h), ctypes.byref(v),
+                                            ctypes.byref(p), ctypes.byref(a)))
+    return _finish_any(h), v.value, p.value, a.value
+
+
+def _finish_any(h) -> dict:
+    """Like _finish for a handle whose ngram / d only the library knows."""
+    ngram, d = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    try:
+        check(_native.lib().hmi_plot_table_shape(h, ctypes.byref(ngram), ctypes.byref(d)))
+    except Exception:
+        _native.lib().hmi_plot_table_free(h)
+        raise
+    return _finish(h, ngram.value, d.value)
+
+
+def save_plt1(table: dict, path: str, version_id: int, parent_id: int, label: str = "",
+              alpha_centi: int = 0, ngram: int | None = None, d: int | None = None) -> None:
+    """Persist a table as PLT1 (plot_io.cpp:17-33), readable by the reference's plot::load."""
+    ngram = ngram or np.asarray(table["keys"]).shape[1]
+    d = d or np.asarray(table["reps"]).shape[1]
+    h = table_handle(table, ngram, d)
+    try:
+        check(_native.lib().hmi_plot_table_save(h, path.encode(), version_id, parent_id & 0xFFFFFFFF,
+                                                label.encode(), alpha_centi))
+    finally:
+        _native.lib().hmi_plot_table_free(h)
+
+
+def load_adp1(path: str):
+    """An ADP1 adapter set (adapter_set.cpp:48-75) -> (task_id, f32 body [layers, floats])."""
+    L = _native.lib()
+    layers, d, r = ctypes.c_uint32(0), ctypes.c_uint32(0), ctypes.c_uint32(0)
+    name = ctypes.create_string_buffer(1024)
+    check(L.hmi_adapter_set_load(path.encode(), name, 1024, ctypes.byref(layers), ctypes.byref(d),
+                                 ctypes.byref(r), None))
+    per = 2 * d.value * r.value + r.value + d.value
+    body = np.empty((layers.value, per), np.float32)
+    check(L.hmi_adapter_set_load(path.encode(), None, 0, None, None, None, _p(body, ctypes.c_float)))
+    return name.value.decode(), body
+
+
+def load_hmi1(path: str):
+    """An HMI1 model (model_io.cpp:83-115) -> (ModelConfig, token_emb, pos_emb, lower, higher)."""
+    L = _native.lib()
+    cfg = ModelConfig()
+    check(L.hmi_model_load(path.encode(), ctypes.byref(cfg), None, None, None, None))
+    d = cfg.hidden_size
+    tok = np.empty((cfg.vocab_size, d), np.float32)
+    pos = np.empty((cfg.max_fragment, d), np.float32)
+    low = np.empty((cfg.lower_layers, layer_floats(cfg)), np.float32)
+    hi = np.empty((cfg.higher_layers, layer_floats(cfg)), np.float32)
+    check(L.hmi_model_load(path.encode(), ctypes.byref(cfg), _p(tok, ctypes.c_float),
+                           _p(pos, ctypes.c_float), _p(low, ctypes.c_float), _p(hi, ctypes.c_float)))
+    return cfg, tok, pos, low, hi
+
+
 def select_root(corpus, ngram: int, vocab: int) -> dict:
     """build_root's key selection only (host, no GPU): keys + frequencies."""
     n_seq, lens, toks = _corpus(corpus)
