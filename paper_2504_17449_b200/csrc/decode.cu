@@ -28,6 +28,7 @@
 #include <cstdint>
 
 #include "decode.hpp"
+#include "sm100.cuh"
 
 namespace hmi_b200 {
 
@@ -380,6 +381,134 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnDecodeArgs A) {
   }
 }
 
+// TMA-staged decode attention: one CTA per (head, request). Shared memory: the prompt's K and V
+// head slices (S rows x 128 B each, SWIZZLE_128B: 16-byte chunk c of row r at (c ^ r % 8)) and
+// the generated rows' K and V (tail_cap rows each); keys / values are read from shared memory
+// only, the new row (j == pos) from this step's projections.
+constexpr int kDecS = 256;     // max prompt rows staged (2 boxes of 128)
+__global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_constant__ AttnDecodeMaps M,
+                                                             AttnDecodeArgs A) {
+  extern __shared__ uint8_t dsm[];
+  uint8_t* base = dsm + ((1024 - (smem_u32(dsm) & 1023)) & 1023);
+  const int S = A.S, T = A.tail_cap;
+  uint8_t* kpre = base;                         // [S][128 B]
+  uint8_t* vpre = kpre + S * 128;
+  uint8_t* ktail = vpre + S * 128;              // [T][128 B] (1024-aligned: S % 128 == 0)
+  uint8_t* vtail = ktail + ((T * 128 + 1023) & ~1023);
+  float* sc = reinterpret_cast<float*>(vtail + ((T * 128 + 1023) & ~1023));  // [S + T] scores
+  __shared__ float qs[64];
+  __shared__ float red[32];
+  __shared__ float part[4 * 64];
+  __shared__ uint64_t bar;
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = A.d;
+  const int pos = A.gen_pos[b];
+  const int len0 = A.lens[b];
+  const int nk = pos + 1;
+  const int n_tail = pos - len0;  // generated rows already cached
+  const uint16_t* qrow = A.qkv_new + static_cast<long long>(b) * 3 * d;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nbox = (len0 + 127) / 128;
+    const uint32_t bytes = nbox * 2 * 16384 + (n_tail > 0 ? 2 * T * 128 : 0);
+    mbar_arrive_expect_tx(&bar, bytes);
+    for (int x = 0; x < nbox; ++x) {
+      tma_load_2d(kpre + x * 16384, &M.prefill, &bar, d + h * 64, b * S + 128 * x);
+      tma_load_2d(vpre + x * 16384, &M.prefill, &bar, 2 * d + h * 64, b * S + 128 * x);
+    }
+    if (n_tail > 0) {
+      tma_load_2d(ktail, &M.tail, &bar, h * 64, b * T);
+      tma_load_2d(vtail, &M.tail, &bar, d + h * 64, b * T);
+    }
+  }
+  if (threadIdx.x < 64) qs[threadIdx.x] = ld16(qrow, h * 64 + threadIdx.x, A.bf16);
+  __syncthreads();
+  // append this row's k, v (head slice) to the generated-rows cache (global; the staged copy of
+  // that row is never read: j == pos comes from qkv_new)
+  if (threadIdx.x < 64) {
+    uint16_t* trow = A.tail + (static_cast<long long>(b) * T + n_tail) * 2 * d;
+    if (threadIdx.x < 32) {
+      reinterpret_cast<uint32_t*>(trow + h * 64)[threadIdx.x] =
+          reinterpret_cast<const uint32_t*>(qrow + d + h * 64)[threadIdx.x];
+    } else {
+      reinterpret_cast<uint32_t*>(trow + d + h * 64)[threadIdx.x - 32] =
+          reinterpret_cast<const uint32_t*>(qrow + 2 * d + h * 64)[threadIdx.x - 32];
+    }
+  }
+  mbar_wait(&bar, 0);
+  // row r of a staged operand: 8 chunks of 16 B, swizzled
+  auto srow = [&](const uint8_t* box, int r, int c) -> const uint4* {
+    return reinterpret_cast<const uint4*>(box + r * 128 + ((c ^ (r & 7)) << 4));
+  };
+  for (int j = threadIdx.x; j < nk; j += blockDim.x) {
+    float s = 0.f;
+    if (j == pos) {
+      const uint4* kp = reinterpret_cast<const uint4*>(qrow + d + h * 64);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float f[8];
+        unpack8(kp[c], f, A.bf16);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += f[i] * qs[8 * c + i];
+      }
+    } else {
+      const uint8_t* box = j < len0 ? kpre : ktail;
+      const int r = j < len0 ? j : j - len0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float f[8];
+        unpack8(*srow(box, r, c), f, A.bf16);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += f[i] * qs[8 * c + i];
+      }
+    }
+    sc[j] = s * A.scale;
+  }
+  __syncthreads();
+  float m = -INFINITY;
+  for (int j = threadIdx.x; j < nk; j += blockDim.x) m = fmaxf(m, sc[j]);
+  m = block_max_f(m, red);
+  float sum = 0.f;
+  for (int j = threadIdx.x; j < nk; j += blockDim.x) {
+    const float e = __expf(sc[j] - m);
+    sc[j] = e;
+    sum += e;
+  }
+  sum = block_sum_t(sum, red);  // contains the barrier that publishes sc[]
+  // context: warp w takes keys j = w (mod 4); lane its dims 2 lane, 2 lane + 1 (4 bytes of the
+  // row's chunk lane / 4)
+  float a0 = 0.f, a1 = 0.f;
+  const int c = lane >> 2, cb = (lane & 3) * 4;
+  for (int j = warp; j < nk; j += 4) {
+    uint32_t u;
+    if (j == pos) {
+      u = reinterpret_cast<const uint32_t*>(qrow + 2 * d + h * 64)[lane];
+    } else {
+      const uint8_t* box = j < len0 ? vpre : vtail;
+      const int r = j < len0 ? j : j - len0;
+      u = *reinterpret_cast<const uint32_t*>(box + r * 128 + ((c ^ (r & 7)) << 4) + cb);
+    }
+    const float2 v = A.bf16 ? make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u))
+                            : __half22float2(*reinterpret_cast<const __half2*>(&u));
+    const float p = sc[j];
+    a0 += p * v.x;
+    a1 += p * v.y;
+  }
+  part[warp * 64 + 2 * lane] = a0;
+  part[warp * 64 + 2 * lane + 1] = a1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int cc = threadIdx.x;
+    const float o = (part[cc] + part[64 + cc] + part[128 + cc] + part[192 + cc]) / sum;
+    A.ctx[static_cast<long long>(b) * d + h * 64 + cc] = st16(o, A.bf16);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // One CTA per decode row: y = relu(a.Wd + bd).Wu + bu + a + h, x = LN1(y).
 __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A) {
@@ -480,6 +609,40 @@ void launch_attn_decode(const AttnDecodeArgs& a, int n_req, int heads, int max_k
                                   static_cast<int>(smem)));
   }
   attn_decode_kernel<<<dim3(heads, n_req), 128, smem, stream>>>(a);
+  HMI_CUDA(cudaGetLastError());
+}
+
+bool attn_decode_tma_ok(int S, int tail_cap) {
+  return S % 128 == 0 && S <= kDecS && tail_cap >= 1 && tail_cap <= 256;
+}
+
+AttnDecodeMaps make_attn_decode_maps(const void* qkv_prefill, int max_rows, void* tail,
+                                     int max_batch, int tail_cap, int d, int precision) {
+  const CUtensorMapDataType t16 =
+      precision == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  AttnDecodeMaps m;
+  m.prefill = make_tmap_2d(qkv_prefill, t16, 3ull * d, max_rows, 3ull * d * 2, 64, 128,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+  m.tail = make_tmap_2d(tail, t16, 2ull * d, static_cast<uint64_t>(max_batch) * tail_cap,
+                        2ull * d * 2, 64, static_cast<uint32_t>(tail_cap), CU_TENSOR_MAP_SWIZZLE_128B);
+  return m;
+}
+
+void launch_attn_decode_tma(const AttnDecodeArgs& a, const AttnDecodeMaps& m, int n_req,
+                            int heads, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  HMI_CHECK(attn_decode_tma_ok(a.S, a.tail_cap) && a.d == heads * 64, HMI_CONFIG_ERROR,
+            "decode attention: staged form needs S % 128 == 0, S <= 256, tail <= 256, dh 64");
+  const size_t tail_b = (static_cast<size_t>(a.tail_cap) * 128 + 1023) & ~static_cast<size_t>(1023);
+  const size_t smem = 1024 + 2 * static_cast<size_t>(a.S) * 128 + 2 * tail_b +
+                      static_cast<size_t>(a.S + a.tail_cap + 4) * 4;
+  static size_t configured = 0;
+  if (smem > configured) {
+    HMI_CUDA(cudaFuncSetAttribute(attn_decode_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  attn_decode_tma_kernel<<<dim3(heads, n_req), 128, smem, stream>>>(m, a);
   HMI_CUDA(cudaGetLastError());
 }
 

@@ -2,6 +2,7 @@
 // Launchers of the causal-generation kernels (decode.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -56,6 +57,20 @@ struct AttnDecodeArgs {
 };
 void launch_attn_decode(const AttnDecodeArgs& a, int n_req, int heads, int max_keys,
                         cudaStream_t stream);
+
+// TMA-staged form (one layer): the request's prompt K / V head slices (SWIZZLE_128B boxes of
+// 128 rows x 64 dims over the layer's prompt q|k|v buffer) and its generated rows' k / v (one
+// box of tail_cap rows over the layer's tail buffer) land in shared memory with four bulk
+// copies; scores and context then read shared memory only.
+struct AttnDecodeMaps {
+  CUtensorMap prefill;  // [rows][3d] 16-bit, box 64 x 128
+  CUtensorMap tail;     // [n * tail_cap][2d] 16-bit, box 64 x tail_cap
+};
+bool attn_decode_tma_ok(int S, int tail_cap);
+AttnDecodeMaps make_attn_decode_maps(const void* qkv_prefill, int max_rows, void* tail,
+                                     int max_batch, int tail_cap, int d, int precision);
+void launch_attn_decode_tma(const AttnDecodeArgs& a, const AttnDecodeMaps& m, int n_req,
+                            int heads, cudaStream_t stream);
 
 struct AdapterRowsArgs {
   const uint16_t* a16 = nullptr;  // [n][d] attention output (after Wo, bo)

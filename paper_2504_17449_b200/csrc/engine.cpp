@@ -304,6 +304,7 @@ struct Ctx {
   int gen_stride = 0;
   struct DecPlans {
     GemmPlan qkv, oproj, ffn1, ffn2;
+    AttnDecodeMaps attn;  // TMA maps over this layer's prompt q|k|v and generated k|v
   };
   std::vector<DecPlans> dec;
   // wide lm heads (kind 2, labels > max_labels): 16-bit [V_pad][d] GEMM operand + padded bias
@@ -700,6 +701,11 @@ void Ctx::build_plans() {
       s.b_group_stride_bytes = size_t(d) * f * 2; s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
       s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, mt, sms);
       dp.ffn2 = make_gemm_plan(s);
+      dp.attn = make_attn_decode_maps(qkv_at(l), max_rows,
+                                      kv_tail.p + static_cast<size_t>(l) * opt.max_batch *
+                                                      opt.max_new_tokens * 2 * d,
+                                      static_cast<int>(opt.max_batch),
+                                      static_cast<int>(opt.max_new_tokens), d, prec);
       dec.push_back(dp);
     }
   }
@@ -1182,7 +1188,11 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
         a.d = d;
         a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d / heads)));
         a.bf16 = prec;
-        launch_attn_decode(a, n, heads, S + static_cast<int>(n_new), s);
+        if (attn_decode_tma_ok(S, T)) {
+          launch_attn_decode_tma(a, dec[l].attn, n, heads, s);
+        } else {
+          launch_attn_decode(a, n, heads, S + static_cast<int>(n_new), s);
+        }
       });
       timed(P_OPROJ, s, [&] { launch_gemm(dp.oproj, Mp, s); });
       timed(P_AD_UP, s, [&] {
