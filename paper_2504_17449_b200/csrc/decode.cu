@@ -511,11 +511,13 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
 
 // ---------------------------------------------------------------------------
 // One CTA per decode row: y = relu(a.Wd + bd).Wu + bu + a + h, x = LN1(y).
+// RP > 0: bottleneck fixed at compile time (all weight loads of a unit / an output in flight)
+template <int RP>
 __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A) {
   extern __shared__ float sm[];  // a[d], y[d], mid[r_pad]
   __shared__ float red[32];
   const int b = blockIdx.x;
-  const int d = A.d, rp = A.r_pad;
+  const int d = A.d, rp = RP > 0 ? RP : A.r_pad;
   float* a = sm;
   float* y = sm + d;
   float* mid = sm + 2 * d;
@@ -536,17 +538,19 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   __syncthreads();
   // down projection: warp per bottleneck unit, 16-byte weight vectors across the lanes
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < rp; j += nw) {
-    const uint4* w4 = reinterpret_cast<const uint4*>(wd + static_cast<size_t>(j) * d);
-    float acc = 0.f;
-    for (int c = lane; c < d / 8; c += 32) {
-      float f[8];
-      unpack8(__ldg(w4 + c), f, A.bf16);
+  {
+    for (int j = warp; j < rp; j += nw) {
+      const uint4* w4 = reinterpret_cast<const uint4*>(wd + static_cast<size_t>(j) * d);
+      float acc = 0.f;
+      for (int c = lane; c < d / 8; c += 32) {
+        float f[8];
+        unpack8(__ldg(w4 + c), f, A.bf16);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc += a[c * 8 + e] * f[e];
+        for (int e = 0; e < 8; ++e) acc += a[c * 8 + e] * f[e];
+      }
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) mid[j] = fmaxf(acc + bd[j], 0.f);
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) mid[j] = fmaxf(acc + bd[j], 0.f);
   }
   __syncthreads();
   // the GEMM path rounds the bottleneck activations to 16 bits; so does this one
@@ -560,11 +564,24 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const uint4* w4 = reinterpret_cast<const uint4*>(wu + static_cast<size_t>(i) * rp);
     float acc = 0.f;
-    for (int c = 0; c < rp / 8; ++c) {
-      float f[8];
-      unpack8(__ldg(w4 + c), f, A.bf16);
+    if constexpr (RP > 0) {
+      uint4 w[RP / 8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
+      for (int c = 0; c < RP / 8; ++c) w[c] = __ldg(w4 + c);
+#pragma unroll
+      for (int c = 0; c < RP / 8; ++c) {
+        float f[8];
+        unpack8(w[c], f, A.bf16);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
+      }
+    } else {
+      for (int c = 0; c < rp / 8; ++c) {
+        float f[8];
+        unpack8(__ldg(w4 + c), f, A.bf16);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
+      }
     }
     const float v = acc + bu[i] + a[i] + ld16(hrow, i, A.bf16);
     y[i] = v;
@@ -650,7 +667,11 @@ void launch_adapter_rows_ln(const AdapterRowsArgs& a, int n_req, cudaStream_t st
   if (n_req <= 0) return;
   HMI_CHECK(a.d % 8 == 0 && a.r_pad % 8 == 0, HMI_CONFIG_ERROR, "adapter rows: d, r_pad % 8");
   const size_t smem = static_cast<size_t>(2 * a.d + a.r_pad) * sizeof(float);
-  adapter_rows_ln_kernel<<<n_req, 256, smem, stream>>>(a);
+  if (a.r_pad == 64) {
+    adapter_rows_ln_kernel<64><<<n_req, 256, smem, stream>>>(a);
+  } else {
+    adapter_rows_ln_kernel<0><<<n_req, 256, smem, stream>>>(a);
+  }
   HMI_CUDA(cudaGetLastError());
 }
 
