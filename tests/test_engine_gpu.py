@@ -302,6 +302,21 @@ def test_base_parity(n_req):
     w.eng.close()
 
 
+def test_large_parity_three_level_tree():
+    """C5 shapes (hBERT-large: d=1024, 16 heads, 12 higher layers, ffn 4096, r=64): the fused
+    adapter at d=1024 (16 row-statistics partials), a 3-level domain tree."""
+    w = World(oracle.LARGE, n_tasks=6, r=64, labels=8, max_batch=6,
+              branches=((0, 60), (0, 60), (1, 40), (2, 40)), n_hot=64, n_bi=300, n_tri=300)
+    inst, toks, lens = w.requests(43, 6, 128, min_len=90)
+    res = w.eng.infer_batch(inst, toks, lens)
+    ref_scores, ref_labels, _ = w.oracle_batch(inst, toks, lens, threads=32)
+    err = logit_error(res.scores, ref_scores)
+    print(f"C5 logit err {err:.3e}, argmax agreement {(res.labels == ref_labels).mean():.4f}")
+    assert err <= TOL
+    assert (res.labels == ref_labels).mean() >= 0.999
+    w.eng.close()
+
+
 @pytest.fixture(scope="module")
 def gpt():
     """hGPT-style tiny causal model, one vocabulary-wide lm head (1024 > max_labels) shared
