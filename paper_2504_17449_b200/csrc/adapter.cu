@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   // TMEM columns: mid acc 0..63, y acc[0] 128..255, y acc[1] 256..383
 
   if (warp == 0) {
@@ -441,9 +443,9 @@ void launch_adapter(const AdapterPlan& p, int rows, cudaStream_t stream) {
   a.num_m_tiles = rows / 128;
   const int grid = a.num_m_tiles < device_sm_count() ? a.num_m_tiles : device_sm_count();
   if (bf) {
-    adapter_fused_kernel<true><<<grid, kThreads, kSmem, stream>>>(p.maps, a);
+    launch_pdl(adapter_fused_kernel<true>, dim3(grid), dim3(kThreads), kSmem, stream, p.maps, a);
   } else {
-    adapter_fused_kernel<false><<<grid, kThreads, kSmem, stream>>>(p.maps, a);
+    launch_pdl(adapter_fused_kernel<false>, dim3(grid), dim3(kThreads), kSmem, stream, p.maps, a);
   }
   HMI_CUDA(cudaGetLastError());
 }

@@ -110,6 +110,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   // TMEM columns: S[0] 0..127, S[1] 128..255, O[0] 256..319, O[1] 320..383
   const int my_first = blockIdx.x, step = gridDim.x;
 
@@ -309,11 +311,11 @@ void launch_attention_tc(const AttnPlan& p, const int* lens, int n_req, int head
     configured[bf] = true;
   }
   if (bf) {
-    attention_tc_kernel<true><<<grid, kTcThreads, kSmem, stream>>>(p.map_qkv, p.map_ctx, lens, items,
-                                                                   heads, p.d, causal, scale_log2);
+    launch_pdl(attention_tc_kernel<true>, dim3(grid), dim3(kTcThreads), kSmem, stream, p.map_qkv,
+               p.map_ctx, lens, items, heads, p.d, causal, scale_log2);
   } else {
-    attention_tc_kernel<false><<<grid, kTcThreads, kSmem, stream>>>(p.map_qkv, p.map_ctx, lens, items,
-                                                                    heads, p.d, causal, scale_log2);
+    launch_pdl(attention_tc_kernel<false>, dim3(grid), dim3(kTcThreads), kSmem, stream, p.map_qkv,
+               p.map_ctx, lens, items, heads, p.d, causal, scale_log2);
   }
   HMI_CUDA(cudaGetLastError());
 }

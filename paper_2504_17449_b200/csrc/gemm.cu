@@ -319,8 +319,7 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
     grid = tiles < device_sm_count() ? tiles : device_sm_count();
   }
   KernelFn fn = reinterpret_cast<KernelFn>(p.fn);
-  fn<<<grid, kGemmThreads, p.smem_bytes, stream>>>(p.maps, a);
-  HMI_CUDA(cudaGetLastError());
+  launch_pdl(fn, dim3(grid), dim3(kGemmThreads), p.smem_bytes, stream, p.maps, a);
 }
 
 }  // namespace hmi_b200

@@ -577,6 +577,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // inputs of the previous kernel are complete and visible from here on
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -793,6 +795,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // inputs of the previous kernel are complete and visible from here on
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)

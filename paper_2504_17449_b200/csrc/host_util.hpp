@@ -10,6 +10,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -91,6 +93,26 @@ inline CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dtype, uin
     throw HmiError(HMI_CUDA_ERROR, "cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
   }
   return m;
+}
+
+// Launch with programmatic stream serialization (the kernel may begin before its predecessor
+// in the stream completes; it must griddepcontrol.wait before reading that predecessor's
+// outputs). HMI_PDL=0 launches normally.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+  static const bool on = std::getenv("HMI_PDL") == nullptr || std::string(std::getenv("HMI_PDL")) != "0";
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = on ? 1 : 0;
+  HMI_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
 inline int device_sm_count() {

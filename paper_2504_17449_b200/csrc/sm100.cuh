@@ -28,6 +28,18 @@ __device__ __forceinline__ uint32_t warp_id() {
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // ---------------------------------------------------------------------------
+// programmatic dependent launch: the next kernel in the stream (launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization) may start once every CTA of this grid
+// has triggered; griddepcontrol.wait blocks until the previous grid completed and its memory
+// is visible. Persistent kernels trigger right after their prologue, so the next kernel's
+// CTAs take SMs as this grid's CTAs retire and run their own prologue meanwhile.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // mbarrier
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
