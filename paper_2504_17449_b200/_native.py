@@ -148,6 +148,8 @@ def _sig(L):
     L.hmi_plot_table_free.argtypes = [vp]
     L.hmi_gpu_trace.argtypes = [vp, ctypes.c_int]
     L.hmi_gpu_stage_trace.argtypes = [vp, ctypes.c_void_p, u32, u32p]
+    L.hmi_gpu_copy_probe.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.c_int,
+                                     ctypes.c_int, f64p]
     L.hmi_gpu_submit_batch.argtypes = [vp, u32, u32p, u32p, u32, u32p, u64p]
     L.hmi_gpu_wait_batch.argtypes = [vp, u64, f32p, i32p]
     L.hmi_gpu_synchronize.argtypes = [vp]

@@ -935,22 +935,22 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[L - 1], 0));
   }
   timed(P_H2D, s, [&] {
-    HMI_CUDA(cudaMemcpyAsync(d_inst.p, st.inst, n_req * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    // inputs fetched by a kernel (SM loads over PCIe from the pinned staging): copy-engine
+    // transfers on this stream would queue behind later batches' adapter copies
+    FetchArgs fa;
+    fa.inst = st.inst; fa.d_inst = d_inst.p; fa.n_inst = static_cast<int>(n_req);
+    fa.d_tokens = d_tokens.p; fa.n_req = static_cast<int>(n_req); fa.S = S;
     if (tokens_host) {
-      HMI_CUDA(cudaMemcpyAsync(d_tokens.p, st.tokens, static_cast<size_t>(n_req) * S * sizeof(uint32_t),
-                               cudaMemcpyHostToDevice, s));
-      HMI_CUDA(cudaMemcpyAsync(d_lens.p, st.lens, n_req * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      fa.tokens = st.tokens; fa.src_stride = S;
+      fa.lens = st.lens;
     } else {
-      HMI_CUDA(cudaMemcpy2DAsync(d_tokens.p, static_cast<size_t>(S) * sizeof(uint32_t), tokens_dev,
-                                 static_cast<size_t>(stride) * sizeof(uint32_t),
-                                 std::min<uint32_t>(stride, S) * sizeof(uint32_t), n_req,
-                                 cudaMemcpyDeviceToDevice, s));
-      HMI_CUDA(cudaMemcpyAsync(d_lens.p, lens_dev, n_req * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+      fa.tokens = tokens_dev; fa.src_stride = static_cast<int>(stride);
+      fa.lens = reinterpret_cast<const int32_t*>(lens_dev);
     }
-    if (!delta.empty()) {
-      HMI_CUDA(cudaMemcpyAsync(d_delta.p, st.delta, delta.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    }
-    HMI_CUDA(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), s));
+    fa.d_lens = d_lens.p;
+    fa.delta = st.delta; fa.d_delta = d_delta.p; fa.n_delta = static_cast<int>(delta.size());
+    fa.d_err = d_err.p;
+    launch_fetch_inputs(fa, s);
   });
   timed(P_ROUTE, s, [&] {
     if (!delta.empty()) launch_apply_deltas(d_slot_of.p, d_delta.p, static_cast<int>(delta.size() / 2), s);
@@ -1076,7 +1076,8 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   inflight.push_back(Inflight{st.done, si, uniq});
   last_n = n_req;
   const uint64_t per_layer = ln_mode == 1 ? 9ull : (ln_mode == 0 && adapter_fused) ? 6ull : 7ull;
-  n_launches += (delta.empty() ? 0 : 1) + 2 + (gen ? 0 : 1) + per_layer * L;
+  // fetch_inputs + route + retrieve (+ apply_deltas) + layers + head
+  n_launches += (delta.empty() ? 0 : 1) + 3 + (gen ? 0 : 1) + per_layer * L;
   if (wide_head >= 0) n_launches += 3 + (gen ? (n_new - 1ull) * (3 + 7ull * L) : 0);
   ++n_batches;
   last_S = static_cast<uint32_t>(S);

@@ -6,6 +6,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -396,5 +397,91 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
   for (void* p : {dA, dB, dBias, dC, dSlot, dR0, dR1}) {
     if (p) cudaFree(p);
   }
+  return status;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI: host -> HBM copy probe (adapter slot transfers): n pieces of `bytes` each from
+// pinned host memory into scattered device slots. mode 0: one contiguous copy of n * bytes;
+// 1: n cudaMemcpyAsync; 2: one cudaMemcpyBatchAsync; 3: zero-copy gather kernel (device reads
+// mapped pinned memory, `ctas` CTAs). Returns GB/s of the timed (second) repetition.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void zero_copy_gather_kernel(const uint4* const* src, uint4* const* dst, int n,
+                                        size_t vec_per_piece) {
+  const size_t total = static_cast<size_t>(n) * vec_per_piece;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t p = i / vec_per_piece, o = i - p * vec_per_piece;
+    dst[p][o] = src[p][o];
+  }
+}
+}  // namespace
+
+extern "C" int hmi_gpu_copy_probe(int device, int n, size_t bytes, int mode, int ctas,
+                                  double* gbps) {
+  using namespace hmi_b200;
+  uint8_t *h = nullptr, *dbuf = nullptr;
+  void **d_src = nullptr, **d_dst = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int status = HMI_OK;
+  try {
+    HMI_CUDA(cudaSetDevice(device));
+    HMI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h), static_cast<size_t>(n) * bytes, cudaHostAllocMapped));
+    std::memset(h, 1, static_cast<size_t>(n) * bytes);
+    HMI_CUDA(cudaMalloc(&dbuf, static_cast<size_t>(2 * n) * bytes));
+    std::vector<void*> src(n), dst(n), hs(n);
+    std::vector<size_t> sz(n, bytes);
+    for (int i = 0; i < n; ++i) {
+      hs[i] = h + static_cast<size_t>(i) * bytes;
+      dst[i] = dbuf + static_cast<size_t>((i * 7919) % (2 * n)) * bytes;  // scattered slots
+      void* dp = nullptr;
+      HMI_CUDA(cudaHostGetDevicePointer(&dp, hs[i], 0));
+      src[i] = dp;
+    }
+    HMI_CUDA(cudaMalloc(&d_src, n * sizeof(void*)));
+    HMI_CUDA(cudaMalloc(&d_dst, n * sizeof(void*)));
+    HMI_CUDA(cudaMemcpy(d_src, src.data(), n * sizeof(void*), cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaMemcpy(d_dst, dst.data(), n * sizeof(void*), cudaMemcpyHostToDevice));
+    HMI_CUDA(cudaEventCreate(&e0));
+    HMI_CUDA(cudaEventCreate(&e1));
+    float ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {
+      HMI_CUDA(cudaEventRecord(e0, st));
+      if (mode == 0) {
+        HMI_CUDA(cudaMemcpyAsync(dbuf, h, static_cast<size_t>(n) * bytes, cudaMemcpyHostToDevice, st));
+      } else if (mode == 1) {
+        for (int i = 0; i < n; ++i)
+          HMI_CUDA(cudaMemcpyAsync(dst[i], hs[i], bytes, cudaMemcpyHostToDevice, st));
+      } else if (mode == 2) {
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+        size_t ai = 0, fi = 0;
+        HMI_CUDA(cudaMemcpyBatchAsync(dst.data(), hs.data(), sz.data(), n, &attr, &ai, 1, &fi, st));
+      } else {
+        zero_copy_gather_kernel<<<ctas, 512, 0, st>>>(reinterpret_cast<const uint4* const*>(d_src),
+                                                      reinterpret_cast<uint4* const*>(d_dst), n,
+                                                      bytes / 16);
+        HMI_CUDA(cudaGetLastError());
+      }
+      HMI_CUDA(cudaEventRecord(e1, st));
+      HMI_CUDA(cudaEventSynchronize(e1));
+      HMI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    }
+    if (gbps) *gbps = static_cast<double>(n) * bytes / (ms * 1e-3) / 1e9;
+  } catch (const HmiError& e) {
+    set_last_error(e.what());
+    status = e.code;
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (d_src) cudaFree(d_src);
+  if (d_dst) cudaFree(d_dst);
+  if (dbuf) cudaFree(dbuf);
+  if (h) cudaFreeHost(h);
+  if (st) cudaStreamDestroy(st);
   return status;
 }

@@ -50,6 +50,19 @@ void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* len
                      int32_t* err, cudaStream_t stream, const int32_t* dec_pos = nullptr,
                      int tok_stride = 0);
 
+// Per-batch inputs into their device buffers with SM loads (instance ids, tokens with a source
+// row stride, lengths, slot-table deltas; the error word zeroed). Sources may be pinned host
+// memory (read over PCIe through unified addressing) or device memory. Unlike cudaMemcpyAsync
+// this never queues behind the copy engine's adapter transfers of later batches.
+struct FetchArgs {
+  const uint32_t* inst = nullptr;   uint32_t* d_inst = nullptr;   int n_inst = 0;
+  const uint32_t* tokens = nullptr; uint32_t* d_tokens = nullptr; int n_req = 0, S = 0, src_stride = 0;
+  const int32_t* lens = nullptr;    int32_t* d_lens = nullptr;
+  const int32_t* delta = nullptr;   int32_t* d_delta = nullptr;   int n_delta = 0;
+  int32_t* d_err = nullptr;
+};
+void launch_fetch_inputs(const FetchArgs& a, cudaStream_t stream);
+
 // K6: routing instance -> (version, task, head) and task -> per-layer HBM slot.
 void launch_route(const uint32_t* instance_idx, int n_req, const int32_t* inst_version,
                   const int32_t* inst_task, const int32_t* inst_head, int n_instances,

@@ -9,6 +9,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -304,6 +305,22 @@ __global__ void __launch_bounds__(256, 6) retrieve_kernel(PlotDev P, const uint3
       *reinterpret_cast<uint2*>(static_cast<uint16_t*>(h16) + orow * d + col) = pk;
     }
   }
+}
+
+__global__ void fetch_inputs_kernel(FetchArgs A) {
+  const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long nthr = static_cast<long long>(gridDim.x) * blockDim.x;
+  if (tid == 0 && A.d_err) *A.d_err = 0;
+  const int cols = A.src_stride < A.S ? A.src_stride : A.S;
+  const long long ntok = static_cast<long long>(A.n_req) * A.S;
+  for (long long i = tid; i < ntok; i += nthr) {
+    const long long r = i / A.S, c = i - r * A.S;
+    if (c < cols) A.d_tokens[i] = A.tokens[r * A.src_stride + c];
+  }
+  for (long long i = tid; i < A.n_inst; i += nthr) A.d_inst[i] = A.inst[i];
+  if (A.lens)
+    for (long long i = tid; i < A.n_req; i += nthr) A.d_lens[i] = A.lens[i];
+  for (long long i = tid; i < A.n_delta; i += nthr) A.d_delta[i] = A.delta[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -604,6 +621,13 @@ void launch_normalize_rows(const void* y16, const float2* stats, int n_part, flo
   normalize_rows_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(
       static_cast<const uint16_t*>(y16), stats, n_part, inv_n, gamma, beta, out, rows, d,
       precision);
+  HMI_CUDA(cudaGetLastError());
+}
+
+void launch_fetch_inputs(const FetchArgs& a, cudaStream_t stream) {
+  const long long work = static_cast<long long>(a.n_req) * a.S;
+  const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256 + 1, 4 * device_sm_count()));
+  fetch_inputs_kernel<<<blocks, 256, 0, stream>>>(a);
   HMI_CUDA(cudaGetLastError());
 }
 

@@ -16,7 +16,7 @@ from paper_2504_17449_b200.workload import CONFIGS, World  # noqa: E402
 
 n_tenants = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
 pool = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
-n_batches = int(sys.argv[3]) if len(sys.argv) > 3 else 12
+n_batches = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 12
 wl = CONFIGS["c2"]
 world = World(wl)
 mc = E.model_config(wl.hidden_size, wl.heads, wl.lower_layers, wl.higher_layers, wl.ffn_size,
@@ -90,6 +90,15 @@ for name, mode in (("sync", E.MODE_SYNC), ("coarse", E.MODE_COARSE), ("fine", E.
         "io_hidden_frac": overlap(io, comp) / io_busy if io_busy > 0 else 1.0,
     }
     print(name, json.dumps({k: round(v, 3) for k, v in rows[name].items()}), flush=True)
+    if "--timeline" in sys.argv:
+        t0 = min(r["start_ms"] for r in dev)
+        for bt in sorted({r["batch"] for r in recs})[:6]:
+            io_b = [r for r in recs if r["batch"] == bt and r["worker"] == "io"]
+            cp_b = [r for r in recs if r["batch"] == bt and r["worker"] == "compute"]
+            host = [r for r in recs if r["batch"] == bt and r["worker"] == "cpu"]
+            print(f"  batch {bt}: host {host[0]['start_ms'] - t0:7.2f}-{host[0]['end_ms'] - t0:7.2f}  "
+                  f"io {min(r['start_ms'] for r in io_b) - t0:7.2f}-{max(r['end_ms'] for r in io_b) - t0:7.2f}  "
+                  f"compute {min(r['start_ms'] for r in cp_b) - t0:7.2f}-{max(r['end_ms'] for r in cp_b) - t0:7.2f}")
 print(json.dumps({"ablation": "pipeline modes with StageTrace", "tenants": n_tenants,
                   "pool_fraction": pool, "batches": n_batches, "batch": wl.batch, "modes": rows,
                   "fine_over_sync": rows["fine"]["req_per_s"] / rows["sync"]["req_per_s"]}))
