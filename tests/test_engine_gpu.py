@@ -136,6 +136,26 @@ def test_stage_trace_invariants(mode):
             assert ret["start_ms"] >= max(p["end_ms"] for p in pre.values()) - eps
 
 
+def test_zero_adapter_is_identity():
+    """SPEC S:124 / S:169: an adapter whose parameters are all zero is the identity, so a
+    request of that tenant equals the reference's layer_forward without an adapter."""
+    w = World(oracle.TINY, n_tasks=4, r=16, labels=8, max_batch=8)
+    zero = np.zeros_like(w.adapters[2])
+    w.eng.replace_task(2, zero)
+    inst, toks, lens = w.requests(71, 8, 128, min_len=1)
+    inst[:] = 2
+    res = w.eng.infer_batch(inst, toks, lens)
+    ref = []
+    for i in range(len(inst)):
+        hw, hb = w.heads[2]
+        ref.append(oracle.infer_one(w.cfg, w.higher, w.tree, int(w.inst_version[2]), toks[i, :lens[i]],
+                                    None, w.r, hw, hb)[0])
+    ref = np.stack(ref)
+    assert logit_error(res.scores, ref) <= TOL
+    assert (res.labels == ref.argmax(axis=1)).mean() >= 0.999
+    w.eng.close()
+
+
 def test_c1_swap_small_pool_bit_identical(c1):
     """A pool holding only 3 tasks forces evictions and reloads every batch; outputs
     are bit-identical to the all-resident run and the trace obeys the LRU law."""

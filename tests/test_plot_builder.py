@@ -173,3 +173,22 @@ def test_gpu_built_tables_serve_within_tolerance():
     assert (res.labels == g["labels"]).all()
     eng.close()
     b.close()
+
+
+def test_spec_build_root_and_alpha_kats():
+    """SPEC known answers: build_root over [[5, 6, 7]] holds (5), (6), (7), (5, 6),
+    (6, 7), (5, 6, 7) plus every vocabulary uni-gram; (5, 6) occurs twice in
+    [[5, 6, 5, 6]]; with counts {A: 5, B: 3, C: 2} alpha = 50 keeps {A}."""
+    t = plot.select_root([np.array([5, 6, 7])], 3, 10)
+    keys = {k for k, _ in _as_pairs(t)}
+    assert {(5,), (6,), (7,), (5, 6), (6, 7), (5, 6, 7)} <= keys
+    assert all((v,) in keys for v in range(10)) and len(keys) == 10 + 3
+    f = dict(_as_pairs(plot.select_root([np.array([5, 6, 5, 6])], 3, 10)))
+    assert f[(5, 6)] == 2 and f[(6, 5)] == 1 and f[(0,)] == 1
+    # three distinct 2-grams with counts A=5, B=3, C=2 (ngram = 2 so each sequence is one 2-gram)
+    A, B, C = (1, 2), (3, 4), (5, 6)
+    corpus = [np.array(A)] * 5 + [np.array(B)] * 3 + [np.array(C)] * 2
+    kept = [k for k, _ in _as_pairs(plot.select_branch(corpus, 2, 50.0))]
+    assert kept == [A]
+    kept = [k for k, _ in _as_pairs(plot.select_branch(corpus, 2, 50.01))]
+    assert kept == [A, B]  # alpha monotonicity: a larger share keeps a superset
