@@ -186,44 +186,59 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
     consider(x4.w, j0 + 3);
   }
   for (int j = V4 + static_cast<int>(threadIdx.x); j < A.V; j += kArgThreads) consider(lg[j], j);
-#pragma unroll
-  for (int k = 0; k < kTopK; ++k) {
-    cv[threadIdx.x * kTopK + k] = v[k];
-    ci[threadIdx.x * kTopK + k] = ix[k];
-  }
-  __syncthreads();
-  // warp 0 extracts the block's top-k by repeated arg-max over the candidates
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    constexpr int per = kArgThreads * kTopK / 32;
+  // merge the sorted per-thread lists in registers: each round the warp's best head (value,
+  // then lower index) is taken and its owner lane shifts its list; warps' top-k go to shared
+  // memory and warp 0 merges those the same way
+  auto warp_topk = [&](float* hv, int* hi, float* out_v, int* out_i) {
+    const int lane = threadIdx.x & 31;
     for (int k = 0; k < kTopK; ++k) {
-      float bv = -INFINITY;
-      int bi = 0x7fffffff, bp = -1;
-      for (int t = 0; t < per; ++t) {
-        const int p = lane * per + t;
-        const float x = cv[p];
-        const int i = ci[p];
-        if (x > bv || (x == bv && i < bi)) {
-          bv = x;
-          bi = i;
-          bp = p;
-        }
-      }
+      float bv = hv[0];
+      int bi = hi[0];
+      int bl = lane;
+#pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
         if (ov > bv || (ov == bv && oi < bi)) {
           bv = ov;
           bi = oi;
-          bp = op;
+          bl = ol;
         }
       }
-      if (lane == 0) {
-        cand[k] = bi < A.V ? bi : -1;
-        if (bp >= 0) cv[bp] = -INFINITY;
+      if (lane == bl) {  // the winner drops its head
+#pragma unroll
+        for (int t = 0; t < kTopK - 1; ++t) {
+          hv[t] = hv[t + 1];
+          hi[t] = hi[t + 1];
+        }
+        hv[kTopK - 1] = -INFINITY;
+        hi[kTopK - 1] = 0x7fffffff;
       }
-      __syncwarp();
+      if (lane == 0) {
+        out_v[k] = bv;
+        out_i[k] = bi;
+      }
+    }
+  };
+  warp_topk(v, ix, cv + (threadIdx.x >> 5) * kTopK, ci + (threadIdx.x >> 5) * kTopK);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // kArgThreads / 32 warps x kTopK candidates: lane l takes warp l's list when l < #warps
+    float hv[kTopK];
+    int hi[kTopK];
+#pragma unroll
+    for (int t = 0; t < kTopK; ++t) {
+      const bool own = static_cast<int>(threadIdx.x) < kArgThreads / 32;
+      hv[t] = own ? cv[threadIdx.x * kTopK + t] : -INFINITY;
+      hi[t] = own ? ci[threadIdx.x * kTopK + t] : 0x7fffffff;
+    }
+    float tv[kTopK];
+    int ti[kTopK];
+    warp_topk(hv, hi, tv, ti);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < kTopK; ++k) cand[k] = ti[k] < A.V ? ti[k] : -1;
     }
   }
   __syncthreads();
