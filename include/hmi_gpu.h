@@ -335,6 +335,42 @@ int hmi_gpu_upload_plot_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t pa
 int hmi_gpu_register_task_file(hmi_gpu_ctx* ctx, uint32_t task_idx, const char* adp1_path);
 int hmi_gpu_check_adapter_dims(hmi_gpu_ctx* ctx, uint32_t layers, uint32_t d, uint32_t r);
 
+/* ---- peer rebalancing of tenants' adapters ---- */
+/* A task migrating between shards (or a hot task replicated onto another GPU)
+ * moves its HBM slots device to device over NVLink / NVSwitch instead of
+ * re-crossing PCIe from the host store (DeviceSlotPool::ensure_resident,
+ * device_pool.cpp:50-91, fed from a peer instead of AdapterStore::get). The
+ * reference has one device and no such path; the numbers loaded are the ones
+ * register_set would have loaded, bit for bit.                                */
+#define HMI_EXPORT_MAX_LAYERS 64
+typedef struct hmi_task_export {
+  int32_t device;            /* CUDA ordinal of the source engine, in its process */
+  int32_t pid;               /* source process id                                 */
+  uint64_t arena;            /* source slot-arena device address (same process)   */
+  uint8_t ipc_handle[64];    /* cudaIpcMemHandle_t of the arena (other processes) */
+  uint64_t slot_bytes;       /* device bytes per (task, layer) slot               */
+  uint64_t fingerprint;      /* d, layers, bottleneck, precision, slot layout     */
+  uint32_t layers;
+  uint32_t task_idx;
+  int32_t slot[HMI_EXPORT_MAX_LAYERS]; /* per layer: physical slot in the arena   */
+} hmi_task_export;
+/* Makes every layer of a registered task resident in the source's slot pool
+ * (under the LRU law, H2D for missing layers), pins it there until
+ * hmi_gpu_release_export, and describes where its slots live.
+ * Unknown task -> ROUTING; layers > HMI_EXPORT_MAX_LAYERS -> CONFIG.          */
+int hmi_gpu_export_task(hmi_gpu_ctx* src, uint32_t task_idx, hmi_task_export* out);
+/* Registers task_idx in dst and fills its slots from the exported ones by
+ * peer copies (same process: direct; another process: CUDA IPC). The host
+ * copy comes from adapter_f32 when given, else from the freshly filled HBM
+ * slots (D2H, off any batch's critical path). Already registered -> CONFLICT;
+ * model / bottleneck / precision mismatch -> CONFIG. *peer_bytes (nullable):
+ * bytes moved device to device.                                               */
+int hmi_gpu_import_task(hmi_gpu_ctx* dst, uint32_t task_idx, const hmi_task_export* ex,
+                        const float* adapter_f32, uint64_t* peer_bytes);
+/* Unpins an exported task; drop != 0 then unregisters it from the source
+ * (a migration), drop == 0 keeps it (a replication of a hot tenant).         */
+int hmi_gpu_release_export(hmi_gpu_ctx* src, uint32_t task_idx, int drop);
+
 /* ---- standalone kernel probe (K1/K2 GEMM) ------------------------------ */
 /* C[M x N] = epi(A[M x K] . B[g]^T + bias[g]) for a device-side tcgen05 GEMM,
  * host buffers in/out, used by the parity tests of the GEMM kernel alone.

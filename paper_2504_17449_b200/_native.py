@@ -92,6 +92,15 @@ class LoadRecord(ctypes.Structure):
                 ("evicted_offset", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
 
 
+class TaskExport(ctypes.Structure):
+    """hmi_task_export: where an exported task's HBM slots live (include/hmi_gpu.h)."""
+
+    _fields_ = [("device", ctypes.c_int32), ("pid", ctypes.c_int32), ("arena", ctypes.c_uint64),
+                ("ipc_handle", ctypes.c_uint8 * 64), ("slot_bytes", ctypes.c_uint64),
+                ("fingerprint", ctypes.c_uint64), ("layers", ctypes.c_uint32),
+                ("task_idx", ctypes.c_uint32), ("slot", ctypes.c_int32 * 64)]
+
+
 class StageRecord(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_uint64), ("stage", ctypes.c_uint32), ("layer", ctypes.c_int32),
                 ("worker", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("start_ms", ctypes.c_double),
@@ -142,6 +151,9 @@ def _sig(L):
     L.hmi_gpu_upload_plot_table.argtypes = [vp, u32, u32, vp]
     L.hmi_gpu_register_task_file.argtypes = [vp, u32, cp]
     L.hmi_gpu_check_adapter_dims.argtypes = [vp, u32, u32, u32]
+    L.hmi_gpu_export_task.argtypes = [vp, u32, P(TaskExport)]
+    L.hmi_gpu_import_task.argtypes = [vp, u32, P(TaskExport), f32p, u64p]
+    L.hmi_gpu_release_export.argtypes = [vp, u32, ctypes.c_int]
     L.hmi_plot_table_create.argtypes = [u32, u32, u32, u32p, u32p, u64p, f32p, P(vp)]
     L.hmi_plot_table_info.argtypes = [vp, u32p, u64p, u32p]
     L.hmi_plot_table_read.argtypes = [vp, u32p, u32p, u64p, f32p]

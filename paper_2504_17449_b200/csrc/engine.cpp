@@ -27,6 +27,7 @@
 // layer, so layer l+1's copies overlap layer l's compute.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -275,6 +276,18 @@ struct Ctx {
   bool use_batch_copy = std::getenv("HMI_BATCH_COPY") == nullptr ||
                         std::string(std::getenv("HMI_BATCH_COPY")) != "0";
   std::vector<cudaEvent_t> ev_layer;
+  // peer rebalancing: export pins per task, peer arenas opened over CUDA IPC, bytes moved
+  std::map<uint32_t, int> exported;
+  std::map<std::string, void*> ipc_open;
+  uint64_t peer_bytes = 0;
+  uint64_t fingerprint() const {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (uint64_t v : {uint64_t(d), uint64_t(L), uint64_t(r), uint64_t(r_pad), uint64_t(opt.precision),
+                       uint64_t(slot_bytes)}) {
+      for (int i = 0; i < 8; ++i) h = (h ^ ((v >> (8 * i)) & 0xff)) * 0x100000001b3ULL;
+    }
+    return h;
+  }
   // staging / in-flight batches
   Staging stg[kStaging];
   int stg_next = 0;
@@ -454,6 +467,7 @@ Ctx::~Ctx() {
     if (s.done) cudaEventDestroy(s.done);
   }
   for (auto* p : pinned_chunks) cudaFreeHost(p);
+  for (auto& [k, p] : ipc_open) cudaIpcCloseMemHandle(p);
   for (auto e : ev_layer) cudaEventDestroy(e);
   for (auto& [c, e] : prof_pending) {
     cudaEventDestroy(e.first);
@@ -1641,6 +1655,7 @@ int hmi_gpu_replace_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapt
     c.reap(true);
     if (task_idx >= c.store.size() || !c.store[task_idx])
       throw HmiError(HMI_ROUTING_ERROR, "no adapter set registered for task");
+    HMI_CHECK(!c.exported.count(task_idx), HMI_CONFLICT_ERROR, "task is exported to a peer engine");
     c.convert_adapter(adapter_f32, c.store[task_idx]);
     evict_task_slots(c, task_idx, false);
   });
@@ -1654,9 +1669,178 @@ int hmi_gpu_unregister_task(hmi_gpu_ctx* ctx, uint32_t task_idx) {
     HMI_CUDA(cudaSetDevice(c.device));
     c.reap(true);
     if (task_idx >= c.store.size() || !c.store[task_idx]) return;  // AdapterStore::erase is a no-op
+    HMI_CHECK(!c.exported.count(task_idx), HMI_CONFLICT_ERROR, "task is exported to a peer engine");
     evict_task_slots(c, task_idx, true);
     c.free_blocks.push_back(c.store[task_idx]);
     c.store[task_idx] = nullptr;
+  });
+}
+
+// ---- peer rebalancing ---------------------------------------------
+// Out-of-band residency change (nothing in flight): the slot-table entries of the records'
+// evictions and loads are written directly; the batch path ships the same entries as deltas.
+static void write_slot_entries(hmi_b200::Ctx& c, const std::vector<hmi_b200::PoolRecord>& recs) {
+  using namespace hmi_b200;
+  std::vector<std::pair<size_t, int32_t>> w;
+  for (const PoolRecord& rec : recs) {
+    for (const PoolFree& fr : rec.freed) w.push_back({size_t(fr.task) * c.L + fr.layer, -1});
+    for (const PoolLoad& ld : rec.loads) w.push_back({size_t(rec.task) * c.L + ld.layer, ld.slot});
+  }
+  for (const auto& [i, v] : w)
+    HMI_CUDA(cudaMemcpy(c.d_slot_of.p + i, &v, 4, cudaMemcpyHostToDevice));
+}
+
+int hmi_gpu_export_task(hmi_gpu_ctx* src, uint32_t task_idx, hmi_task_export* out) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(src != nullptr && out != nullptr, HMI_CONFIG_ERROR, "null argument");
+    Ctx& c = src->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    HMI_CHECK(c.L <= HMI_EXPORT_MAX_LAYERS, HMI_CONFIG_ERROR, "too many higher layers to export");
+    if (task_idx >= c.store.size() || !c.store[task_idx])
+      throw HmiError(HMI_ROUTING_ERROR, "no adapter set registered for task");
+    c.reap(true);
+    // every layer resident under the LRU law; missing layers come from the pinned host copy
+    auto recs = c.pool->ensure_resident({task_idx});
+    for (const PoolRecord& rec : recs) {
+      for (const PoolLoad& ld : rec.loads) {
+        HMI_CUDA(cudaMemcpyAsync(c.arena.p + size_t(ld.slot) * c.slot_bytes,
+                                 c.store[rec.task] + size_t(ld.layer) * c.slot_bytes, c.slot_bytes,
+                                 cudaMemcpyHostToDevice, c.copy));
+        c.bytes_copied += c.slot_bytes;
+        ++c.n_copies;
+      }
+    }
+    HMI_CUDA(cudaStreamSynchronize(c.copy));
+    write_slot_entries(c, recs);
+    c.pool->pin({task_idx});
+    ++c.exported[task_idx];
+    std::memset(out, 0, sizeof(*out));
+    out->device = c.device;
+    out->pid = static_cast<int32_t>(getpid());
+    out->arena = reinterpret_cast<uint64_t>(c.arena.p);
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, c.arena.p) == cudaSuccess) {
+      static_assert(sizeof(h) == sizeof(out->ipc_handle), "IPC handle size");
+      std::memcpy(out->ipc_handle, &h, sizeof(h));
+    } else {
+      (void)cudaGetLastError();  // same-process peers still work through the raw address
+    }
+    out->slot_bytes = c.slot_bytes;
+    out->fingerprint = c.fingerprint();
+    out->layers = static_cast<uint32_t>(c.L);
+    out->task_idx = task_idx;
+    for (int l = 0; l < c.L; ++l) out->slot[l] = c.pool->slot_of(task_idx, static_cast<uint32_t>(l));
+  });
+}
+
+int hmi_gpu_import_task(hmi_gpu_ctx* dst, uint32_t task_idx, const hmi_task_export* ex,
+                        const float* adapter_f32, uint64_t* peer_bytes) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(dst != nullptr && ex != nullptr, HMI_CONFIG_ERROR, "null argument");
+    Ctx& c = dst->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    HMI_CHECK(task_idx < c.store.size(), HMI_CONFIG_ERROR, "task index exceeds max_tasks");
+    if (c.store[task_idx]) throw HmiError(HMI_CONFLICT_ERROR, "adapter set for task already registered");
+    HMI_CHECK(ex->fingerprint == c.fingerprint() && ex->layers == static_cast<uint32_t>(c.L) &&
+                  ex->slot_bytes == c.slot_bytes,
+              HMI_CONFIG_ERROR,
+              "exported adapter set does not match this engine's model / bottleneck / precision");
+    for (int l = 0; l < c.L; ++l)
+      HMI_CHECK(ex->slot[l] >= 0, HMI_CONFIG_ERROR, "export holds a non-resident layer");
+    const bool local = ex->pid == static_cast<int32_t>(getpid());
+    const uint8_t* base = nullptr;
+    if (local) {
+      base = reinterpret_cast<const uint8_t*>(ex->arena);
+      if (ex->device != c.device) {
+        int can = 0;
+        HMI_CUDA(cudaDeviceCanAccessPeer(&can, c.device, ex->device));
+        if (can) {
+          const cudaError_t e = cudaDeviceEnablePeerAccess(ex->device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) HMI_CUDA(e);
+          (void)cudaGetLastError();
+        }
+      }
+    } else {
+      const std::string key(reinterpret_cast<const char*>(ex->ipc_handle), sizeof(ex->ipc_handle));
+      auto it = c.ipc_open.find(key);
+      if (it == c.ipc_open.end()) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, ex->ipc_handle, sizeof(h));
+        void* p = nullptr;
+        HMI_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        it = c.ipc_open.emplace(key, p).first;
+      }
+      base = static_cast<const uint8_t*>(it->second);
+    }
+    c.reap(true);
+    uint8_t* p = c.store_alloc();
+    c.store[task_idx] = p;
+    c.pool->set_task(task_idx, static_cast<uint32_t>(c.L), c.ref_layer_bytes);
+    try {
+      auto recs = c.pool->ensure_resident({task_idx});
+      uint64_t moved = 0;
+      for (const PoolRecord& rec : recs) {
+        for (const PoolLoad& ld : rec.loads) {
+          uint8_t* to = c.arena.p + size_t(ld.slot) * c.slot_bytes;
+          const uint8_t* from = base + size_t(ex->slot[ld.layer]) * c.slot_bytes;
+          if (local) {
+            HMI_CUDA(cudaMemcpyPeerAsync(to, c.device, from, ex->device, c.slot_bytes, c.copy));
+          } else {
+            HMI_CUDA(cudaMemcpyAsync(to, from, c.slot_bytes, cudaMemcpyDefault, c.copy));
+          }
+          moved += c.slot_bytes;
+        }
+      }
+      HMI_CUDA(cudaStreamSynchronize(c.copy));
+      write_slot_entries(c, recs);
+      if (adapter_f32) {
+        c.convert_adapter(adapter_f32, p);
+      } else {
+        // the host copy (for later refills after eviction) is the slot image itself
+        for (int l = 0; l < c.L; ++l)
+          HMI_CUDA(cudaMemcpy(p + size_t(l) * c.slot_bytes,
+                              c.arena.p + size_t(c.pool->slot_of(task_idx, l)) * c.slot_bytes,
+                              c.slot_bytes, cudaMemcpyDeviceToHost));
+      }
+      c.peer_bytes += moved;
+      if (peer_bytes) *peer_bytes = moved;
+    } catch (...) {
+      std::vector<PoolFree> freed;
+      c.pool->remove_task(task_idx, &freed);
+      for (const PoolFree& fr : freed) {
+        const int32_t minus1 = -1;
+        cudaMemcpy(c.d_slot_of.p + size_t(fr.task) * c.L + fr.layer, &minus1, 4, cudaMemcpyHostToDevice);
+      }
+      c.free_blocks.push_back(p);
+      c.store[task_idx] = nullptr;
+      throw;
+    }
+  });
+}
+
+int hmi_gpu_release_export(hmi_gpu_ctx* src, uint32_t task_idx, int drop) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(src != nullptr, HMI_CONFIG_ERROR, "null context");
+    Ctx& c = src->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    auto it = c.exported.find(task_idx);
+    if (it == c.exported.end()) throw HmiError(HMI_ROUTING_ERROR, "task is not exported");
+    c.pool->unpin({task_idx});
+    if (--it->second == 0) c.exported.erase(it);
+    if (drop) {
+      HMI_CHECK(!c.exported.count(task_idx), HMI_CONFLICT_ERROR,
+                "task is still exported to another peer engine");
+      c.reap(true);
+      evict_task_slots(c, task_idx, true);
+      c.free_blocks.push_back(c.store[task_idx]);
+      c.store[task_idx] = nullptr;
+    }
   });
 }
 

@@ -118,6 +118,40 @@ class GpuEngine:
     def unregister_task(self, task: int) -> None:
         check(_native.lib().hmi_gpu_unregister_task(self.h, task))
 
+    # ---- peer rebalancing of tenants' adapters
+    def export_task(self, task: int) -> bytes:
+        """Pins every layer of ``task`` resident in this engine's HBM slot pool and returns the
+        hmi_task_export record (bytes: it crosses processes as-is) until release_export."""
+        ex = _native.TaskExport()
+        check(_native.lib().hmi_gpu_export_task(self.h, task, ctypes.byref(ex)))
+        return bytes(ex)
+
+    def import_task(self, task: int, export: bytes, adapter_f32=None) -> int:
+        """Registers ``task`` here with its HBM slots copied device to device from the exporting
+        engine (same process: peer copy; another process: CUDA IPC). Returns the bytes moved."""
+        ex = _native.TaskExport.from_buffer_copy(export)
+        a = None if adapter_f32 is None else np.ascontiguousarray(adapter_f32, np.float32)
+        moved = ctypes.c_uint64(0)
+        check(_native.lib().hmi_gpu_import_task(self.h, task, ctypes.byref(ex),
+                                                None if a is None else _p(a, ctypes.c_float),
+                                                ctypes.byref(moved)))
+        return int(moved.value)
+
+    def release_export(self, task: int, drop: bool = False) -> None:
+        check(_native.lib().hmi_gpu_release_export(self.h, task, int(drop)))
+
+    def migrate_task(self, dst: "GpuEngine", task: int, keep_source: bool = False) -> int:
+        """Moves (or, keep_source=True, replicates) a task's adapter set to ``dst`` over the
+        device interconnect; the source keeps serving it until the import has landed."""
+        ex = self.export_task(task)
+        try:
+            moved = dst.import_task(task, ex)
+        except BaseException:
+            self.release_export(task, drop=False)
+            raise
+        self.release_export(task, drop=not keep_source)
+        return moved
+
     def register_head(self, head: int, kind: int, w, b) -> None:
         w = np.ascontiguousarray(w, np.float32)
         b = np.ascontiguousarray(b, np.float32)

@@ -196,18 +196,74 @@ class Server:
 
 class ShardRouter:
     """Tenant sharding across GPUs: task index t is owned by
-    rank t % world_size. split() keeps arrival order within each shard;
-    merge() restores the original order."""
+    rank t % world_size unless it was moved (peer rebalancing, §8(f) rank 3).
+    split() keeps arrival order within each shard; merge() restores the
+    original order."""
 
     def __init__(self, world_size: int):
         self.world_size = world_size
+        self.moved: dict[int, int] = {}
 
     def owner(self, task_idx: int) -> int:
-        return int(task_idx) % self.world_size
+        t = int(task_idx)
+        return self.moved.get(t, t % self.world_size)
+
+    def owners(self, task_of_request) -> np.ndarray:
+        t = np.asarray(task_of_request).astype(np.int64)
+        o = t % self.world_size
+        if self.moved:
+            keys = np.fromiter(self.moved.keys(), np.int64, len(self.moved))
+            vals = np.fromiter(self.moved.values(), np.int64, len(self.moved))
+            order = np.argsort(keys)
+            keys, vals = keys[order], vals[order]
+            pos = np.minimum(np.searchsorted(keys, t), len(keys) - 1)
+            hit = keys[pos] == t
+            o[hit] = vals[pos[hit]]
+        return o
 
     def split(self, task_of_request) -> list[np.ndarray]:
-        t = np.asarray(task_of_request)
-        return [np.nonzero(t % self.world_size == r)[0] for r in range(self.world_size)]
+        o = self.owners(task_of_request)
+        return [np.nonzero(o == r)[0] for r in range(self.world_size)]
+
+    def move(self, task_idx: int, rank: int) -> None:
+        if not 0 <= rank < self.world_size:
+            raise ValueError(f"rank {rank} outside [0, {self.world_size})")
+        t = int(task_idx)
+        if rank == t % self.world_size:
+            self.moved.pop(t, None)
+        else:
+            self.moved[t] = int(rank)
+
+    def plan_rebalance(self, load, tolerance: float = 0.1, max_moves: int = 64):
+        """Greedy migration plan from per-task load (requests per task index over a window,
+        identical on every rank, e.g. all-reduced): while the busiest rank exceeds the idlest by
+        more than ``tolerance`` x the mean rank load, move the busiest rank's heaviest task whose
+        load is at most half the gap (so the move never overshoots). Deterministic: ties break on
+        the lower task index. Returns [(task, src_rank, dst_rank)]; apply with move() once the
+        adapters have been migrated (GpuEngine.migrate_task / export_task + import_task)."""
+        load = np.asarray(load, np.float64)
+        tasks = np.nonzero(load > 0)[0]
+        owner = {int(t): self.owner(int(t)) for t in tasks}
+        rank_load = np.zeros(self.world_size)
+        for t in tasks:
+            rank_load[owner[int(t)]] += load[t]
+        mean = rank_load.sum() / self.world_size
+        plan = []
+        while len(plan) < max_moves and mean > 0:
+            hi = int(np.argmax(rank_load))
+            lo = int(np.argmin(rank_load))
+            gap = rank_load[hi] - rank_load[lo]
+            if gap <= tolerance * mean:
+                break
+            cand = [(-load[t], int(t)) for t in tasks if owner[int(t)] == hi and load[t] <= gap / 2]
+            if not cand:
+                break
+            _, t = min(cand)
+            owner[t] = lo
+            rank_load[hi] -= load[t]
+            rank_load[lo] += load[t]
+            plan.append((t, hi, lo))
+        return plan
 
     def merge(self, parts: list[np.ndarray], values: list[np.ndarray], n: int):
         first = next(v for v in values if len(v))
