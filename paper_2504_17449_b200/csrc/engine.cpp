@@ -279,6 +279,8 @@ struct Ctx {
   // peer rebalancing: export pins per task, peer arenas opened over CUDA IPC, bytes moved
   std::map<uint32_t, int> exported;
   std::map<std::string, void*> ipc_open;
+  int ipc_state = 0;  // 0 not asked yet, 1 handle valid, -1 arena not exportable
+  cudaIpcMemHandle_t ipc_handle{};
   uint64_t peer_bytes = 0;
   uint64_t fingerprint() const {
     uint64_t h = 0xcbf29ce484222325ULL;
@@ -1639,9 +1641,12 @@ static void evict_task_slots(Ctx& c, uint32_t task, bool remove) {
   } else {
     c.pool->evict(task, &freed);
   }
-  for (const PoolFree& fr : freed) {
-    const int32_t minus1 = -1;
-    HMI_CUDA(cudaMemcpy(c.d_slot_of.p + static_cast<size_t>(fr.task) * c.L + fr.layer, &minus1, 4,
+  // the freed entries are all of one task's row: one write of L entries
+  if (!freed.empty()) {
+    std::vector<int32_t> row(c.L);
+    for (int l = 0; l < c.L; ++l) row[l] = remove ? -1 : c.pool->slot_of(task, static_cast<uint32_t>(l));
+    for (const PoolFree& fr : freed) row[fr.layer] = -1;
+    HMI_CUDA(cudaMemcpy(c.d_slot_of.p + static_cast<size_t>(task) * c.L, row.data(), 4 * c.L,
                         cudaMemcpyHostToDevice));
   }
 }
@@ -1681,13 +1686,17 @@ int hmi_gpu_unregister_task(hmi_gpu_ctx* ctx, uint32_t task_idx) {
 // evictions and loads are written directly; the batch path ships the same entries as deltas.
 static void write_slot_entries(hmi_b200::Ctx& c, const std::vector<hmi_b200::PoolRecord>& recs) {
   using namespace hmi_b200;
-  std::vector<std::pair<size_t, int32_t>> w;
+  std::set<uint32_t> touched;
   for (const PoolRecord& rec : recs) {
-    for (const PoolFree& fr : rec.freed) w.push_back({size_t(fr.task) * c.L + fr.layer, -1});
-    for (const PoolLoad& ld : rec.loads) w.push_back({size_t(rec.task) * c.L + ld.layer, ld.slot});
+    for (const PoolFree& fr : rec.freed) touched.insert(fr.task);
+    if (!rec.loads.empty()) touched.insert(rec.task);
   }
-  for (const auto& [i, v] : w)
-    HMI_CUDA(cudaMemcpy(c.d_slot_of.p + i, &v, 4, cudaMemcpyHostToDevice));
+  // one row of L entries per touched task (rows are contiguous in the slot table)
+  std::vector<int32_t> row(c.L);
+  for (uint32_t t : touched) {
+    for (int l = 0; l < c.L; ++l) row[l] = c.pool->slot_of(t, static_cast<uint32_t>(l));
+    HMI_CUDA(cudaMemcpy(c.d_slot_of.p + size_t(t) * c.L, row.data(), 4 * c.L, cudaMemcpyHostToDevice));
+  }
 }
 
 int hmi_gpu_export_task(hmi_gpu_ctx* src, uint32_t task_idx, hmi_task_export* out) {
@@ -1720,13 +1729,12 @@ int hmi_gpu_export_task(hmi_gpu_ctx* src, uint32_t task_idx, hmi_task_export* ou
     out->device = c.device;
     out->pid = static_cast<int32_t>(getpid());
     out->arena = reinterpret_cast<uint64_t>(c.arena.p);
-    cudaIpcMemHandle_t h;
-    if (cudaIpcGetMemHandle(&h, c.arena.p) == cudaSuccess) {
-      static_assert(sizeof(h) == sizeof(out->ipc_handle), "IPC handle size");
-      std::memcpy(out->ipc_handle, &h, sizeof(h));
-    } else {
-      (void)cudaGetLastError();  // same-process peers still work through the raw address
+    if (c.ipc_state == 0) {
+      c.ipc_state = cudaIpcGetMemHandle(&c.ipc_handle, c.arena.p) == cudaSuccess ? 1 : -1;
+      (void)cudaGetLastError();  // not exportable: same-process peers still use the raw address
     }
+    static_assert(sizeof(c.ipc_handle) == sizeof(out->ipc_handle), "IPC handle size");
+    if (c.ipc_state == 1) std::memcpy(out->ipc_handle, &c.ipc_handle, sizeof(c.ipc_handle));
     out->slot_bytes = c.slot_bytes;
     out->fingerprint = c.fingerprint();
     out->layers = static_cast<uint32_t>(c.L);
@@ -1802,9 +1810,10 @@ int hmi_gpu_import_task(hmi_gpu_ctx* dst, uint32_t task_idx, const hmi_task_expo
       } else {
         // the host copy (for later refills after eviction) is the slot image itself
         for (int l = 0; l < c.L; ++l)
-          HMI_CUDA(cudaMemcpy(p + size_t(l) * c.slot_bytes,
-                              c.arena.p + size_t(c.pool->slot_of(task_idx, l)) * c.slot_bytes,
-                              c.slot_bytes, cudaMemcpyDeviceToHost));
+          HMI_CUDA(cudaMemcpyAsync(p + size_t(l) * c.slot_bytes,
+                                   c.arena.p + size_t(c.pool->slot_of(task_idx, l)) * c.slot_bytes,
+                                   c.slot_bytes, cudaMemcpyDeviceToHost, c.copy));
+        HMI_CUDA(cudaStreamSynchronize(c.copy));
       }
       c.peer_bytes += moved;
       if (peer_bytes) *peer_bytes = moved;
