@@ -81,6 +81,11 @@ class GpuEngine:
         self._pending: dict[int, int] = {}
         self.max_batch = max_batch
         self.max_seq = max_seq
+        self.bottleneck = bottleneck
+        self.max_tasks = max_tasks
+        self.max_instances = max_instances or max_tasks
+        self.max_heads = max_heads or max_tasks
+        self.max_versions = max_versions
         opts = Options(precision, max_batch, max_seq, bottleneck, max_labels, pipeline_mode,
                        pool_bytes, max_tasks, max_instances or max_tasks, max_heads or max_tasks,
                        max_versions, max_new_tokens, 0)

@@ -120,6 +120,17 @@ def load_adp1(path: str):
     return name.value.decode(), body
 
 
+def save_adp1(path: str, task_id: str, body, d: int, r: int) -> None:
+    """ADP1 writer (adapter_set.cpp:27-46): magic, task id, layers, d, r, f32 body."""
+    body = np.ascontiguousarray(body, np.float32).reshape(-1, 2 * d * r + r + d)
+    name = task_id.encode()
+    with open(path, "wb") as f:
+        f.write(b"ADP1" + len(name).to_bytes(4, "little") + name)
+        for v in (body.shape[0], d, r):
+            f.write(int(v).to_bytes(4, "little"))
+        f.write(body.tobytes())
+
+
 def load_hmi1(path: str):
     """An HMI1 model (model_io.cpp:83-115) -> (ModelConfig, token_emb, pos_emb, lower, higher)."""
     L = _native.lib()

@@ -150,12 +150,15 @@ class Server:
     InferResults in batch order and request order."""
 
     def __init__(self, backend, registry: Registry, max_batch_size: int, max_seq: int,
-                 head_kinds: dict[int, int] | None = None):
+                 head_kinds: dict[int, int] | None = None, manager=None):
         self.backend = backend
         self.registry = registry
         self.queue = BatchQueue(max_batch_size)
         self.max_seq = max_seq
         self.head_kinds = head_kinds or {}
+        # manage.Manager: its queued mutations are applied between batches, never inside one
+        self.manager = manager
+        self.rejected: list[tuple[str, str]] = []  # (request_id, reason): queue conservation
 
     def enqueue(self, req: InferRequest) -> int:
         self.registry.instance_index(req.instance_id)  # unknown instance -> RoutingError
@@ -168,6 +171,17 @@ class Server:
     def run(self) -> list[InferResult]:
         results = []
         for batch in self.queue.take_all():
+            if self.manager is not None:
+                self.manager.apply_pending()
+                kept = []
+                for r in batch.requests:  # instances deleted since enqueue are rejected
+                    if r.instance_id in self.registry.bindings:
+                        kept.append(r)
+                    else:
+                        self.rejected.append((r.request_id, f"instance {r.instance_id} is not bound"))
+                batch = InferBatch(batch.batch_id, kept)
+                if not kept:
+                    continue
             t_deq = time.perf_counter() * 1e3
             n = len(batch.requests)
             stride = max(len(r.tokens) for r in batch.requests)
