@@ -331,6 +331,13 @@ int hmi_model_load(const char* path, hmi_model_config* cfg, float* token_emb, fl
 /* VersionTree::add_branch from a table handle (e.g. a loaded PLT1, or a GPU-built table) */
 int hmi_gpu_upload_plot_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t parent_id,
                               const hmi_plot_table* t);
+/* Streaming PLT1 ingest (plot_io.cpp:35-72): VersionTree::add_branch straight from a file.
+ * Chunks are read into pinned memory and shipped whole; a kernel moves each entry's rep rows
+ * into the reps arena while the host reads the next chunk (the host parses headers only).
+ * Same checks and fail-closed commit as hmi_gpu_upload_table; ngram / d must match the model
+ * (DIMENSION). *version_id / *parent_id (nullable) return the header's ids.                   */
+int hmi_gpu_upload_plt1(hmi_gpu_ctx* ctx, const char* path, uint32_t* version_id,
+                        uint32_t* parent_id);
 /* AdapterStore::register_set from an ADP1 file (dimensions checked against the context) */
 int hmi_gpu_register_task_file(hmi_gpu_ctx* ctx, uint32_t task_idx, const char* adp1_path);
 int hmi_gpu_check_adapter_dims(hmi_gpu_ctx* ctx, uint32_t layers, uint32_t d, uint32_t r);

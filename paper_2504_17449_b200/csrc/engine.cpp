@@ -40,6 +40,7 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -1532,6 +1533,122 @@ int hmi_gpu_destroy(hmi_gpu_ctx* ctx) {
   return HMI_OK;
 }
 
+namespace hmi_b200 {
+// VersionTree::add_branch checks (version_tree.cpp): free id, existing parent, one root, depth.
+static void check_new_version(Ctx& c, uint32_t version_id, uint32_t parent_id) {
+  HMI_CHECK(version_id < c.h_parent.size(), HMI_CONFIG_ERROR, "version id exceeds max_versions");
+  if (c.h_parent[version_id] != -2) throw HmiError(HMI_CONFLICT_ERROR, "version already exists");
+  if (parent_id != kNoParent) {
+    if (parent_id >= c.h_parent.size() || c.h_parent[parent_id] == -2)
+      throw HmiError(HMI_ROUTING_ERROR, "branch parent version " + std::to_string(parent_id) +
+                                            " does not exist");
+    int depth = 2;  // device retrieval resolves chains of up to 8 tables
+    for (int32_t v = c.h_parent[parent_id]; v >= 0; v = c.h_parent[v]) ++depth;
+    HMI_CHECK(depth <= 8, HMI_CONFIG_ERROR, "version tree deeper than 8 levels");
+  } else {
+    for (int32_t p : c.h_parent)
+      if (p == -1) throw HmiError(HMI_CONFLICT_ERROR, "a root table is already registered");
+  }
+}
+
+// Keys of one version into a copy of the host hash (fail-closed on duplicates); returns it with
+// the hash grown to keep load <= 0.5. Rows are numbered from c.rep_rows on.
+static std::vector<PlotSlot> stage_keys(Ctx& c, uint32_t version_id, uint32_t n_entries,
+                                        const uint32_t* key_len, const uint32_t* keys,
+                                        uint64_t* rows_out) {
+  const uint32_t n = static_cast<uint32_t>(c.ngram);
+  uint64_t rows = 0;
+  for (uint32_t e = 0; e < n_entries; ++e) {
+    if (key_len[e] == 0 || key_len[e] > n)
+      throw HmiError(HMI_FORMAT_ERROR, "entry key length outside [1, n]");
+    for (uint32_t j = 0; j < key_len[e]; ++j)
+      if (keys[static_cast<size_t>(e) * n + j] >= c.cfg.vocab_size)
+        throw HmiError(HMI_VOCABULARY_ERROR, "key token outside vocabulary");
+    rows += key_len[e];
+  }
+  uint64_t need = c.n_keys + n_entries;
+  if (need * 2 > c.h_slots.size()) {
+    uint64_t cap = c.h_slots.size();
+    while (need * 2 > cap) cap <<= 1;
+    std::vector<PlotSlot> old;
+    old.swap(c.h_slots);
+    c.h_slots.assign(cap, PlotSlot{kEmptyKey, 0, {0, 0, 0, 0, 0}, 0});
+    for (const PlotSlot& s : old) {
+      if (s.version == kEmptyKey) continue;
+      uint64_t i = plot_hash(s.version, s.len, s.tok) & (cap - 1);
+      while (c.h_slots[i].version != kEmptyKey) i = (i + 1) & (cap - 1);
+      c.h_slots[i] = s;
+    }
+  }
+  std::vector<PlotSlot> staged(c.h_slots);
+  const uint64_t mask = staged.size() - 1;
+  uint64_t row = c.rep_rows;
+  for (uint32_t e = 0; e < n_entries; ++e) {
+    PlotSlot s{version_id, key_len[e], {0, 0, 0, 0, 0}, static_cast<uint32_t>(row)};
+    for (uint32_t j = 0; j < key_len[e]; ++j) s.tok[j] = keys[static_cast<size_t>(e) * n + j];
+    uint64_t i = plot_hash(s.version, s.len, s.tok) & mask;
+    for (;; i = (i + 1) & mask) {
+      const PlotSlot& o = staged[i];
+      if (o.version == kEmptyKey) break;
+      if (o.version == s.version && o.len == s.len &&
+          std::memcmp(o.tok, s.tok, sizeof(uint32_t) * s.len) == 0)
+        throw HmiError(HMI_FORMAT_ERROR, "duplicate entry key");
+    }
+    staged[i] = s;
+    row += key_len[e];
+  }
+  HMI_CHECK(row < (1ull << 31), HMI_CAPACITY_ERROR, "PLOT row count exceeds 2^31");
+  *rows_out = rows;
+  return staged;
+}
+
+// pread of [off, off + n) into dst by up to 4 threads; returns the bytes read.
+static size_t read_parallel(int fd, uint8_t* dst, size_t n, uint64_t off) {
+  if (n == 0) return 0;
+  const int parts = n >= (size_t(8) << 20) ? 4 : 1;
+  const size_t step = (n + parts - 1) / parts;
+  size_t got[4] = {0, 0, 0, 0};
+  auto work = [&](int i) {
+    const size_t a = i * step, b = std::min(n, a + step);
+    size_t done = 0;
+    while (a + done < b) {
+      const ssize_t r = pread(fd, dst + a + done, b - a - done, static_cast<off_t>(off + a + done));
+      if (r <= 0) break;
+      done += static_cast<size_t>(r);
+    }
+    got[i] = done;
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < parts; ++i) th.emplace_back(work, i);
+  work(0);
+  for (auto& t : th) t.join();
+  size_t total = 0;
+  for (int i = 0; i < parts; ++i) total += got[i];
+  return total;
+}
+
+// The reps arena holds at least `rows` rows (appending, growing geometrically).
+static void reserve_rep_rows(Ctx& c, uint64_t rows) {
+  const size_t need_f = static_cast<size_t>(rows) * c.d;
+  if (need_f <= c.d_reps.n) return;
+  DevBuf<float> grown;
+  grown.alloc(std::max(need_f, c.d_reps.n * 3 / 2 + 1));
+  if (c.rep_rows) HMI_CUDA(cudaMemcpy(grown.p, c.d_reps.p, c.rep_rows * c.d * 4, cudaMemcpyDeviceToDevice));
+  c.d_reps.free();
+  c.d_reps = grown;
+  grown.p = nullptr;
+}
+
+static void commit_version(Ctx& c, uint32_t version_id, uint32_t parent_id, uint32_t n_entries,
+                           uint64_t rows, std::vector<PlotSlot>& staged) {
+  c.h_slots.swap(staged);
+  c.n_keys += n_entries;
+  c.rep_rows += rows;
+  c.h_parent[version_id] = parent_id == kNoParent ? -1 : static_cast<int32_t>(parent_id);
+  c.upload_plot_hash();
+}
+}  // namespace hmi_b200
+
 int hmi_gpu_upload_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t parent_id,
                          uint32_t n_entries, const uint32_t* key_len, const uint32_t* keys,
                          const float* reps) {
@@ -1541,81 +1658,188 @@ int hmi_gpu_upload_table(hmi_gpu_ctx* ctx, uint32_t version_id, uint32_t parent_
     std::lock_guard<std::mutex> lock(c.mu);
     HMI_CUDA(cudaSetDevice(c.device));
     c.reap(true);
-    HMI_CHECK(version_id < c.h_parent.size(), HMI_CONFIG_ERROR, "version id exceeds max_versions");
-    if (c.h_parent[version_id] != -2) throw HmiError(HMI_CONFLICT_ERROR, "version already exists");
-    if (parent_id != kNoParent) {
-      if (parent_id >= c.h_parent.size() || c.h_parent[parent_id] == -2)
-        throw HmiError(HMI_ROUTING_ERROR, "branch parent version " + std::to_string(parent_id) +
-                                              " does not exist");
-    } else {
-      for (int32_t p : c.h_parent)
-        if (p == -1) throw HmiError(HMI_CONFLICT_ERROR, "a root table is already registered");
-    }
-    if (parent_id != kNoParent) {  // device retrieval resolves chains of up to 8 tables
-      int depth = 2;
-      for (int32_t v = c.h_parent[parent_id]; v >= 0; v = c.h_parent[v]) ++depth;
-      HMI_CHECK(depth <= 8, HMI_CONFIG_ERROR, "version tree deeper than 8 levels");
-    }
-    const uint32_t n = static_cast<uint32_t>(c.ngram);
+    check_new_version(c, version_id, parent_id);
     uint64_t rows = 0;
-    for (uint32_t e = 0; e < n_entries; ++e) {
-      if (key_len[e] == 0 || key_len[e] > n)
-        throw HmiError(HMI_FORMAT_ERROR, "entry key length outside [1, n]");
-      for (uint32_t j = 0; j < key_len[e]; ++j)
-        if (keys[static_cast<size_t>(e) * n + j] >= c.cfg.vocab_size)
-          throw HmiError(HMI_VOCABULARY_ERROR, "key token outside vocabulary");
-      rows += key_len[e];
-    }
-    // grow the hash to keep load <= 0.5, then insert
-    uint64_t need = c.n_keys + n_entries;
-    if (need * 2 > c.h_slots.size()) {
-      uint64_t cap = c.h_slots.size();
-      while (need * 2 > cap) cap <<= 1;
-      std::vector<PlotSlot> old;
-      old.swap(c.h_slots);
-      c.h_slots.assign(cap, PlotSlot{kEmptyKey, 0, {0, 0, 0, 0, 0}, 0});
-      for (const PlotSlot& s : old) {
-        if (s.version == kEmptyKey) continue;
-        uint64_t i = plot_hash(s.version, s.len, s.tok) & (cap - 1);
-        while (c.h_slots[i].version != kEmptyKey) i = (i + 1) & (cap - 1);
-        c.h_slots[i] = s;
-      }
-    }
-    std::vector<PlotSlot> staged(c.h_slots);  // insert into a copy: fail-closed on duplicates
-    const uint64_t mask = staged.size() - 1;
-    uint64_t row = c.rep_rows;
-    for (uint32_t e = 0; e < n_entries; ++e) {
-      PlotSlot s{version_id, key_len[e], {0, 0, 0, 0, 0}, static_cast<uint32_t>(row)};
-      for (uint32_t j = 0; j < key_len[e]; ++j) s.tok[j] = keys[static_cast<size_t>(e) * n + j];
-      uint64_t i = plot_hash(s.version, s.len, s.tok) & mask;
-      for (;; i = (i + 1) & mask) {
-        const PlotSlot& o = staged[i];
-        if (o.version == kEmptyKey) break;
-        if (o.version == s.version && o.len == s.len &&
-            std::memcmp(o.tok, s.tok, sizeof(uint32_t) * s.len) == 0)
-          throw HmiError(HMI_FORMAT_ERROR, "duplicate entry key");
-      }
-      staged[i] = s;
-      row += key_len[e];
-    }
-    HMI_CHECK(row < (1ull << 31), HMI_CAPACITY_ERROR, "PLOT row count exceeds 2^31");
-    // reps arena (append, growing geometrically)
-    const size_t need_f = static_cast<size_t>(row) * c.d;
-    if (need_f > c.d_reps.n) {
-      DevBuf<float> grown;
-      grown.alloc(std::max(need_f, c.d_reps.n * 3 / 2 + 1));
-      if (c.rep_rows) HMI_CUDA(cudaMemcpy(grown.p, c.d_reps.p, c.rep_rows * c.d * 4, cudaMemcpyDeviceToDevice));
-      c.d_reps.free();
-      c.d_reps = grown;
-      grown.p = nullptr;
-    }
+    auto staged = stage_keys(c, version_id, n_entries, key_len, keys, &rows);
+    reserve_rep_rows(c, c.rep_rows + rows);
     if (rows)
       HMI_CUDA(cudaMemcpy(c.d_reps.p + c.rep_rows * c.d, reps, rows * c.d * 4, cudaMemcpyHostToDevice));
-    c.h_slots.swap(staged);
-    c.n_keys += n_entries;
-    c.rep_rows = row;
-    c.h_parent[version_id] = parent_id == kNoParent ? -1 : static_cast<int32_t>(parent_id);
-    c.upload_plot_hash();
+    commit_version(c, version_id, parent_id, n_entries, rows, staged);
+  });
+}
+
+// Streaming PLT1 ingest (plot_io.cpp:35-72 format): the file is read in chunks straight into
+// pinned memory and each chunk goes to the GPU whole; a kernel moves the entries' rep rows out
+// of the raw chunk into the reps arena while the host reads the next chunk. The host touches
+// only the entry headers; validation and fail-closed commit as hmi_gpu_upload_table.
+int hmi_gpu_upload_plt1(hmi_gpu_ctx* ctx, const char* path, uint32_t* version_out,
+                        uint32_t* parent_out) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(ctx != nullptr && path != nullptr, HMI_CONFIG_ERROR, "null argument");
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw HmiError(HMI_FORMAT_ERROR, std::string("cannot open ") + path + " (offset 0)");
+    struct Closer {
+      FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    std::fseek(f, 0, SEEK_END);
+    const uint64_t file_size = static_cast<uint64_t>(std::max<long>(0, std::ftell(f)));
+    std::fseek(f, 0, SEEK_SET);
+    auto fail = [](const std::string& what, uint64_t at) {
+      throw HmiError(HMI_FORMAT_ERROR, what + " (offset " + std::to_string(at) + ")");
+    };
+    // header (small, plain reads)
+    uint64_t off = 0;
+    auto rd = [&](void* p, size_t n) {
+      if (off + n > file_size || std::fread(p, 1, n, f) != n) fail("unexpected end of file", off);
+      off += n;
+    };
+    char magic[4];
+    rd(magic, 4);
+    if (std::memcmp(magic, "PLT1", 4) != 0) fail("bad magic, expected PLT1", 0);
+    uint32_t version = 0, parent = 0, label_len = 0, ngram = 0, d = 0, count = 0, alpha = 0;
+    rd(&version, 4);
+    rd(&parent, 4);
+    const uint64_t label_at = off;
+    rd(&label_len, 4);
+    if (label_len > (1u << 20)) fail("string length " + std::to_string(label_len) + " implausible", label_at);
+    std::vector<char> label(label_len);
+    if (label_len) rd(label.data(), label_len);
+    rd(&ngram, 4);
+    rd(&d, 4);
+    rd(&count, 4);
+    rd(&alpha, 4);
+    if (ngram == 0 || d == 0) fail("table header has zero ngram or hidden size", off);
+    HMI_CHECK(ngram == static_cast<uint32_t>(c.ngram) && d == static_cast<uint32_t>(c.d),
+              HMI_DIMENSION_ERROR, "PLT1 table (ngram " + std::to_string(ngram) + ", d " +
+                                       std::to_string(d) + ") does not match the model");
+    check_new_version(c, version, parent);
+    const bool dbg = std::getenv("HMI_DEBUG_INGEST") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::milli>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t_a = now(), t_read = 0, t_parse = 0, t_wait = 0;
+    // rows are bounded by the payload size: reserve once, stream into [rep_rows, ...)
+    const uint64_t row_bytes = static_cast<uint64_t>(d) * 4;
+    reserve_rep_rows(c, c.rep_rows + (file_size - off) / row_bytes + 1);
+    float* dst_base = c.d_reps.p + c.rep_rows * c.d;
+
+    const size_t kChunk = size_t(64) << 20;
+    const size_t max_entry = 4 + 4 * ngram + 8 + ngram * row_bytes;
+    HMI_CHECK(max_entry <= kChunk, HMI_CONFIG_ERROR, "PLT1 entry larger than the ingest chunk");
+    struct Slot {
+      uint8_t* host = nullptr;
+      int4* segs_h = nullptr;  // {src byte offset in chunk, dst row (low), dst row (high), rows}
+      uint8_t* dev = nullptr;
+      int4* segs_d = nullptr;
+      cudaEvent_t done = nullptr;
+      size_t seg_cap = 0;
+    } slot[2];
+    struct Freer {
+      Slot* s;
+      ~Freer() {
+        for (int i = 0; i < 2; ++i) {
+          if (s[i].done) cudaEventSynchronize(s[i].done), cudaEventDestroy(s[i].done);
+          if (s[i].host) cudaFreeHost(s[i].host);
+          if (s[i].segs_h) cudaFreeHost(s[i].segs_h);
+          if (s[i].dev) cudaFree(s[i].dev);
+          if (s[i].segs_d) cudaFree(s[i].segs_d);
+        }
+      }
+    } freer{slot};
+    for (auto& sl : slot) {
+      sl.seg_cap = kChunk / (4 + 8 + row_bytes) + 1;
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.host), kChunk, cudaHostAllocDefault));
+      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.segs_h), sl.seg_cap * sizeof(int4), cudaHostAllocDefault));
+      HMI_CUDA(cudaMalloc(reinterpret_cast<void**>(&sl.dev), kChunk));
+      HMI_CUDA(cudaMalloc(reinterpret_cast<void**>(&sl.segs_d), sl.seg_cap * sizeof(int4)));
+      HMI_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
+    const double t_alloc = now() - t_a;
+    std::vector<uint32_t> key_len;
+    std::vector<uint32_t> keys;
+    key_len.reserve(count);
+    keys.reserve(static_cast<size_t>(count) * ngram);
+    uint64_t row = 0;       // rows streamed so far (relative to rep_rows)
+    uint32_t entries = 0;
+    size_t carry = 0;       // bytes of a partial entry carried to the next chunk
+    uint64_t chunk_at = off; // file offset of the current chunk's first byte
+    int k = 0;
+    const uint8_t* prev = nullptr;
+    while (entries < count) {
+      Slot& sl = slot[k];
+      double t0 = now();
+      HMI_CUDA(cudaEventSynchronize(sl.done));  // the GPU is done with this slot's last chunk
+      t_wait += now() - t0;
+      t0 = now();
+      if (carry) std::memmove(sl.host, prev, carry);
+      const size_t want = std::min<uint64_t>(kChunk - carry, file_size - (chunk_at + carry));
+      // page-cache copies are bound by one core's memcpy: read the chunk's quarters in parallel
+      const size_t got = read_parallel(fileno(f), sl.host + carry, want, chunk_at + carry);
+      if (got != want) fail("read failed", chunk_at + carry);
+      t_read += now() - t0;
+      t0 = now();
+      const size_t avail = carry + got;
+      if (avail == 0) fail("unexpected end of file", chunk_at);
+      size_t p = 0;
+      size_t nseg = 0;
+      while (entries < count) {
+        if (p + 4 > avail) break;
+        uint32_t kl;
+        std::memcpy(&kl, sl.host + p, 4);
+        if (kl == 0 || kl > ngram)
+          fail("entry key length " + std::to_string(kl) + " outside [1, " + std::to_string(ngram) + "]", chunk_at + p);
+        const size_t need = 4 + 4 * size_t(kl) + 8 + kl * row_bytes;
+        if (p + need > avail) break;
+        uint64_t fr;
+        std::memcpy(&fr, sl.host + p + 4 + 4 * kl, 8);
+        if (fr == 0) fail("entry frequency must be >= 1", chunk_at + p);
+        key_len.push_back(kl);
+        const uint32_t* kp = reinterpret_cast<const uint32_t*>(sl.host + p + 4);
+        for (uint32_t j = 0; j < ngram; ++j) keys.push_back(j < kl ? kp[j] : 0);
+        sl.segs_h[nseg++] = make_int4(static_cast<int>(p + 4 + 4 * kl + 8),
+                                      static_cast<int>(row & 0x7fffffff), static_cast<int>(row >> 31),
+                                      static_cast<int>(kl));
+        row += kl;
+        ++entries;
+        p += need;
+      }
+      if (p == 0 && entries < count) {
+        if (avail < kChunk && chunk_at + avail >= file_size) fail("unexpected end of file", chunk_at + avail);
+        fail("PLT1 entry larger than the ingest chunk", chunk_at);
+      }
+      t_parse += now() - t0;
+      if (nseg) {
+        HMI_CUDA(cudaMemcpyAsync(sl.dev, sl.host, p, cudaMemcpyHostToDevice, c.copy));
+        HMI_CUDA(cudaMemcpyAsync(sl.segs_d, sl.segs_h, nseg * sizeof(int4), cudaMemcpyHostToDevice, c.copy));
+        launch_scatter_rows(sl.dev, sl.segs_d, static_cast<int>(nseg), dst_base, static_cast<int>(d), c.copy);
+        HMI_CUDA(cudaEventRecord(sl.done, c.copy));
+      }
+      carry = avail - p;
+      prev = sl.host + p;
+      chunk_at += p;
+      k ^= 1;
+    }
+    if (chunk_at != file_size) fail("trailing bytes after payload", chunk_at);
+    double t0 = now();
+    HMI_CUDA(cudaStreamSynchronize(c.copy));
+    t_wait += now() - t0;
+    t0 = now();
+    // keys into the hash; duplicates / vocabulary as hmi_gpu_upload_table (the rows streamed
+    // above are only reachable once the hash is committed)
+    uint64_t rows = 0;
+    auto staged = stage_keys(c, version, count, key_len.data(), keys.data(), &rows);
+    HMI_CHECK(rows == row, HMI_SCHEDULING_BUG, "streamed row count mismatch");
+    commit_version(c, version, parent, count, rows, staged);
+    if (dbg)
+      std::fprintf(stderr, "[ingest] alloc+reserve %.1f ms, read %.1f, parse %.1f, gpu wait %.1f, hash+commit %.1f, total %.1f\n",
+                   t_alloc, t_read, t_parse, t_wait, now() - t0, now() - t_a);
+    if (version_out) *version_out = version;
+    if (parent_out) *parent_out = parent;
   });
 }
 

@@ -63,6 +63,11 @@ struct FetchArgs {
 };
 void launch_fetch_inputs(const FetchArgs& a, cudaStream_t stream);
 
+// Streaming PLT1 ingest: segment s = {byte offset of its rep rows in the raw chunk, dst row
+// (low 31 bits), dst row (high bits), rows}; copies rows x d f32 from the chunk to dst rows.
+void launch_scatter_rows(const uint8_t* chunk, const int4* segs, int n_seg, float* dst, int d,
+                         cudaStream_t stream);
+
 // K6: routing instance -> (version, task, head) and task -> per-layer HBM slot.
 void launch_route(const uint32_t* instance_idx, int n_req, const int32_t* inst_version,
                   const int32_t* inst_task, const int32_t* inst_head, int n_instances,

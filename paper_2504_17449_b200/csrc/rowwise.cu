@@ -631,6 +631,29 @@ void launch_fetch_inputs(const FetchArgs& a, cudaStream_t stream) {
   HMI_CUDA(cudaGetLastError());
 }
 
+// One warp per entry: its rows are contiguous f32 in the raw chunk (4-byte aligned: PLT1 entry
+// sizes are multiples of 4) and contiguous in the reps arena.
+__global__ void scatter_rows_kernel(const uint8_t* __restrict__ chunk, const int4* __restrict__ segs,
+                                    int n_seg, float* __restrict__ dst, int d) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = static_cast<int>(gridDim.x * blockDim.x >> 5);
+  for (int s = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); s < n_seg; s += nwarps) {
+    const int4 g = segs[s];
+    const float* in = reinterpret_cast<const float*>(chunk + g.x);
+    float* out = dst + ((static_cast<size_t>(g.y) | (static_cast<size_t>(g.z) << 31)) * d);
+    const int n = g.w * d;
+    for (int i = lane; i < n; i += 32) out[i] = in[i];
+  }
+}
+
+void launch_scatter_rows(const uint8_t* chunk, const int4* segs, int n_seg, float* dst, int d,
+                         cudaStream_t stream) {
+  if (n_seg <= 0) return;
+  const int blocks = std::min((n_seg + 7) / 8, 8 * device_sm_count());
+  scatter_rows_kernel<<<blocks, 256, 0, stream>>>(chunk, segs, n_seg, dst, d);
+  HMI_CUDA(cudaGetLastError());
+}
+
 void launch_apply_deltas(int32_t* table, const int32_t* pairs, int n, cudaStream_t stream) {
   if (n <= 0) return;
   apply_deltas_kernel<<<1, 32, 0, stream>>>(table, pairs, n);

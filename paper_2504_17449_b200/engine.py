@@ -200,11 +200,16 @@ class GpuEngine:
                               "evicted": [int(x) for x in ev[r.evicted_offset:r.evicted_offset + r.n_evicted]]})
         return BatchResult(scores, labels, tags, trace)
 
-    def upload_plt1(self, path: str) -> tuple[int, int]:
-        """VersionTree::add_branch from a PLT1 file (plot_io.cpp:35-72); (version, parent)."""
+    def upload_plt1(self, path: str, streamed: bool = True) -> tuple[int, int]:
+        """VersionTree::add_branch from a PLT1 file (plot_io.cpp:35-72); (version, parent).
+        streamed: chunked pinned reads shipped to the GPU whole, rows scattered on the device
+        (hmi_gpu_upload_plt1); else load the table on the host, then upload it."""
         L = _native.lib()
-        h = ctypes.c_void_p()
         v, p = ctypes.c_uint32(0), ctypes.c_uint32(0)
+        if streamed:
+            check(L.hmi_gpu_upload_plt1(self.h, path.encode(), ctypes.byref(v), ctypes.byref(p)))
+            return v.value, p.value
+        h = ctypes.c_void_p()
         check(L.hmi_plot_table_load(path.encode(), ctypes.byref(h), ctypes.byref(v), ctypes.byref(p),
                                     None))
         try:

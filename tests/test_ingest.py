@@ -223,3 +223,129 @@ def _write_adp1(path, task_id, body, d, r):
         f.write(len(task_id).to_bytes(4, "little") + task_id.encode())
         f.write(body.shape[0].to_bytes(4, "little") + d.to_bytes(4, "little") + r.to_bytes(4, "little"))
         f.write(np.ascontiguousarray(body, np.float32).tobytes())
+
+
+def _big_table(seed, n, d, vocab, ngram=3):
+    """n distinct keys of length 2..ngram with random f32 reps (a multi-chunk PLT1 at d=128)."""
+    rng = np.random.default_rng(seed)
+    kl = rng.integers(2, ngram + 1, n).astype(np.uint32)
+    keys = np.zeros((n, ngram), np.uint32)
+    seen, i = set(), 0
+    while i < n:
+        k = tuple(int(x) for x in rng.integers(0, vocab, kl[i]))
+        if k in seen:
+            continue
+        seen.add(k)
+        keys[i, :kl[i]] = k
+        i += 1
+    reps = rng.standard_normal((int(kl.sum()), d)).astype(np.float32)
+    return {"key_len": kl, "keys": keys, "freq": np.ones(n, np.uint64), "reps": reps}, seen
+
+
+@pytest.mark.gpu
+def test_gpu_streamed_plt1_multi_chunk(tmp_path):
+    """hmi_gpu_upload_plt1 over a table larger than its 64 MiB chunk: the gathered rows (h0, f64
+    bit pattern) equal those of the array upload; corrupt files fail closed (FormatError, the
+    version stays free and a good upload of it then succeeds)."""
+    from paper_2504_17449_b200 import engine as E
+    from paper_2504_17449_b200._native import DimensionError
+
+    cfg = oracle.Config(128, 2, 2, 2, 256, 5000, 0, 3, 9)
+    mc = E.model_config(*oracle.astuple(cfg))
+    root = {"key_len": np.ones(5000, np.uint32),
+            "keys": np.stack([np.arange(5000), np.zeros(5000), np.zeros(5000)], 1).astype(np.uint32),
+            "reps": np.random.default_rng(2).standard_normal((5000, 128)).astype(np.float32)}
+    big, seen = _big_table(3, 90_000, 128, 5000)  # ~180k rows x 512 B = ~92 MB of reps
+    p = str(tmp_path / "big.plt1")
+    plot.save_plt1(big, p, 1, 0, "big", 5000)
+    assert os.path.getsize(p) > (64 << 20)
+    rng = np.random.default_rng(4)
+    n, S = 16, 128
+    toks = np.zeros((n, S), np.uint32)
+    lens = np.full(n, 60, np.uint32)
+    hot = [k for k in list(seen)[:400] if len(k) == 3]
+    for i in range(n):
+        toks[i, :60] = rng.integers(0, 2000, 60)
+        for j in range(0, 57, 6):
+            toks[i, j:j + 3] = hot[int(rng.integers(0, len(hot)))]
+    h0s = []
+    for streamed in (False, True):
+        eng = E.GpuEngine(mc, E.generate_higher(mc), max_batch=n, max_seq=S, bottleneck=8,
+                          max_labels=5, max_tasks=1, max_versions=4)
+        eng.upload_table(0, 0xFFFFFFFF, root["key_len"], root["keys"], root["reps"])
+        if streamed:
+            # fail-closed: a truncated copy is rejected and leaves version 1 free
+            bad = str(tmp_path / "trunc.plt1")
+            _corrupt(p, bad, lambda b: b[:-100])
+            with pytest.raises(FormatError):
+                eng.upload_plt1(bad)
+            assert eng.upload_plt1(p) == (1, 0)
+        else:
+            eng.upload_table(1, 0, big["key_len"], big["keys"], big["reps"])
+        eng.register_task(0, E.generate_adapter(mc, 8, 1))
+        eng.register_head(0, 0, *E.generate_head(128, 5, 2))
+        eng.bind_instance(0, 1, 0, 0)
+        eng.set_debug(1)
+        eng.infer_batch(np.zeros(n, np.uint32), toks, lens)
+        h0s.append(eng.debug_h0(n, S))
+        rows, lev = eng.debug_gather(n)
+        assert (lev[:, :60] == 1).sum() > 0  # the branch is hit
+        eng.close()
+    assert np.array_equal(h0s[0].view(np.uint64), h0s[1].view(np.uint64))
+    # header checks: wrong hidden size -> DimensionError
+    small = str(tmp_path / "d64.plt1")
+    t = {k: v for k, v in big.items()}
+    t["reps"] = t["reps"][:, :64].copy()
+    plot.save_plt1(t, small, 2, 0, "", 0)
+    eng = E.GpuEngine(mc, E.generate_higher(mc), max_batch=n, max_seq=S, bottleneck=8,
+                      max_labels=5, max_tasks=1, max_versions=4)
+    eng.upload_table(0, 0xFFFFFFFF, root["key_len"], root["keys"], root["reps"])
+    with pytest.raises(DimensionError):
+        eng.upload_plt1(small)
+    eng.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["magic", "truncated", "trailing", "zero_freq", "key_len0",
+                                  "key_len_big", "duplicate"])
+def test_gpu_streamed_plt1_format_errors(tmp_path, case):
+    """The streamed reader rejects exactly the files the reference's plot::load rejects."""
+    from paper_2504_17449_b200 import engine as E
+
+    g = np.load(GOLD)
+    cfg = oracle.Config(*[int(x) for x in g["cfg"]])
+    mc = E.model_config(*oracle.astuple(cfg))
+    t = _golden_table()
+    good = str(tmp_path / "good.plt1")
+    plot.save_plt1(t, good, 1, 0, "", 0)
+    d = t["reps"].shape[1]
+    e0 = 4 + 4 + 4 + 4 + 4 + 4 + 4 + 4
+    k0 = int(t["key_len"][0])
+    e1 = e0 + 4 + 4 * k0 + 8 + 4 * k0 * d
+
+    def edit(b):
+        if case == "magic":
+            b[0:4] = b"PLT2"
+        elif case == "truncated":
+            b = b[:-7]
+        elif case == "trailing":
+            b += b"\0"
+        elif case == "zero_freq":
+            b[e0 + 4 + 4 * k0:e0 + 12 + 4 * k0] = (0).to_bytes(8, "little")
+        elif case == "key_len0":
+            b[e0:e0 + 4] = (0).to_bytes(4, "little")
+        elif case == "key_len_big":
+            b[e0:e0 + 4] = (9).to_bytes(4, "little")
+        elif case == "duplicate":
+            b[e1:e1 + 4 + 4 * k0] = b[e0:e0 + 4 + 4 * k0]
+        return b
+
+    bad = str(tmp_path / f"{case}.plt1")
+    _corrupt(good, bad, edit)
+    eng = E.GpuEngine(mc, E.generate_higher(mc), max_batch=4, max_seq=128, bottleneck=8,
+                      max_labels=5, max_tasks=1, max_versions=4)
+    eng.upload_table(0, 0xFFFFFFFF, g["t0_key_len"], g["t0_keys"], g["t0_reps"])
+    with pytest.raises(FormatError):
+        eng.upload_plt1(bad)
+    assert eng.upload_plt1(good) == (1, 0)  # nothing of the failed attempt was committed
+    eng.close()
