@@ -108,6 +108,16 @@ int hmi_gpu_register_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adap
 int hmi_gpu_replace_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapter_f32);
 /* AdapterStore::erase + DeviceSlotPool::evict (SPEC.md:527 delete_instance). */
 int hmi_gpu_unregister_task(hmi_gpu_ctx* ctx, uint32_t task_idx);
+/* Bulk register_set (start-up of 10,000 tenants): n tasks converted on `threads` host
+ * threads (0 = the machine's cores, at most 32). All-or-nothing: any registered or repeated
+ * index -> CONFLICT before any work; a failing task (by index order) is reported and
+ * nothing is registered.                                                      */
+int hmi_gpu_register_tasks(hmi_gpu_ctx* ctx, uint32_t n, const uint32_t* task_idx,
+                           const float* const* adapter_f32, uint32_t threads);
+/* Same from ADP1 files (adapter_set.cpp:48-75), read in parallel; a file whose header does
+ * not match the model -> DIMENSION, a malformed one -> FORMAT.                           */
+int hmi_gpu_register_task_files(hmi_gpu_ctx* ctx, uint32_t n, const uint32_t* task_idx,
+                                const char* const* adp1_paths, uint32_t threads);
 
 /* OutputHead (weights.hpp:45-53): kind 0 cls_classify, 1 token_tag,
  * 2 lm_logits; w [hidden x labels] f32, b [labels] f32.

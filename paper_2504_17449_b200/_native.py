@@ -151,6 +151,8 @@ def _sig(L):
     L.hmi_gpu_upload_plot_table.argtypes = [vp, u32, u32, vp]
     L.hmi_gpu_register_task_file.argtypes = [vp, u32, cp]
     L.hmi_gpu_check_adapter_dims.argtypes = [vp, u32, u32, u32]
+    L.hmi_gpu_register_tasks.argtypes = [vp, u32, u32p, P(f32p), u32]
+    L.hmi_gpu_register_task_files.argtypes = [vp, u32, u32p, P(cp), u32]
     L.hmi_gpu_upload_plt1.argtypes = [vp, cp, u32p, u32p]
     L.hmi_gpu_export_task.argtypes = [vp, u32, P(TaskExport)]
     L.hmi_gpu_import_task.argtypes = [vp, u32, P(TaskExport), f32p, u64p]

@@ -27,14 +27,17 @@
 // layer, so layer l+1's copies overlap layer l's compute.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <immintrin.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -48,6 +51,7 @@
 #include "adapter.hpp"
 #include "gemm.hpp"
 #include "kernels.hpp"
+#include "plot_builder.hpp"
 #include "slot_pool.hpp"
 
 namespace hmi_b200 {
@@ -71,11 +75,24 @@ const char* kProfNames[HMI_PROF_CLASSES] = {
     "adapter_down", "adapter_up", "layernorm1", "gemm_ffn1", "gemm_ffn2", "layernorm2",
     "head", "d2h_outputs", "adapter_copy", "step"};
 
+// Host f32 -> fp16 / bf16, round to nearest even. The F16C instruction and the bf16 bit
+// rounding equal __float2half_rn / __float2bfloat16_rn on every non-NaN input (checked
+// exhaustively over all 2^32 patterns) at a fraction of the software routines' cost.
+__attribute__((target("f16c"))) static inline uint16_t f2h_f16c(float x) {
+  return static_cast<uint16_t>(_cvtss_sh(x, _MM_FROUND_TO_NEAREST_INT));
+}
+static const bool kHasF16c = __builtin_cpu_supports("f16c");
+
 uint16_t f2h(float x, int precision) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  const bool nan = (u & 0x7fffffffu) > 0x7f800000u;
   if (precision == 1) {
+    if (!nan) return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
     __nv_bfloat16 b = __float2bfloat16_rn(x);
     return *reinterpret_cast<uint16_t*>(&b);
   }
+  if (kHasF16c && !nan) return f2h_f16c(x);
   __half h = __float2half_rn(x);
   return *reinterpret_cast<uint16_t*>(&h);
 }
@@ -506,10 +523,18 @@ void Ctx::convert_adapter(const float* src, uint8_t* dst) const {
     float* bdd = reinterpret_cast<float*>(wut + static_cast<size_t>(d) * r_pad);
     float* bud = bdd + r_pad;
     std::memset(slot, 0, slot_bytes);
-    for (int j = 0; j < r; ++j)
-      for (int i = 0; i < d; ++i) wdt[static_cast<size_t>(j) * d + i] = f2h(wd[static_cast<size_t>(i) * r + j], prec);
-    for (int i = 0; i < d; ++i)
-      for (int j = 0; j < r; ++j) wut[static_cast<size_t>(i) * r_pad + j] = f2h(wu[static_cast<size_t>(j) * d + i], prec);
+    // transposes in 32 x 32 tiles (both sides stay in L1)
+    constexpr int kT = 32;
+    for (int j0 = 0; j0 < r; j0 += kT)
+      for (int i0 = 0; i0 < d; i0 += kT)
+        for (int j = j0; j < std::min(j0 + kT, r); ++j)
+          for (int i = i0; i < std::min(i0 + kT, d); ++i)
+            wdt[static_cast<size_t>(j) * d + i] = f2h(wd[static_cast<size_t>(i) * r + j], prec);
+    for (int i0 = 0; i0 < d; i0 += kT)
+      for (int j0 = 0; j0 < r; j0 += kT)
+        for (int i = i0; i < std::min(i0 + kT, d); ++i)
+          for (int j = j0; j < std::min(j0 + kT, r); ++j)
+            wut[static_cast<size_t>(i) * r_pad + j] = f2h(wu[static_cast<size_t>(j) * d + i], prec);
     for (int j = 0; j < r; ++j) bdd[j] = bd[j];
     for (int i = 0; i < d; ++i) bud[i] = bu[i];
   }
@@ -1854,6 +1879,89 @@ int hmi_gpu_register_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adap
     c.convert_adapter(adapter_f32, p);
     c.store[task_idx] = p;
     c.pool->set_task(task_idx, static_cast<uint32_t>(c.L), c.ref_layer_bytes);
+  });
+}
+
+// Bulk registration (10k-tenant start-up): indices validated up front,
+// host blocks taken under the lock, then the adapters are read / converted on `threads` host
+// threads; all-or-nothing (the first failing task, in index order, is reported).
+static int register_many(hmi_gpu_ctx* ctx, uint32_t n, const uint32_t* task_idx, uint32_t threads,
+                         const std::function<void(uint32_t, std::vector<float>&, uint8_t*)>& fill) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(ctx != nullptr && (n == 0 || task_idx != nullptr), HMI_CONFIG_ERROR, "null argument");
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    std::set<uint32_t> seen;
+    for (uint32_t k = 0; k < n; ++k) {
+      HMI_CHECK(task_idx[k] < c.store.size(), HMI_CONFIG_ERROR, "task index exceeds max_tasks");
+      if (c.store[task_idx[k]] || !seen.insert(task_idx[k]).second)
+        throw HmiError(HMI_CONFLICT_ERROR, "adapter set for task already registered");
+    }
+    std::vector<uint8_t*> blocks(n);
+    for (uint32_t k = 0; k < n; ++k) blocks[k] = c.store_alloc();
+    const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint32_t nt = std::min<uint32_t>(std::max<uint32_t>(1, n), threads ? threads : std::min(hw, 32u));
+    std::atomic<uint32_t> next{0};
+    std::vector<int> code(n, HMI_OK);
+    std::vector<std::string> msg(n);
+    auto work = [&] {
+      std::vector<float> scratch;
+      for (uint32_t k; (k = next.fetch_add(1)) < n;) {
+        try {
+          fill(k, scratch, blocks[k]);
+        } catch (const HmiError& e) {
+          code[k] = e.code;
+          msg[k] = e.what();
+        } catch (const std::exception& e) {
+          code[k] = HMI_CAPACITY_ERROR;
+          msg[k] = e.what();
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (uint32_t k = 0; k < n; ++k) {
+      if (code[k] != HMI_OK) {
+        for (uint8_t* b : blocks) c.free_blocks.push_back(b);
+        throw HmiError(code[k], "task " + std::to_string(task_idx[k]) + ": " + msg[k]);
+      }
+    }
+    for (uint32_t k = 0; k < n; ++k) {
+      c.store[task_idx[k]] = blocks[k];
+      c.pool->set_task(task_idx[k], static_cast<uint32_t>(c.L), c.ref_layer_bytes);
+    }
+  });
+}
+
+int hmi_gpu_register_tasks(hmi_gpu_ctx* ctx, uint32_t n, const uint32_t* task_idx,
+                           const float* const* adapter_f32, uint32_t threads) {
+  using namespace hmi_b200;
+  if (n && !adapter_f32) {
+    set_last_error("null argument");
+    return HMI_CONFIG_ERROR;
+  }
+  return register_many(ctx, n, task_idx, threads, [&](uint32_t k, std::vector<float>&, uint8_t* blk) {
+    HMI_CHECK(adapter_f32[k] != nullptr, HMI_CONFIG_ERROR, "null adapter");
+    ctx->impl.convert_adapter(adapter_f32[k], blk);
+  });
+}
+
+int hmi_gpu_register_task_files(hmi_gpu_ctx* ctx, uint32_t n, const uint32_t* task_idx,
+                                const char* const* adp1_paths, uint32_t threads) {
+  using namespace hmi_b200;
+  if (n && !adp1_paths) {
+    set_last_error("null argument");
+    return HMI_CONFIG_ERROR;
+  }
+  return register_many(ctx, n, task_idx, threads, [&](uint32_t k, std::vector<float>& body, uint8_t* blk) {
+    const Ctx& c = ctx->impl;
+    body.resize((static_cast<size_t>(c.d) * c.r * 2 + c.r + c.d) * c.L);
+    load_adp1_expect(adp1_paths[k], static_cast<uint32_t>(c.L), static_cast<uint32_t>(c.d),
+                     static_cast<uint32_t>(c.r), body.data());
+    c.convert_adapter(body.data(), blk);
   });
 }
 

@@ -127,6 +127,21 @@ int ingest_guarded(F&& fn) {
 }
 
 }  // namespace
+
+// ADP1 body straight into `body` when the header matches the expected dimensions (one pass;
+// the bulk registration path). Dimension mismatch -> DimensionError, format as hmi_adapter_set_load.
+void load_adp1_expect(const char* path, uint32_t L, uint32_t D, uint32_t R, float* body) {
+  Reader rd(path);
+  rd.magic("ADP1");
+  (void)rd.str();
+  const uint32_t l = rd.u32(), d = rd.u32(), r = rd.u32();
+  if (l == 0 || d == 0 || r == 0 || r >= d) rd.fail("adapter header dimensions invalid", rd.off);
+  HMI_CHECK(l == L && d == D && r == R, HMI_DIMENSION_ERROR,
+            std::string("adapter set in ") + path + " does not match the model");
+  const size_t per = static_cast<size_t>(D) * R * 2 + R + D;
+  rd.f32s(body, per * L);
+  rd.expect_end();
+}
 }  // namespace hmi_b200
 
 extern "C" {

@@ -13,6 +13,9 @@
 
 namespace hmi_b200 {
 
+// ingest.cpp: one-pass ADP1 read with the model's dimensions expected
+void load_adp1_expect(const char* path, uint32_t L, uint32_t D, uint32_t R, float* body);
+
 constexpr int kMaxFragment = 5;
 
 void launch_plot_embed(const float* tok_emb, const float* pos_emb, const uint32_t* keys, int ngram,

@@ -116,6 +116,24 @@ class GpuEngine:
         a = np.ascontiguousarray(adapter_f32, np.float32)
         check(_native.lib().hmi_gpu_register_task(self.h, task, _p(a, ctypes.c_float)))
 
+    def register_tasks(self, tasks, adapters, threads: int = 0) -> None:
+        """Bulk register_set on host threads (all-or-nothing)."""
+        idx = np.ascontiguousarray(tasks, np.uint32)
+        arrs = [np.ascontiguousarray(a, np.float32) for a in adapters]
+        assert len(arrs) == len(idx)
+        ptrs = (ctypes.POINTER(ctypes.c_float) * max(1, len(arrs)))(*[_p(a, ctypes.c_float) for a in arrs])
+        check(_native.lib().hmi_gpu_register_tasks(self.h, len(idx), _p(idx, ctypes.c_uint32), ptrs,
+                                                   threads))
+
+    def register_task_files(self, tasks, paths, threads: int = 0) -> None:
+        """Bulk register_set from ADP1 files read and converted on host threads."""
+        idx = np.ascontiguousarray(tasks, np.uint32)
+        enc = [p.encode() for p in paths]
+        assert len(enc) == len(idx)
+        arr = (ctypes.c_char_p * max(1, len(enc)))(*enc)
+        check(_native.lib().hmi_gpu_register_task_files(self.h, len(idx), _p(idx, ctypes.c_uint32),
+                                                        arr, threads))
+
     def replace_task(self, task: int, adapter_f32) -> None:
         a = np.ascontiguousarray(adapter_f32, np.float32)
         check(_native.lib().hmi_gpu_replace_task(self.h, task, _p(a, ctypes.c_float)))

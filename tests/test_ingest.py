@@ -349,3 +349,52 @@ def test_gpu_streamed_plt1_format_errors(tmp_path, case):
         eng.upload_plt1(bad)
     assert eng.upload_plt1(good) == (1, 0)  # nothing of the failed attempt was committed
     eng.close()
+
+
+@pytest.mark.gpu
+def test_gpu_bulk_registration(tmp_path):
+    """register_tasks / register_task_files (threads) register exactly what register_task does
+    (served scores bit-identical), all-or-nothing on conflicts, bad dimensions, bad files."""
+    from paper_2504_17449_b200 import engine as E
+    from paper_2504_17449_b200._native import ConflictError, DimensionError
+    from tests.world import World
+
+    cfg = oracle.Config(128, 2, 2, 2, 256, 300, 0, 3, 5)
+    n = 40
+    w = World(cfg, n_tasks=n, r=8, labels=5)  # per-task register_task
+    inst, toks, lens = w.requests(5, 32, 60)
+    want = w.eng.infer_batch(inst, toks, lens)
+    mc = E.model_config(*oracle.astuple(cfg))
+    paths = []
+    for t in range(n):
+        p = str(tmp_path / f"t{t}.adp1")
+        plot.save_adp1(p, f"task{t}", w.adapters[t], cfg.hidden_size, 8)
+        paths.append(p)
+    for mode in ("arrays", "files"):
+        eng = E.GpuEngine(mc, w.higher, max_batch=32, max_seq=128, bottleneck=8, max_labels=5,
+                          max_tasks=n, max_versions=8)
+        for t in w.tables:
+            eng.upload_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
+        if mode == "arrays":
+            with pytest.raises(ConflictError):  # repeated index: nothing registered
+                eng.register_tasks([0, 1, 1], [w.adapters[0], w.adapters[1], w.adapters[1]])
+            eng.register_tasks(range(n), w.adapters, threads=7)
+        else:
+            bad = str(tmp_path / "r16.adp1")
+            plot.save_adp1(bad, "x", E.generate_adapter(mc, 16, 1), cfg.hidden_size, 16)
+            with pytest.raises(DimensionError):
+                eng.register_task_files([0, 1], [paths[0], bad])
+            trunc = str(tmp_path / "trunc.adp1")
+            _corrupt(paths[3], trunc, lambda b: b[:-5])
+            with pytest.raises(FormatError):
+                eng.register_task_files([2, 3], [paths[2], trunc])
+            eng.register_task_files(range(n), paths)  # indices 0..3 are still free
+        with pytest.raises(ConflictError):
+            eng.register_tasks([5], [w.adapters[5]])
+        for t in range(n):
+            eng.register_head(t, 0, *w.heads[t])
+            eng.bind_instance(t, int(w.inst_version[t]), t, t)
+        got = eng.infer_batch(inst, toks, lens)
+        assert np.array_equal(got.scores, want.scores), mode
+        eng.close()
+    w.eng.close()
