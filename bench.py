@@ -55,6 +55,8 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        if os.environ.get("HMI_BENCH_NO_CLOCKS"):  # variance experiments only
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
