@@ -274,6 +274,24 @@ def test_long_requests_s256(mode):
     w.eng.close()
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_max_length_s512_ragged(mode):
+    """Maximum padded length 512 (four row tiles per request) with ragged lengths down to a
+    single token in one batch: general attention path, per-tile adapter routing, causal and
+    encoder, token_tag head (every position checked)."""
+    cfg = oracle.Config(128, 2, 2, 2, 256, 600, mode, 3, 17)
+    w = World(cfg, n_tasks=5, r=8, labels=6, max_batch=5, max_seq=512, head_kind=E.HEAD_TAG)
+    inst, toks, lens = w.requests(31, 5, 512, min_len=1)
+    lens[:3] = [512, 1, 385]
+    res = w.eng.infer_batch(inst, toks, lens, want_tags=True)
+    ref_scores, ref_labels, ref_tags = w.oracle_batch(inst, toks, lens)
+    agree = np.concatenate([res.tags[i, :lens[i]] == ref_tags[i] for i in range(len(lens))])
+    assert agree.mean() >= 0.99  # per-token argmax (near ties), as test_token_tag_head
+    for i in range(len(lens)):
+        assert (res.tags[i, lens[i]:] == -1).all()
+    w.eng.close()
+
+
 def test_token_tag_head():
     w = World(oracle.TINY, n_tasks=4, r=16, labels=5, head_kind=E.HEAD_TAG, max_batch=8)
     inst, toks, lens = w.requests(5, 6, 40, min_len=3)
