@@ -401,6 +401,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnDecodeArgs A) {
 // the generated rows' K and V (tail_cap rows each); keys / values are read from shared memory
 // only, the new row (j == pos) from this step's projections.
 constexpr int kDecS = 256;     // max prompt rows staged (2 boxes of 128)
+constexpr int kDecTailBox = 8; // generated rows per tail box (one 1 KB swizzle atom)
 __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_constant__ AttnDecodeMaps M,
                                                              AttnDecodeArgs A) {
   extern __shared__ uint8_t dsm[];
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
   __shared__ float qs[64];
   __shared__ float red[32];
   __shared__ float part[4 * 64];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar_k, bar_v;  // K lands first: scores and softmax overlap the V copy
   const int h = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = A.d;
@@ -424,22 +425,25 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
   const int n_tail = pos - len0;  // generated rows already cached
   const uint16_t* qrow = A.qkv_new + static_cast<long long>(b) * 3 * d;
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bar_k, 1);
+    mbar_init(&bar_v, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     const int nbox = (len0 + 127) / 128;
-    const uint32_t bytes = nbox * 2 * 16384 + (n_tail > 0 ? 2 * T * 128 : 0);
-    mbar_arrive_expect_tx(&bar, bytes);
-    for (int x = 0; x < nbox; ++x) {
-      tma_load_2d(kpre + x * 16384, &M.prefill, &bar, d + h * 64, b * S + 128 * x);
-      tma_load_2d(vpre + x * 16384, &M.prefill, &bar, 2 * d + h * 64, b * S + 128 * x);
-    }
-    if (n_tail > 0) {
-      tma_load_2d(ktail, &M.tail, &bar, h * 64, b * T);
-      tma_load_2d(vtail, &M.tail, &bar, d + h * 64, b * T);
-    }
+    const int ntail = (n_tail + kDecTailBox - 1) / kDecTailBox;  // only the cached rows
+    const uint32_t bytes = nbox * 16384 + ntail * kDecTailBox * 128;
+    mbar_arrive_expect_tx(&bar_k, bytes);
+    mbar_arrive_expect_tx(&bar_v, bytes);
+    for (int x = 0; x < nbox; ++x)
+      tma_load_2d(kpre + x * 16384, &M.prefill, &bar_k, d + h * 64, b * S + 128 * x);
+    for (int x = 0; x < ntail; ++x)
+      tma_load_2d(ktail + x * kDecTailBox * 128, &M.tail, &bar_k, h * 64, b * T + kDecTailBox * x);
+    for (int x = 0; x < nbox; ++x)
+      tma_load_2d(vpre + x * 16384, &M.prefill, &bar_v, 2 * d + h * 64, b * S + 128 * x);
+    for (int x = 0; x < ntail; ++x)
+      tma_load_2d(vtail + x * kDecTailBox * 128, &M.tail, &bar_v, d + h * 64, b * T + kDecTailBox * x);
   }
   if (threadIdx.x < 64) qs[threadIdx.x] = ld16(qrow, h * 64 + threadIdx.x, A.bf16);
   __syncthreads();
@@ -455,7 +459,7 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
           reinterpret_cast<const uint32_t*>(qrow + 2 * d + h * 64)[threadIdx.x - 32];
     }
   }
-  mbar_wait(&bar, 0);
+  mbar_wait(&bar_k, 0);
   // row r of a staged operand: 8 chunks of 16 B, swizzled
   auto srow = [&](const uint8_t* box, int r, int c) -> const uint4* {
     return reinterpret_cast<const uint4*>(box + r * 128 + ((c ^ (r & 7)) << 4));
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
     sum += e;
   }
   sum = block_sum_t(sum, red);  // contains the barrier that publishes sc[]
+  mbar_wait(&bar_v, 0);
   // context: warp w takes keys j = w (mod 4); lane its dims 2 lane, 2 lane + 1 (4 bytes of the
   // row's chunk lane / 4)
   float a0 = 0.f, a1 = 0.f;
@@ -656,7 +661,7 @@ AttnDecodeMaps make_attn_decode_maps(const void* qkv_prefill, int max_rows, void
   m.prefill = make_tmap_2d(qkv_prefill, t16, 3ull * d, max_rows, 3ull * d * 2, 64, 128,
                            CU_TENSOR_MAP_SWIZZLE_128B);
   m.tail = make_tmap_2d(tail, t16, 2ull * d, static_cast<uint64_t>(max_batch) * tail_cap,
-                        2ull * d * 2, 64, static_cast<uint32_t>(tail_cap), CU_TENSOR_MAP_SWIZZLE_128B);
+                        2ull * d * 2, 64, kDecTailBox, CU_TENSOR_MAP_SWIZZLE_128B);
   return m;
 }
 
