@@ -558,7 +558,38 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   __syncthreads();
   // down projection: warp per bottleneck unit, 16-byte weight vectors across the lanes
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  {
+  if (RP == 64 && nw == 8 && d <= 96 * 8) {
+    // every weight load of this warp's 8 units in flight at once (the loop below waits one
+    // memory round trip per unit); same per-lane order of sums, so the same mid[]
+    constexpr int U = RP > 0 ? RP / 8 : 1;
+    const int nch = d / 8;
+    uint4 w[U][3];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4* w4 = reinterpret_cast<const uint4*>(wd + static_cast<size_t>(warp + 8 * u) * d);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int c = lane + 32 * m;
+        w[u][m] = c < nch ? __ldg(w4 + c) : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc = 0.f;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int c = lane + 32 * m;
+        if (c < nch) {
+          float f[8];
+          unpack8(w[u][m], f, A.bf16);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc += a[c * 8 + e] * f[e];
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) mid[warp + 8 * u] = fmaxf(acc + bd[warp + 8 * u], 0.f);
+    }
+  } else {
     for (int j = warp; j < rp; j += nw) {
       const uint4* w4 = reinterpret_cast<const uint4*>(wd + static_cast<size_t>(j) * d);
       float acc = 0.f;
@@ -581,6 +612,34 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   __syncthreads();
   // up projection + bias + skip + residual
   float s1 = 0.f;
+  if (RP > 0 && d <= 3 * static_cast<int>(blockDim.x)) {
+    // this thread's (up to) three output rows: all their weight loads in flight at once
+    constexpr int C = RP > 0 ? RP / 8 : 1;
+    uint4 w[3][C];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      const uint4* w4 = reinterpret_cast<const uint4*>(wu + static_cast<size_t>(i < d ? i : 0) * rp);
+#pragma unroll
+      for (int c = 0; c < C; ++c) w[k][c] = i < d ? __ldg(w4 + c) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= d) break;
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        float f[8];
+        unpack8(w[k][c], f, A.bf16);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
+      }
+      const float v = acc + bu[i] + a[i] + ld16(hrow, i, A.bf16);
+      y[i] = v;
+      s1 += v;
+    }
+  } else
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const uint4* w4 = reinterpret_cast<const uint4*>(wu + static_cast<size_t>(i) * rp);
     float acc = 0.f;
