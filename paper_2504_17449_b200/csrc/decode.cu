@@ -290,8 +290,9 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
       int pos = A.gen_pos[b];
       if (A.advance) A.gen_pos[b] = ++pos;
       A.gen_tokens[static_cast<long long>(b) * A.tok_stride + pos] = static_cast<uint32_t>(tok);
-      A.out_tokens[static_cast<long long>(b) * A.out_ld + A.step] = tok;
-      if (A.out_logits) A.out_logits[static_cast<long long>(b) * A.out_ld + A.step] = static_cast<float>(best);
+      const int st = A.step >= 0 ? A.step : pos - A.lens[b];
+      A.out_tokens[static_cast<long long>(b) * A.out_ld + st] = tok;
+      if (A.out_logits) A.out_logits[static_cast<long long>(b) * A.out_ld + st] = static_cast<float>(best);
     }
   }
 }

@@ -38,7 +38,8 @@ struct LmArgmaxArgs {
   int32_t* out_tokens = nullptr;   // [n][out_ld]
   float* out_logits = nullptr;     // [n][out_ld]
   int out_ld = 0;
-  int step = 0;
+  int step = 0;                    // output column; < 0: gen_pos (after advance) - lens[b], so
+  const int* lens = nullptr;       // one launch serves every step (CUDA-graph replay)
 };
 void launch_lm_argmax(const LmArgmaxArgs& a, int n_req, cudaStream_t stream);
 

@@ -44,6 +44,7 @@
 #include <set>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -294,6 +295,12 @@ struct Ctx {
   bool use_batch_copy = std::getenv("HMI_BATCH_COPY") == nullptr ||
                         std::string(std::getenv("HMI_BATCH_COPY")) != "0";
   std::vector<cudaEvent_t> ev_layer;
+  // decode step captured once per (batch shape, head, tables) and replayed with cudaGraphLaunch
+  // (HMI_DECODE_GRAPH=0: eager launches every step)
+  std::map<std::tuple<int, int, int, uint64_t>, cudaGraphExec_t> dec_graphs;
+  uint64_t tables_epoch = 0;
+  bool decode_graph = std::getenv("HMI_DECODE_GRAPH") == nullptr ||
+                      std::string(std::getenv("HMI_DECODE_GRAPH")) != "0";
   // peer rebalancing: export pins per task, peer arenas opened over CUDA IPC, bytes moved
   std::map<uint32_t, int> exported;
   std::map<std::string, void*> ipc_open;
@@ -488,6 +495,7 @@ Ctx::~Ctx() {
   }
   for (auto* p : pinned_chunks) cudaFreeHost(p);
   for (auto& [k, p] : ipc_open) cudaIpcCloseMemHandle(p);
+  for (auto& [k, g] : dec_graphs) cudaGraphExecDestroy(g);
   for (auto e : ev_layer) cudaEventDestroy(e);
   for (auto& [c, e] : prof_pending) {
     cudaEventDestroy(e.first);
@@ -1208,7 +1216,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
   am.out_tokens = gen_out.p;
   am.out_logits = gen_logit.p;
   am.out_ld = T;
-  for (uint32_t k = 1; k < n_new; ++k) {
+  auto step = [&](uint32_t k) {
     timed(P_RETRIEVE, s, [&] {
       launch_retrieve(P, gen_tokens.p, d_lens.p, d_req_version.p, n, S, 1, h16.p, prec, nullptr,
                       nullptr, nullptr, d_err.p, s, gen_pos.p, gen_stride);
@@ -1266,10 +1274,36 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
     }
     timed(P_HEAD, s, [&] {
       launch_gemm(lm.plan, Mp, s);
-      am.step = static_cast<int>(k);
+      (void)k;
+      am.step = -1;  // output column from gen_pos: identical launches every step
+      am.lens = d_lens.p;
       launch_lm_argmax(am, n, s);
     });
+  };
+  // step 1 eagerly (first-use attribute setup), then one captured step replayed: a decode step
+  // is ~90 short launches whose arguments do not change between steps (positions live on the
+  // device), so the graph removes the per-launch submission and inter-kernel gaps
+  if (n_new <= 1) return;
+  step(1);
+  const bool graph = decode_graph && !prof && n_new > 2;
+  if (!graph) {
+    for (uint32_t k = 2; k < n_new; ++k) step(k);
+    return;
   }
+  const auto key = std::make_tuple(n, S, wide_head, tables_epoch);
+  auto it = dec_graphs.find(key);
+  if (it == dec_graphs.end()) {
+    cudaGraph_t g = nullptr;
+    HMI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    step(2);
+    HMI_CUDA(cudaStreamEndCapture(s, &g));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    HMI_CUDA(e);
+    it = dec_graphs.emplace(key, exec).first;
+  }
+  for (uint32_t k = 2; k < n_new; ++k) HMI_CUDA(cudaGraphLaunch(it->second, s));
 }
 
 }  // namespace hmi_b200
@@ -1671,6 +1705,7 @@ static void commit_version(Ctx& c, uint32_t version_id, uint32_t parent_id, uint
   c.rep_rows += rows;
   c.h_parent[version_id] = parent_id == kNoParent ? -1 : static_cast<int32_t>(parent_id);
   c.upload_plot_hash();
+  ++c.tables_epoch;  // retrieval pointers / hash mask may have changed: recapture decode graphs
 }
 }  // namespace hmi_b200
 
