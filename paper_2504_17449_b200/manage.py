@@ -227,9 +227,17 @@ class Manager:
             labels, seed = int(payload.get("labels", self.engine.max_labels)), int(payload.get("head_seed", 0))
             w, b = generate_head(self.engine.cfg.hidden_size, labels, seed)
             href = {"kind": kind, "labels": labels, "seed": seed}
-        if not self._free_inst or not self._free_task or self._next_head >= self.engine.max_heads:
-            raise ValidationError("engine capacity reached (max_instances / max_tasks / max_heads)")
-        task, inst_idx, head = self._free_task.pop(), self._free_inst.pop(), self._next_head
+        want = payload.get("_indices")  # (task, instance, head) of a saved snapshot (load())
+        if want is not None:
+            task, inst_idx, head = (int(x) for x in want)
+            if task not in self._free_task or inst_idx not in self._free_inst or not 0 <= head < self.engine.max_heads:
+                raise ConflictError(f"indices {want} of instance {iid!r} are not free")
+            self._free_task.remove(task)
+            self._free_inst.remove(inst_idx)
+        else:
+            if not self._free_inst or not self._free_task or self._next_head >= self.engine.max_heads:
+                raise ValidationError("engine capacity reached (max_instances / max_tasks / max_heads)")
+            task, inst_idx, head = self._free_task.pop(), self._free_inst.pop(), self._next_head
         try:
             if body is None:
                 self.engine.register_task_file(task, aref["file"])
@@ -237,7 +245,7 @@ class Manager:
                 self.engine.register_task(task, body)
             try:
                 self.engine.register_head(head, kind, w, b)
-                self._next_head += 1
+                self._next_head = max(self._next_head, head + 1)
                 self.engine.bind_instance(inst_idx, vid, task, head)
             except BaseException:
                 self.engine.unregister_task(task)
@@ -294,7 +302,8 @@ class Manager:
                              for k, v in sorted(self.versions.items())},
                 "tenants": {t: sorted(s) for t, s in sorted(self.tenants.items())},
                 "instances": {i: {"tenant": x.tenant, "version": x.version, "task": x.task,
-                                  "head": x.head} for i, x in sorted(self.instances.items())},
+                                  "head": x.head, "index": self.registry.instances[i]}
+                              for i, x in sorted(self.instances.items())},
             }
 
     def save(self, directory: str) -> None:
@@ -344,7 +353,8 @@ class Manager:
             m.versions[vid] = _Version(v["parent"], v["label"], v["tenant"], table, corpus, v["alpha"])
         for iid, x in sorted(snap["instances"].items(), key=lambda kv: kv[1]["task"]):
             ref = snap["artefacts"][iid]
-            p = {"instance_id": iid, "version_id": x["version"]}
+            p = {"instance_id": iid, "version_id": x["version"],
+                 "_indices": (x["task"], x["index"], x["head"])}
             a = ref["adapter"]
             if "file" in a:
                 p["adapter_file"] = os.path.join(directory, a["file"]) if a.get("relative") else a["file"]

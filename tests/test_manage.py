@@ -187,10 +187,15 @@ def test_save_load_round_trip(tmp_path):
         "instance_id": "b", "version_id": 0,
         "adapter": E.generate_adapter(m.engine.cfg, R, 9),
         "head": {"kind": 0, "w": np.ones((CFG.hidden_size, LABELS), np.float32), "b": np.zeros(LABELS, np.float32)}}))
+    _inst(m, "A", "gone", v, 4)  # a deletion leaves holes the reload must reproduce
+    m.handle(ManageRequest("delete_instance", "A", {"instance_id": "gone"}))
+    _inst(m, "B", "c", 0, 5)
     m.save(str(tmp_path))
     m2 = Manager.load(str(tmp_path), FakeEngine(), FakeBuilder(), min_corpus_tokens=200)
     assert m2.snapshot_state() == m.snapshot_state()
-    assert m2.engine.tasks == m.engine.tasks and m2.engine.heads == m.engine.heads
+    live = {x["head"] for x in m.snapshot_state()["instances"].values()}
+    assert m2.engine.tasks == m.engine.tasks  # deleted instances' heads stay on the device
+    assert m2.engine.heads == {h: w for h, w in m.engine.heads.items() if h in live}
     assert m2.engine.binds == m.engine.binds and m2.engine.tables == m.engine.tables
     # the reloaded domain keeps its corpus: update_domain still merges
     assert m2.handle(ManageRequest("update_domain", "A", {"version_id": v, "corpus": _corpus(5, 1, 9)})).version_id == 2
