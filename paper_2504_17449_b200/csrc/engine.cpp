@@ -344,9 +344,17 @@ struct Ctx {
   int gen_stride = 0;
   struct DecPlans {
     GemmPlan qkv, oproj, ffn1, ffn2;
+    std::vector<GemmPlan> ffn2_split;  // K slices of FFN2 (f32 partials, no bias / residual)
     AttnDecodeMaps attn;  // TMA maps over this layer's prompt q|k|v and generated k|v
   };
   std::vector<DecPlans> dec;
+  // decode FFN2 split-K: the M = 256 GEMM has only d / 64 x 2 tiles, so its K = f loop is cut
+  // into slices run as concurrent branches (aux streams; graph branches when captured) and the
+  // LayerNorm after it sums the partials (HMI_DECODE_SPLIT=1 disables)
+  int dec_splits = 1;
+  DevBuf<float> dec_part, dec_zero;
+  std::vector<cudaStream_t> dec_aux;
+  std::vector<cudaEvent_t> dec_ev;  // [0] fork, [1..] joins
   // wide lm heads (kind 2, labels > max_labels): 16-bit [V_pad][d] GEMM operand + padded bias
   struct LmHead {
     int V = 0, V_pad = 0;
@@ -496,6 +504,10 @@ Ctx::~Ctx() {
   for (auto* p : pinned_chunks) cudaFreeHost(p);
   for (auto& [k, p] : ipc_open) cudaIpcCloseMemHandle(p);
   for (auto& [k, g] : dec_graphs) cudaGraphExecDestroy(g);
+  for (auto st : dec_aux) cudaStreamDestroy(st);
+  for (auto e : dec_ev) cudaEventDestroy(e);
+  dec_part.free();
+  dec_zero.free();
   for (auto e : ev_layer) cudaEventDestroy(e);
   for (auto& [c, e] : prof_pending) {
     cudaEventDestroy(e.first);
@@ -751,6 +763,20 @@ void Ctx::build_plans() {
       s.b_group_stride_bytes = size_t(d) * f * 2; s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
       s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, mt, sms);
       dp.ffn2 = make_gemm_plan(s);
+      if (dec_splits > 1) {
+        const int ks = f / dec_splits;
+        for (int sp = 0; sp < dec_splits; ++sp) {
+          GemmSpec t = s;
+          t.a = ffn16.p + static_cast<size_t>(sp) * ks;  // columns [sp ks, (sp + 1) ks) of A
+          t.K = ks;
+          t.b = w.w2 + static_cast<size_t>(sp) * ks;
+          t.bias = dec_zero.p;
+          t.res0 = nullptr;
+          t.c = dec_part.p + static_cast<size_t>(sp) * Bp * d;
+          t.epi = kEpiOutF32;
+          dp.ffn2_split.push_back(make_gemm_plan(t));
+        }
+      }
       dp.attn = make_attn_decode_maps(qkv_at(l), max_rows,
                                       kv_tail.p + static_cast<size_t>(l) * opt.max_batch *
                                                       opt.max_new_tokens * 2 * d,
@@ -1266,11 +1292,31 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
         launch_adapter_rows_ln(a, n, s);
       });
       timed(P_FFN1, s, [&] { launch_gemm(dp.ffn1, Mp, s); });
-      timed(P_FFN2, s, [&] { launch_gemm(dp.ffn2, Mp, s); });
-      timed(P_LN2, s, [&] {
-        launch_layernorm(y32.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p, last ? hdec32.p : nullptr,
-                         n, d, prec, s);
-      });
+      if (!dp.ffn2_split.empty()) {
+        // K slices as concurrent branches: fork from s, join before the LayerNorm that sums them
+        timed(P_FFN2, s, [&] {
+          HMI_CUDA(cudaEventRecord(dec_ev[0], s));
+          for (size_t i = 1; i < dp.ffn2_split.size(); ++i) {
+            cudaStream_t a = dec_aux[i - 1];
+            HMI_CUDA(cudaStreamWaitEvent(a, dec_ev[0], 0));
+            launch_gemm(dp.ffn2_split[i], Mp, a);
+            HMI_CUDA(cudaEventRecord(dec_ev[i], a));
+          }
+          launch_gemm(dp.ffn2_split[0], Mp, s);
+          for (size_t i = 1; i < dp.ffn2_split.size(); ++i) HMI_CUDA(cudaStreamWaitEvent(s, dec_ev[i], 0));
+        });
+        timed(P_LN2, s, [&] {
+          launch_layernorm(dec_part.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p,
+                           last ? hdec32.p : nullptr, n, d, prec, s, dec_splits,
+                           static_cast<long long>(Bp) * d, w.b2, x16.p);
+        });
+      } else {
+        timed(P_FFN2, s, [&] { launch_gemm(dp.ffn2, Mp, s); });
+        timed(P_LN2, s, [&] {
+          launch_layernorm(y32.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p, last ? hdec32.p : nullptr,
+                           n, d, prec, s);
+        });
+      }
     }
     timed(P_HEAD, s, [&] {
       launch_gemm(lm.plan, Mp, s);
@@ -1505,6 +1551,18 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       c.gen_pos.alloc(Bm);
       c.gen_out.alloc(Bm * T);
       c.gen_logit.alloc(Bm * T);
+      const char* sp_env = std::getenv("HMI_DECODE_SPLIT");
+      c.dec_splits = sp_env ? std::max(1, std::atoi(sp_env)) : 2;
+      if (f % (64 * c.dec_splits) != 0) c.dec_splits = 1;
+      if (c.dec_splits > 1) {
+        c.dec_part.alloc(static_cast<size_t>(c.dec_splits) * c.Bp * d);
+        c.dec_zero.alloc(static_cast<size_t>(d));
+        HMI_CUDA(cudaMemset(c.dec_zero.p, 0, static_cast<size_t>(d) * 4));
+        c.dec_aux.resize(c.dec_splits - 1);
+        for (auto& st : c.dec_aux) HMI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        c.dec_ev.resize(c.dec_splits);
+        for (auto& e : c.dec_ev) HMI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
     }
     c.mid16.alloc(R * c.r_pad); c.x16.alloc(R * d); c.ffn16.alloc(R * f);
     c.y32.alloc(R * d); c.h32.alloc(R * d);

@@ -93,8 +93,12 @@ void launch_attention(const void* qkv, void* ctx, const int* lens, int n_req, in
                       int heads, int causal, int precision, cudaStream_t stream);
 
 // K4: LayerNorm over f32 rows (the residual sum is produced by the GEMM epilogue).
+// n_parts > 0: y holds n_parts split-K partials (part_stride floats apart); the row is
+// their sum + bias + res16 (16-bit) before normalising (the split GEMM's reduction)
 void launch_layernorm(const float* y, const float* gamma, const float* beta, void* out16,
-                      float* out32, int rows, int d, int precision, cudaStream_t stream);
+                      float* out32, int rows, int d, int precision, cudaStream_t stream,
+                      int n_parts = 0, long long part_stride = 0, const float* bias = nullptr,
+                      const void* res16 = nullptr);
 
 // K7: per-request task head + first-max argmax (apply_head, model.cpp:120-171).
 struct HeadDev {

@@ -19,6 +19,15 @@ namespace hmi_b200 {
 namespace {
 
 template <bool kBf16>
+__device__ __forceinline__ float2 unpack16x2(uint32_t u) {
+  if constexpr (kBf16) {
+    return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+  } else {
+    return __half22float2(*reinterpret_cast<const __half2*>(&u));
+  }
+}
+
+template <bool kBf16>
 __device__ __forceinline__ uint32_t pack16x2(float a, float b) {
   if constexpr (kBf16) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -37,15 +46,42 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
                                                         const float* __restrict__ gamma,
                                                         const float* __restrict__ beta,
                                                         uint16_t* __restrict__ out16,
-                                                        float* __restrict__ out32, int rows) {
+                                                        float* __restrict__ out32, int rows,
+                                                        int n_parts, long long part_stride,
+                                                        const float* __restrict__ bias,
+                                                        const uint16_t* __restrict__ res16) {
   constexpr int d = 128 * V;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
-  const float4* src = reinterpret_cast<const float4*>(y + static_cast<long long>(warp) * d);
   float4 v[V];
+  if (n_parts == 0) {
+    const float4* src = reinterpret_cast<const float4*>(y + static_cast<long long>(warp) * d);
 #pragma unroll
-  for (int i = 0; i < V; ++i) v[i] = __ldcs(src + lane + 32 * i);
+    for (int i = 0; i < V; ++i) v[i] = __ldcs(src + lane + 32 * i);
+  } else {
+    // split-K partial sums (fixed order) + bias + 16-bit residual: the reduction of a split
+    // GEMM folded into the LayerNorm that follows it
+    const float4* bb = reinterpret_cast<const float4*>(bias);
+    const uint2* rr = reinterpret_cast<const uint2*>(res16 + static_cast<long long>(warp) * d);
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = __ldcs(reinterpret_cast<const float4*>(y + static_cast<long long>(warp) * d) + lane + 32 * i);
+    for (int sp = 1; sp < n_parts; ++sp) {
+      const float4* src = reinterpret_cast<const float4*>(y + sp * part_stride + static_cast<long long>(warp) * d);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float4 t = __ldcs(src + lane + 32 * i);
+        v[i].x += t.x; v[i].y += t.y; v[i].z += t.z; v[i].w += t.w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float4 b = __ldg(bb + lane + 32 * i);
+      const uint2 u = rr[lane + 32 * i];
+      const float2 r01 = unpack16x2<kBf16>(u.x), r23 = unpack16x2<kBf16>(u.y);
+      v[i].x += b.x + r01.x; v[i].y += b.y + r01.y; v[i].z += b.z + r23.x; v[i].w += b.w + r23.y;
+    }
+  }
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < V; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
@@ -563,7 +599,9 @@ __global__ void __launch_bounds__(256) head_kernel(HeadDev H, const float* __res
 }  // namespace
 
 void launch_layernorm(const float* y, const float* gamma, const float* beta, void* out16,
-                      float* out32, int rows, int d, int precision, cudaStream_t stream) {
+                      float* out32, int rows, int d, int precision, cudaStream_t stream,
+                      int n_parts, long long part_stride, const float* bias, const void* res16_) {
+  const auto* res16 = static_cast<const uint16_t*>(res16_);
   if (rows <= 0) return;
   HMI_CHECK(d % 128 == 0 && d <= 2048, HMI_CONFIG_ERROR, "layernorm: d must be a multiple of 128");
   const int blocks = (rows + 7) / 8;
@@ -571,9 +609,9 @@ void launch_layernorm(const float* y, const float* gamma, const float* beta, voi
 #define HMI_LN_CASE(VV)                                                                       \
   case VV:                                                                                    \
     if (precision == 1)                                                                       \
-      layernorm_kernel<VV, true><<<blocks, 256, 0, stream>>>(y, gamma, beta, o16, out32, rows); \
+      layernorm_kernel<VV, true><<<blocks, 256, 0, stream>>>(y, gamma, beta, o16, out32, rows, n_parts, part_stride, bias, res16); \
     else                                                                                      \
-      layernorm_kernel<VV, false><<<blocks, 256, 0, stream>>>(y, gamma, beta, o16, out32, rows); \
+      layernorm_kernel<VV, false><<<blocks, 256, 0, stream>>>(y, gamma, beta, o16, out32, rows, n_parts, part_stride, bias, res16); \
     break;
   switch (d / 128) {
     HMI_LN_CASE(1) HMI_LN_CASE(2) HMI_LN_CASE(3) HMI_LN_CASE(4) HMI_LN_CASE(5) HMI_LN_CASE(6)
