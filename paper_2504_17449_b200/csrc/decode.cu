@@ -251,12 +251,22 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
   double acc[kTopK];
 #pragma unroll
   for (int k = 0; k < kTopK; ++k) acc[k] = 0.0;
-  for (int i = threadIdx.x; i < A.d; i += blockDim.x) {
-    const double hv = static_cast<double>(h[i]);
-    const float* wr = A.w + static_cast<long long>(i) * A.V;
+  if (A.wT) {  // same order of sums per thread; the weights read from contiguous rows
+    for (int i = threadIdx.x; i < A.d; i += blockDim.x) {
+      const double hv = static_cast<double>(h[i]);
 #pragma unroll
-    for (int k = 0; k < kTopK; ++k) {
-      if (cj[k] >= 0) acc[k] += hv * static_cast<double>(__ldg(wr + cj[k]));
+      for (int k = 0; k < kTopK; ++k) {
+        if (cj[k] >= 0) acc[k] += hv * static_cast<double>(__ldg(A.wT + static_cast<long long>(cj[k]) * A.d + i));
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < A.d; i += blockDim.x) {
+      const double hv = static_cast<double>(h[i]);
+      const float* wr = A.w + static_cast<long long>(i) * A.V;
+#pragma unroll
+      for (int k = 0; k < kTopK; ++k) {
+        if (cj[k] >= 0) acc[k] += hv * static_cast<double>(__ldg(wr + cj[k]));
+      }
     }
   }
   __shared__ double red8[kTopK][kArgThreads / 32];

@@ -24,6 +24,7 @@ struct LmArgmaxArgs {
   const float* h32 = nullptr;     // [n][d] f32 final rows
   int d = 0;
   const float* w = nullptr;       // [d][V] f32 head weights (reference layout)
+  const float* wT = nullptr;      // optional [V][d] f32 transpose (coalesced candidate reads)
   const float* bias = nullptr;    // [V] f32
   const int32_t* req_head = nullptr;  // optional: only requests bound to `head`
   int head = -1;

@@ -360,6 +360,7 @@ struct Ctx {
     int V = 0, V_pad = 0;
     uint16_t* w16 = nullptr;
     float* bias = nullptr;
+    float* wT = nullptr;  // [V][d] f32: the exact weights per candidate column, contiguous
     GemmPlan plan;
   };
   std::map<int, LmHead> lm_heads;
@@ -492,6 +493,7 @@ Ctx::~Ctx() {
   for (auto& [id, h] : lm_heads) {
     if (h.w16) cudaFree(h.w16);
     if (h.bias) cudaFree(h.bias);
+    if (h.wT) cudaFree(h.wT);
   }
   for (auto& s : stg) {
     for (void* p : {static_cast<void*>(s.inst), static_cast<void*>(s.tokens),
@@ -1178,6 +1180,7 @@ void Ctx::launch_lm_head(uint32_t n_req, int S, const LmHead& lm, int wide_head,
   a.d = d;
   a.w = d_head_arena.p + h_head_off[wide_head];
   a.bias = a.w + static_cast<size_t>(d) * lm.V;
+  a.wT = lm.wT;
   if (gen) {
     // the prompt's tokens start the generated sequences; token 1 lands at position len
     HMI_CUDA(cudaMemcpy2DAsync(gen_tokens.p, static_cast<size_t>(gen_stride) * 4, d_tokens.p,
@@ -1234,6 +1237,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
   am.h32 = hdec32.p;
   am.d = d;
   am.w = d_head_arena.p + h_head_off[wide_head];
+  am.wT = lm.wT;
   am.bias = am.w + static_cast<size_t>(d) * lm.V;
   am.gen_tokens = gen_tokens.p;
   am.tok_stride = gen_stride;
@@ -2320,8 +2324,16 @@ int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, ui
       h.V_pad = static_cast<int>((labels + 255) / 256 * 256);
       const size_t dd = static_cast<size_t>(c.d);
       std::vector<uint16_t> wt(static_cast<size_t>(h.V_pad) * dd, 0);
+      std::vector<float> wtf(static_cast<size_t>(labels) * dd);
       for (size_t i = 0; i < dd; ++i)
-        for (size_t j = 0; j < labels; ++j) wt[j * dd + i] = f2h(w[i * labels + j], static_cast<int>(c.opt.precision));
+        for (size_t j = 0; j < labels; ++j) {
+          wt[j * dd + i] = f2h(w[i * labels + j], static_cast<int>(c.opt.precision));
+          wtf[j * dd + i] = w[i * labels + j];
+        }
+      // f32 transpose for the candidates' f64 rescoring: a column of the reference layout is
+      // one contiguous row here (coalesced, instead of d scattered 4-byte reads V apart)
+      HMI_CUDA(cudaMalloc(&h.wT, wtf.size() * 4));
+      HMI_CUDA(cudaMemcpy(h.wT, wtf.data(), wtf.size() * 4, cudaMemcpyHostToDevice));
       std::vector<float> bp(h.V_pad, 0.f);
       std::memcpy(bp.data(), b, labels * 4);
       HMI_CUDA(cudaMalloc(&h.w16, wt.size() * 2));
