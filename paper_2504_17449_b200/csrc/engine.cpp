@@ -1341,6 +1341,15 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
     return;
   }
   const auto key = std::make_tuple(n, S, wide_head, tables_epoch);
+  for (auto g = dec_graphs.begin(); g != dec_graphs.end();) {  // graphs of replaced table state
+    if (std::get<3>(g->first) != tables_epoch) {
+      HMI_CUDA(cudaStreamSynchronize(s));
+      cudaGraphExecDestroy(g->second);
+      g = dec_graphs.erase(g);
+    } else {
+      ++g;
+    }
+  }
   auto it = dec_graphs.find(key);
   if (it == dec_graphs.end()) {
     cudaGraph_t g = nullptr;
