@@ -398,3 +398,31 @@ def test_gpu_bulk_registration(tmp_path):
         assert np.array_equal(got.scores, want.scores), mode
         eng.close()
     w.eng.close()
+
+
+@pytest.mark.gpu
+def test_gpu_streamed_plt1_empty_branch(tmp_path):
+    """An empty branch (derive_branch at alpha 0 keeps no keys) streams in as a valid version:
+    requests routed to it retrieve through its parent exactly as through the parent itself."""
+    from paper_2504_17449_b200 import engine as E
+
+    g = np.load(GOLD)
+    cfg = oracle.Config(*[int(x) for x in g["cfg"]])
+    mc = E.model_config(*oracle.astuple(cfg))
+    empty = {"key_len": np.zeros(0, np.uint32), "keys": np.zeros((0, 3), np.uint32),
+             "freq": np.zeros(0, np.uint64), "reps": np.zeros((0, cfg.hidden_size), np.float32)}
+    p = str(tmp_path / "empty.plt1")
+    plot.save_plt1(empty, p, 1, 0, "odd-label", 0)
+    n = len(g["lens"])
+    outs = []
+    for version in (0, 1):
+        eng = E.GpuEngine(mc, E.generate_higher(mc), max_batch=n, max_seq=g["tokens"].shape[1],
+                          bottleneck=8, max_labels=5, max_tasks=1, max_versions=4)
+        eng.upload_table(0, 0xFFFFFFFF, g["t0_key_len"], g["t0_keys"], g["t0_reps"])
+        assert eng.upload_plt1(p) == (1, 0)
+        eng.register_task(0, E.generate_adapter(mc, 8, 3))
+        eng.register_head(0, 0, *E.generate_head(cfg.hidden_size, 5, 4))
+        eng.bind_instance(0, version, 0, 0)
+        outs.append(eng.infer_batch(np.zeros(n, np.uint32), g["tokens"], g["lens"]).scores)
+        eng.close()
+    assert np.array_equal(outs[0], outs[1])
