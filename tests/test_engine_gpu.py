@@ -340,6 +340,30 @@ def test_base_parity(n_req):
     w.eng.close()
 
 
+def test_full_size_batch_composition_invariance():
+    """BASELINE's full C2 batch (256 requests x 128 tokens, hBERT-base, r = 64) against a
+    size-independent property: each request's scores do not depend on the batch it rides in.
+    The full batch, its two halves in swapped order, and a reversed permutation give the same
+    scores bit for bit (rows are independent through every kernel; the GEMM tile order, the
+    wave-tail split and the pipelined copies must not leak across requests)."""
+    w = World(oracle.BASE, n_tasks=64, r=64, labels=8, max_batch=256,
+              branches=tuple((0, 60) for _ in range(8)), n_hot=64, n_bi=400, n_tri=400)
+    inst, toks, lens = w.requests(71, 256, 128, min_len=1)
+    full = w.eng.infer_batch(inst, toks, lens)
+    lo = w.eng.infer_batch(inst[128:], toks[128:], lens[128:])
+    hi = w.eng.infer_batch(inst[:128], toks[:128], lens[:128])
+    assert np.array_equal(np.concatenate([hi.scores, lo.scores]), full.scores)
+    perm = np.arange(256)[::-1]
+    rev = w.eng.infer_batch(inst[perm], toks[perm], lens[perm])
+    assert np.array_equal(rev.scores[perm], full.scores)
+    assert np.array_equal(rev.labels[perm], full.labels)
+    # and a spot check of eight of them against the oracle
+    pick = np.arange(0, 256, 32)
+    ref, _, _ = w.oracle_batch(inst[pick], toks[pick], lens[pick], threads=8)
+    assert logit_error(full.scores[pick], ref) <= TOL
+    w.eng.close()
+
+
 def test_large_parity_three_level_tree():
     """C5 shapes (hBERT-large: d=1024, 16 heads, 12 higher layers, ffn 4096, r=64): the fused
     adapter at d=1024 (16 row-statistics partials), a 3-level domain tree."""
