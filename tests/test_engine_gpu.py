@@ -364,6 +364,28 @@ def test_full_size_batch_composition_invariance():
     w.eng.close()
 
 
+@pytest.mark.parametrize("mode", [E.MODE_SYNC, E.MODE_FINE])
+def test_full_size_swapping_is_invisible(mode):
+    """C2 shapes with a slot pool holding 20 of 64 tenants: adapters stream in and out
+    between (sync) or inside (fine, per layer) batches, and every score equals the all-resident
+    engine's bit for bit."""
+    kw = dict(n_tasks=64, r=64, labels=8, max_batch=256, branches=tuple((0, 60) for _ in range(8)),
+              n_hot=64, n_bi=400, n_tri=400)
+    ref = World(oracle.BASE, **kw)
+    layer_bytes = (768 * 64 * 2 + 64 + 768) * 4
+    small = World(oracle.BASE, pool_bytes=20 * oracle.BASE.higher_layers * layer_bytes,
+                  pipeline_mode=mode, **kw)
+    for k in range(8):  # each batch: 16 tenants (its working set), the sets rotating over all 64
+        inst, toks, lens = ref.requests(81 + k, 96, 128, min_len=1)
+        inst = ((np.arange(96) % 16) + 16 * (k % 4) + (k // 4) * 8) % 64
+        a = ref.eng.infer_batch(inst.astype(np.uint32), toks, lens)
+        b = small.eng.infer_batch(inst.astype(np.uint32), toks, lens)
+        assert np.array_equal(a.scores, b.scores), k
+    assert small.eng.pool_stats()["bytes_copied"] > ref.eng.pool_stats()["bytes_copied"]  # re-loads
+    ref.eng.close()
+    small.eng.close()
+
+
 def test_large_parity_three_level_tree():
     """C5 shapes (hBERT-large: d=1024, 16 heads, 12 higher layers, ffn 4096, r=64): the fused
     adapter at d=1024 (16 row-statistics partials), a 3-level domain tree."""
