@@ -228,7 +228,10 @@ int hmi_gpu_debug_routing(hmi_gpu_ctx* ctx, int32_t* version, int32_t* task, int
  * the sub-gram level; -1 / 0 where unused. Arrays are [n_req x S x max_fragment]
  * with S = the batch's padded length (returned in *S).                        */
 int hmi_gpu_debug_gather(hmi_gpu_ctx* ctx, int32_t* rows, int32_t* levels, uint32_t* S);
-/* flags bit0: capture the f64 retrieval output h0 of the next batches.        */
+/* flags bit0: capture the f64 retrieval output h0 of the next batches;       */
+/*       bit1: materialise the last layer's normalised rows (debug_hidden);   */
+/*       bit2: decode steps as eager launches instead of the captured graph   */
+/*             (the tests compare the two).                                   */
 int hmi_gpu_set_debug(hmi_gpu_ctx* ctx, uint32_t flags);
 int hmi_gpu_debug_h0(hmi_gpu_ctx* ctx, double* out);           /* [n_req x S x d] */
 int hmi_gpu_debug_hidden(hmi_gpu_ctx* ctx, float* out);        /* final f32 rows */

@@ -241,164 +241,6 @@ __global__ void __launch_bounds__(256, 2) attention_kernel(const uint16_t* __res
   }
 }
 
-// ---------------------------------------------------------------------------
-// S == 128 fast path: persistent CTAs walk (request, head) items; thread 0 TMA-loads
-// the next item's Q/K/V tiles (128 rows x 128 B each, SWIZZLE_128B) into the second
-// smem buffer while 8 warps compute the current one; the output tile is staged in
-// the consumed Q buffer and TMA-stored. Single-pass softmax (all 128 keys resident).
-// ---------------------------------------------------------------------------
-constexpr int kTile = 128 * 128;            // bytes of one 128 x 64 16-bit tile
-constexpr int kAttnBuf = 3 * kTile;         // Q, K, V
-
-// byte offset of 16-byte chunk `chunk` of row r inside a SWIZZLE_128B tile
-__device__ __forceinline__ uint32_t sw128(int r, int chunk) {
-  return static_cast<uint32_t>(r * 128 + ((chunk ^ (r & 7)) << 4));
-}
-
-template <bool kBf16>
-__global__ void __launch_bounds__(256, 2) attention_s128_kernel(
-    const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_ctx,
-    const int* __restrict__ lens, int n_items, int heads, int d, int causal, float scale_log2) {
-  extern __shared__ uint8_t att_raw[];
-  uint8_t* base = att_raw + ((1024 - (static_cast<uint32_t>(__cvta_generic_to_shared(att_raw)) & 1023)) & 1023);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 2 * kAttnBuf);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, tq = lane & 3;
-
-  auto issue = [&](int item, int buf) {
-    const int b = item / heads, h = item - b * heads;
-    uint8_t* dst = base + buf * kAttnBuf;
-    mbar_arrive_expect_tx(&bar[buf], kAttnBuf);
-    tma_load_2d(dst, &map_qkv, &bar[buf], h * 64, b * 128);
-    tma_load_2d(dst + kTile, &map_qkv, &bar[buf], d + h * 64, b * 128);
-    tma_load_2d(dst + 2 * kTile, &map_qkv, &bar[buf], 2 * d + h * 64, b * 128);
-  };
-  if (tid == 0) {
-    tma_prefetch_desc(&map_qkv);
-    tma_prefetch_desc(&map_ctx);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0 && static_cast<int>(blockIdx.x) < n_items) issue(blockIdx.x, 0);
-  uint32_t phase0 = 0, phase1 = 0;
-  int k = 0;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
-    const int buf = k & 1;
-    const int next = item + gridDim.x;
-    if (tid == 0 && next < n_items) {
-      tma_store_wait_read<0>();  // the previous output store has read buffer buf ^ 1
-      issue(next, buf ^ 1);
-    }
-    if (buf == 0) {
-      mbar_wait(&bar[0], phase0);
-      phase0 ^= 1;
-    } else {
-      mbar_wait(&bar[1], phase1);
-      phase1 ^= 1;
-    }
-    const uint8_t* Q = base + buf * kAttnBuf;
-    const uint8_t* K = Q + kTile;
-    const uint8_t* V = Q + 2 * kTile;
-    const int b = item / heads, h = item - b * heads;
-    const int valid = lens[b];
-    const int qrow_a = warp * 16 + g;  // this thread's rows: qrow_a, qrow_a + 8
-    const int lim_a = causal ? qrow_a + 1 : valid;
-    const int lim_b = causal ? qrow_a + 9 : valid;
-
-    uint32_t qf[4][4];
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      const int r = warp * 16 + (lane & 15);
-      ldsm_x4(qf[ks], Q + sw128(r, ks * 2 + (lane >> 4)));
-    }
-    // S = Q K^T over all 128 keys (16 n tiles of 8)
-    float s[16][4];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
-#pragma unroll
-    for (int np = 0; np < 8; ++np) {
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        uint32_t bf[4];
-        const int n = np * 16 + (lane & 7) + ((lane >> 4) << 3);
-        ldsm_x4(bf, K + sw128(n, ks * 2 + ((lane >> 3) & 1)));
-        mma16816<kBf16>(s[2 * np], qf[ks], bf[0], bf[1]);
-        mma16816<kBf16>(s[2 * np + 1], qf[ks], bf[2], bf[3]);
-      }
-    }
-    float mx_a = -INFINITY, mx_b = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      const int key = nt * 8 + 2 * tq;
-      s[nt][0] = key < lim_a ? s[nt][0] * scale_log2 : -INFINITY;
-      s[nt][1] = key + 1 < lim_a ? s[nt][1] * scale_log2 : -INFINITY;
-      s[nt][2] = key < lim_b ? s[nt][2] * scale_log2 : -INFINITY;
-      s[nt][3] = key + 1 < lim_b ? s[nt][3] * scale_log2 : -INFINITY;
-      mx_a = fmaxf(mx_a, fmaxf(s[nt][0], s[nt][1]));
-      mx_b = fmaxf(mx_b, fmaxf(s[nt][2], s[nt][3]));
-    }
-    mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 1));
-    mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 2));
-    mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 1));
-    mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 2));
-    const float base_a = mx_a == -INFINITY ? 0.f : mx_a;
-    const float base_b = mx_b == -INFINITY ? 0.f : mx_b;
-    float l_a = 0.f, l_b = 0.f;
-#pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      s[nt][0] = exp2f(s[nt][0] - base_a);
-      s[nt][1] = exp2f(s[nt][1] - base_a);
-      s[nt][2] = exp2f(s[nt][2] - base_b);
-      s[nt][3] = exp2f(s[nt][3] - base_b);
-      l_a += s[nt][0] + s[nt][1];
-      l_b += s[nt][2] + s[nt][3];
-    }
-    float o[8][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {  // 16 keys per step
-      uint32_t pa[4];
-      pa[0] = pack2<kBf16>(s[2 * ks][0], s[2 * ks][1]);
-      pa[1] = pack2<kBf16>(s[2 * ks][2], s[2 * ks][3]);
-      pa[2] = pack2<kBf16>(s[2 * ks + 1][0], s[2 * ks + 1][1]);
-      pa[3] = pack2<kBf16>(s[2 * ks + 1][2], s[2 * ks + 1][3]);
-#pragma unroll
-      for (int np = 0; np < 4; ++np) {
-        uint32_t bf[4];
-        const int kr = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        ldsm_x4_t(bf, V + sw128(kr, np * 2 + (lane >> 4)));
-        mma16816<kBf16>(o[2 * np], pa, bf[0], bf[1]);
-        mma16816<kBf16>(o[2 * np + 1], pa, bf[2], bf[3]);
-      }
-    }
-    l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
-    l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
-    l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
-    l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
-    const float inv_a = l_a > 0.f ? 1.f / l_a : 0.f;
-    const float inv_b = l_b > 0.f ? 1.f / l_b : 0.f;
-    // stage O in this warp's own (already consumed) Q rows, swizzled like the TMA tile
-    uint8_t* O = base + buf * kAttnBuf;
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      *reinterpret_cast<uint32_t*>(O + sw128(qrow_a, nt) + tq * 4) =
-          pack2<kBf16>(o[nt][0] * inv_a, o[nt][1] * inv_a);
-      *reinterpret_cast<uint32_t*>(O + sw128(qrow_a + 8, nt) + tq * 4) =
-          pack2<kBf16>(o[nt][2] * inv_b, o[nt][3] * inv_b);
-    }
-    fence_proxy_async_smem();
-    __syncthreads();  // all warps are done with Q/K/V of this buffer and O is staged
-    if (tid == 0) {
-      tma_store_2d(&map_ctx, O, h * 64, b * 128);
-      tma_store_commit();
-    }
-  }
-  if (tid == 0) tma_store_wait_all<0>();
-}
-
 }  // namespace
 
 AttnPlan make_attention_plan(const void* qkv, void* ctx, int max_rows, int d, int precision) {
@@ -412,35 +254,6 @@ AttnPlan make_attention_plan(const void* qkv, void* ctx, int max_rows, int d, in
   p.d = d;
   p.precision = precision;
   return p;
-}
-
-void launch_attention_s128(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
-                           cudaStream_t stream) {
-  if (n_req <= 0) return;
-  const float scale_log2 = 1.4426950408889634f / sqrtf(64.0f);
-  const int smem = 2 * kAttnBuf + 1024 + 64;
-  const int items = n_req * heads;
-  const int grid = items < 2 * device_sm_count() ? items : 2 * device_sm_count();
-  static bool configured[2] = {false, false};
-  const int bf = p.precision == 1 ? 1 : 0;
-  if (!configured[bf]) {
-    if (bf) {
-      HMI_CUDA(cudaFuncSetAttribute(attention_s128_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    } else {
-      HMI_CUDA(cudaFuncSetAttribute(attention_s128_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    }
-    configured[bf] = true;
-  }
-  if (bf) {
-    attention_s128_kernel<true><<<grid, 256, smem, stream>>>(p.map_qkv, p.map_ctx, lens, items,
-                                                             heads, p.d, causal, scale_log2);
-  } else {
-    attention_s128_kernel<false><<<grid, 256, smem, stream>>>(p.map_qkv, p.map_ctx, lens, items,
-                                                              heads, p.d, causal, scale_log2);
-  }
-  HMI_CUDA(cudaGetLastError());
 }
 
 void launch_attention(const void* qkv, void* ctx, const int* lens, int n_req, int S, int d,

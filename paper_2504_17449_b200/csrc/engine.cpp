@@ -119,7 +119,6 @@ struct LayerDev {
   uint16_t *wqkv, *wo, *w1, *w2;  // [N][K] 16-bit (transposed from [in x out])
   float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
   GemmPlan qkv, oproj, ad_down, ad_up, ffn1, ffn2;
-  GemmPlan ad_up_ln, ffn2_ln;  // LayerNorm fused into the epilogue (cluster row reduction)
   AdapterPlan adapter;         // fused down + up + skip + residual (adapter.cu), folded LN mode
   // LayerNorm folding (default mode): gamma folded into the consumer's weights, beta.W into
   // its bias, and the per-column sums of the folded 16-bit weights for the mean correction
@@ -210,32 +209,6 @@ void fold_weights(const float* w, size_t in, size_t out, const float* bias, cons
   }
 }
 
-// LN-fused GEMM plan: one cluster of N / bn CTAs per 128-row tile. Per-tile time scales
-// with bn and the number of rounds with ceil(m_tiles / co-resident clusters); pick the
-// N tile minimising rounds x bn.
-GemmPlan best_ln_plan(GemmSpec s, int m_tiles) {
-  GemmPlan best;
-  long best_cost = -1;
-  for (int bn : {256, 192, 128, 64}) {
-    if (s.N % bn || s.N / bn > 8) continue;
-    s.bn = bn;
-    GemmPlan p;
-    try {
-      p = make_gemm_plan(s);
-    } catch (const HmiError&) {
-      continue;  // no kernel instance for this tile width (e.g. smem budget)
-    }
-    const long rounds = (m_tiles + p.max_clusters - 1) / p.max_clusters;
-    const long cost = rounds * bn;
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best = p;
-    }
-  }
-  HMI_CHECK(best_cost >= 0, HMI_CONFIG_ERROR, "no LayerNorm-fused GEMM fits this hidden size");
-  return best;
-}
-
 }  // namespace
 
 struct Ctx {
@@ -292,15 +265,23 @@ struct Ctx {
   uint64_t next_ticket = 0;
   std::vector<void*> cp_dst, cp_src;
   std::vector<size_t> cp_size;
-  bool use_batch_copy = std::getenv("HMI_BATCH_COPY") == nullptr ||
-                        std::string(std::getenv("HMI_BATCH_COPY")) != "0";
+  bool use_batch_copy = true;  // cleared if the driver lacks cudaMemcpyBatchAsync
   std::vector<cudaEvent_t> ev_layer;
   // decode step captured once per (batch shape, head, tables) and replayed with cudaGraphLaunch
-  // (HMI_DECODE_GRAPH=0: eager launches every step)
+  // (debug flag 4: eager launches every step)
   std::map<std::tuple<int, int, int, uint64_t>, cudaGraphExec_t> dec_graphs;
   uint64_t tables_epoch = 0;
-  bool decode_graph = std::getenv("HMI_DECODE_GRAPH") == nullptr ||
-                      std::string(std::getenv("HMI_DECODE_GRAPH")) != "0";
+  // A captured decode graph holds raw pointers into the reps arena, the head arena, the lm
+  // logits buffer and the lm GEMM plans' tensor maps: anything that reallocates one of them
+  // drops every graph first (they are recaptured on the next generate).
+  void drop_decode_graphs() {
+    if (dec_graphs.empty()) return;
+    HMI_CUDA(cudaStreamSynchronize(compute));
+    for (auto& [k, g] : dec_graphs) cudaGraphExecDestroy(g);
+    dec_graphs.clear();
+    ++tables_epoch;
+  }
+
   // peer rebalancing: export pins per task, peer arenas opened over CUDA IPC, bytes moved
   std::map<uint32_t, int> exported;
   std::map<std::string, void*> ipc_open;
@@ -319,15 +300,17 @@ struct Ctx {
   Staging stg[kStaging];
   int stg_next = 0;
   std::deque<Inflight> inflight;
+  int sticky_err = 0;  // first device-side error of a batch retired without a waiter
+  void raise_sticky() {
+    const int e = sticky_err;
+    sticky_err = 0;
+    if (e) throw HmiError(e, "device-side error in an earlier batch (status " + std::to_string(e) + ")");
+  }
   // last batch (introspection)
   uint32_t last_n = 0, last_S = 0;
   uint32_t debug_flags = 0;
-  // LayerNorm placement: 0 folded into the consumers (default), 1 separate K4 kernels
-  // (HMI_LN_MODE=unfused), 2 cluster-reduced GEMM epilogues (HMI_LN_MODE=cluster)
-  int ln_mode = 0;
-  bool attn_tc = true;  // tcgen05 attention for padded length 128 (HMI_ATTN=mma selects mma.sync)
-  // one fused adapter kernel per layer (folded LN mode, r <= 64); HMI_ADAPTER=gemm selects the
-  // two grouped GEMMs
+  // one fused adapter kernel per layer when r <= 64 and d % 128 == 0, else the two
+  // tenant-grouped GEMMs
   bool adapter_fused = true;
   DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
   static constexpr int kStatsLd = kStatsStride;
@@ -350,7 +333,7 @@ struct Ctx {
   std::vector<DecPlans> dec;
   // decode FFN2 split-K: the M = 256 GEMM has only d / 64 x 2 tiles, so its K = f loop is cut
   // into slices run as concurrent branches (aux streams; graph branches when captured) and the
-  // LayerNorm after it sums the partials (HMI_DECODE_SPLIT=1 disables)
+  // LayerNorm after it sums the partials
   int dec_splits = 1;
   DevBuf<float> dec_part, dec_zero;
   std::vector<cudaStream_t> dec_aux;
@@ -632,7 +615,7 @@ void Ctx::build_plans() {
     s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
     s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, m_tiles, sms, true);
     w.ffn2 = make_gemm_plan(s);
-    if (ln_mode == 0) {
+    {
       // LayerNorm folding. Buffers hold PRE-norm rows: x16 = y1 (pre-LN1), h16 = y2 (pre-LN2
       // of layer l-1; h0 for l = 0); d_stats1/2 their partial row sums.
       const LayerDev* prev = l > 0 ? &layers[l - 1] : nullptr;
@@ -710,34 +693,6 @@ void Ctx::build_plans() {
         g.bn = stats2_bn;
         w.ffn2 = make_gemm_plan(g);
       }
-      continue;
-    }
-    // fused variants: adapter up + skip + residual + LN1 -> x16; FFN2 + residual + LN2 -> h16
-    if (ln_mode == 2) {
-      GemmSpec u;
-      u.precision = prec;
-      u.a_rows = max_rows;
-      u.a = mid16.p; u.a_ld = r_pad; u.K = r_pad;
-      u.b = arena.p + off_wu; u.N = d; u.groups = static_cast<int>(n_slots); u.b_ld = r_pad;
-      u.b_group_stride_bytes = slot_bytes;
-      u.bias = reinterpret_cast<const float*>(arena.p + off_bu);
-      u.bias_group_stride = static_cast<long long>(slot_bytes / 4);
-      u.tile_slot = d_tile_slot.p + static_cast<size_t>(l) * tile_stride;
-      u.res0 = a16.p; u.res1 = h16.p; u.res_ld = d;
-      u.c = x16.p; u.c_ld = d; u.epi = kEpiRes2 | kEpiLN | kEpiResTma;
-      u.ln_gamma = w.ln1g; u.ln_beta = w.ln1b;
-      w.ad_up_ln = best_ln_plan(u, m_tiles);
-      GemmSpec g;
-      g.precision = prec;
-      g.a_rows = max_rows;
-      g.a = ffn16.p; g.a_ld = f; g.K = f;
-      g.b = w.w2; g.N = d; g.groups = 1; g.b_ld = f; g.b_group_stride_bytes = size_t(d) * f * 2;
-      g.bias = w.b2; g.res0 = x16.p; g.res_ld = d;
-      g.c = h16.p; g.c_ld = d;
-      g.epi = kEpiRes1 | kEpiLN | (l == L - 1 ? kEpiOut2F32 : 0);
-      g.c2 = h32.p; g.c2_ld = d;
-      g.ln_gamma = w.ln2g; g.ln_beta = w.ln2b;
-      w.ffn2_ln = best_ln_plan(g, m_tiles);
     }
   }
   // single-row decode steps: unfolded weights, explicit LayerNorms, 1-CTA tiles
@@ -819,7 +774,15 @@ void Ctx::reap(bool all) {
       break;
     }
     pool->unpin(f.tasks);
-    stg[f.staging].busy = false;
+    Staging& st = stg[f.staging];
+    // a finished batch nobody waits on (infer_batch_device): latch its device-side error
+    // for hmi_gpu_synchronize / the next asynchronous submit; synchronous callers have read
+    // and cleared theirs already
+    if (!st.held) {
+      if (*st.err != 0 && sticky_err == 0) sticky_err = *st.err;
+      *st.err = 0;
+    }
+    st.busy = false;
     inflight.pop_front();
   }
 }
@@ -909,19 +872,34 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
       }
     }
   };
-  auto absorb_pending = [&]() {
-    for (const PoolFree& fr : pool->take_pending_freed()) {
-      delta.push_back(static_cast<int32_t>(fr.task * L + fr.layer));
-      delta.push_back(-1);
+  // Every decision the pool makes for this batch is absorbed, including those of an attempt
+  // that failed on pinned blockers (take_partial): the retry sees those tasks as hits, so
+  // their copies and slot-table deltas must come from here. If submit throws before the
+  // batch is enqueued, the guard rolls the placements back (their copies were never issued)
+  // and releases the pins.
+  struct Undo {
+    SlotPool* pool;
+    std::vector<std::pair<uint32_t, uint32_t>> placed;  // (task, layer)
+    const std::vector<uint32_t>* pinned = nullptr;
+    bool armed = true;
+    ~Undo() {
+      if (!armed) return;
+      if (pinned) pool->unpin(*pinned);
+      for (auto it = placed.rbegin(); it != placed.rend(); ++it) pool->unload(it->first, it->second);
     }
+  } undo{pool.get(), {}};
+  auto absorb_all = [&](std::vector<PoolRecord>&& recs, int layer_tag) {
+    for (const auto& rec : recs)
+      for (const PoolLoad& ld : rec.loads) undo.placed.push_back({rec.task, ld.layer});
+    absorb(recs, layer_tag);
   };
   if (!fine) {
     for (;;) {
       try {
-        auto recs = pool->ensure_resident(uniq);
-        absorb(recs, -1);
+        absorb_all(pool->ensure_resident(uniq), -1);
         break;
       } catch (const HmiError& e) {
+        absorb_all(pool->take_partial(), -1);
         // a pinned in-flight working set blocks the load: retire the oldest batch and retry
         if (e.code != HMI_CAPACITY_ERROR || inflight.empty()) throw;
         HMI_CUDA(cudaEventSynchronize(inflight.front().done));
@@ -931,10 +909,16 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   } else {
     for (int l = 0; l < L; ++l) {
       for (;;) {
-        auto recs = pool->try_ensure_layer_resident(uniq, static_cast<uint32_t>(l));
-        absorb_pending();
+        std::optional<std::vector<PoolRecord>> recs;
+        try {
+          recs = pool->try_ensure_layer_resident(uniq, static_cast<uint32_t>(l));
+        } catch (...) {
+          absorb_all(pool->take_partial(), l);
+          throw;
+        }
+        absorb_all(pool->take_partial(), l);
         if (recs) {
-          absorb(*recs, l);
+          absorb_all(std::move(*recs), l);
           break;
         }
         if (inflight.empty()) {
@@ -946,6 +930,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     }
   }
   pool->pin(uniq);
+  undo.pinned = &uniq;
 
   // ---- staging buffer for this batch
   const int si = stg_next;
@@ -1063,14 +1048,11 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   });
   for (int l = 0; l < L; ++l) traced(kStageCompute, l, kWorkerCompute, s, [&] {
     LayerDev& w = layers[l];
-    const bool last = l == L - 1;
     timed(P_QKV, s, [&] { launch_gemm(w.qkv, rows, s); });
     timed(P_ATTN, s, [&] {
       const AttnPlan& ap = attn[kv ? l : 0];
-      if (S == 128 && attn_tc) {
+      if (S == 128) {
         launch_attention_tc(ap, d_lens.p, static_cast<int>(n_req), heads, causal, s);
-      } else if (S == 128) {
-        launch_attention_s128(ap, d_lens.p, static_cast<int>(n_req), heads, causal, s);
       } else {
         launch_attention(qkv_at(l), ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal,
                          prec, s);
@@ -1078,28 +1060,14 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     });
     timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
     if (fine) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
-    if (ln_mode == 0 && adapter_fused) {
+    if (adapter_fused) {
       timed(P_AD_UP, s, [&] { launch_adapter(w.adapter, rows, s); });
-    } else {
+    } else {  // r > 64 or d not a multiple of 128: the two tenant-grouped GEMMs
       timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
-    }
-    if (ln_mode == 0) {
-      if (!adapter_fused) timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
-      timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
-      timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
-    } else if (ln_mode == 2) {
-      timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up_ln, rows, s); });
-      timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
-      timed(P_FFN2, s, [&] { launch_gemm(w.ffn2_ln, rows, s); });
-    } else {
       timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
-      timed(P_LN1, s, [&] { launch_layernorm(y32.p, w.ln1g, w.ln1b, x16.p, nullptr, rows, d, prec, s); });
-      timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
-      timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
-      timed(P_LN2, s, [&] {
-        launch_layernorm(y32.p, w.ln2g, w.ln2b, h16.p, last ? h32.p : nullptr, rows, d, prec, s);
-      });
     }
+    timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
+    timed(P_FFN2, s, [&] { launch_gemm(w.ffn2, rows, s); });
   });
   HeadDev H;
   H.arena = d_head_arena.p;
@@ -1112,15 +1080,14 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     HMI_CUDA(cudaMemsetAsync(scores_dst, 0, static_cast<size_t>(n_req) * opt.max_labels * 4, s));
   }
   if (!gen) timed(P_HEAD, s, [&] {
-    if (ln_mode == 0) {  // the head applies the last layer's LN2 to its pre-norm row
-      H.y16 = h16.p;
-      H.ln_g = layers[L - 1].ln2g;
-      H.ln_b = layers[L - 1].ln2b;
-      H.bf16 = prec;
-      if (debug_flags & 2) {
-        launch_normalize_rows(h16.p, d_stats2.p, stats2_n, 1.0f / d, layers[L - 1].ln2g,
-                              layers[L - 1].ln2b, h32.p, rows, d, prec, s);
-      }
+    // the head applies the last layer's LN2 to its pre-norm row
+    H.y16 = h16.p;
+    H.ln_g = layers[L - 1].ln2g;
+    H.ln_b = layers[L - 1].ln2b;
+    H.bf16 = prec;
+    if (debug_flags & 2) {
+      launch_normalize_rows(h16.p, d_stats2.p, stats2_n, 1.0f / d, layers[L - 1].ln2g,
+                            layers[L - 1].ln2b, h32.p, rows, d, prec, s);
     }
     launch_head(H, h32.p, d_req_head.p, d_lens.p, static_cast<int>(n_req), S, d,
                 static_cast<int>(opt.max_labels), scores_dst, labels_dst, d_tags.p, s);
@@ -1152,8 +1119,9 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   }
   st.busy = true;
   inflight.push_back(Inflight{st.done, si, uniq});
+  undo.armed = false;
   last_n = n_req;
-  const uint64_t per_layer = ln_mode == 1 ? 9ull : (ln_mode == 0 && adapter_fused) ? 6ull : 7ull;
+  const uint64_t per_layer = adapter_fused ? 6ull : 7ull;
   // fetch_inputs + route + retrieve (+ apply_deltas) + layers + head
   n_launches += (delta.empty() ? 0 : 1) + 3 + (gen ? 0 : 1) + per_layer * L;
   if (wide_head >= 0) n_launches += 3 + (gen ? (n_new - 1ull) * (3 + 7ull * L) : 0);
@@ -1169,7 +1137,7 @@ void Ctx::launch_lm_head(uint32_t n_req, int S, const LmHead& lm, int wide_head,
   cudaStream_t s = compute;
   const int prec = static_cast<int>(opt.precision);
   const int Mp = static_cast<int>((n_req + 127) / 128 * 128);
-  launch_lm_gather(ln_mode == 0 ? h16.p : nullptr, h32.p, layers[L - 1].ln2g, layers[L - 1].ln2b,
+  launch_lm_gather(h16.p, h32.p, layers[L - 1].ln2g, layers[L - 1].ln2b,
                    d_lens.p, static_cast<int>(n_req), S, d, prec, hdec32.p, hdec16.p, s);
   launch_gemm(lm.plan, Mp, s);
   LmArgmaxArgs a;
@@ -1335,7 +1303,8 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
   // device), so the graph removes the per-launch submission and inter-kernel gaps
   if (n_new <= 1) return;
   step(1);
-  const bool graph = decode_graph && !prof && n_new > 2;
+  // debug flag 4 (hmi_gpu_set_debug): eager launches every step (tests compare the two)
+  const bool graph = !(debug_flags & 4) && !prof && n_new > 2;
   if (!graph) {
     for (uint32_t k = 2; k < n_new; ++k) step(k);
     return;
@@ -1564,10 +1533,9 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       c.gen_pos.alloc(Bm);
       c.gen_out.alloc(Bm * T);
       c.gen_logit.alloc(Bm * T);
-      const char* sp_env = std::getenv("HMI_DECODE_SPLIT");
       // three slices measured best for GPT-2 small (10.45k vs 10.35k at two, 10.25k unsplit);
       // fall back to the largest count that divides f into 64-wide K blocks
-      c.dec_splits = sp_env ? std::max(1, std::atoi(sp_env)) : 3;
+      c.dec_splits = 3;
       while (c.dec_splits > 1 && f % (64 * c.dec_splits) != 0) --c.dec_splits;
       if (c.dec_splits > 1) {
         c.dec_part.alloc(static_cast<size_t>(c.dec_splits) * c.Bp * d);
@@ -1642,13 +1610,7 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     c.pool = std::make_unique<SlotPool>(pool_bytes, static_cast<uint32_t>(n_slots64));
     c.arena.alloc(static_cast<size_t>(n_slots64) * c.slot_bytes);
     HMI_CUDA(cudaMemset(c.arena.p, 0, c.arena.n));
-    if (const char* env = std::getenv("HMI_LN_MODE")) {
-      const std::string m(env);
-      c.ln_mode = m == "unfused" ? 1 : m == "cluster" ? 2 : 0;
-    }
-    if (const char* env = std::getenv("HMI_ATTN")) c.attn_tc = std::string(env) != "mma";
     c.adapter_fused = c.r_pad == 64 && c.d % 128 == 0;
-    if (const char* env = std::getenv("HMI_ADAPTER")) c.adapter_fused &= std::string(env) != "gemm";
     c.d_stats1.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.d_stats2.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.build_plans();
@@ -1763,6 +1725,7 @@ static size_t read_parallel(int fd, uint8_t* dst, size_t n, uint64_t off) {
 static void reserve_rep_rows(Ctx& c, uint64_t rows) {
   const size_t need_f = static_cast<size_t>(rows) * c.d;
   if (need_f <= c.d_reps.n) return;
+  c.drop_decode_graphs();
   DevBuf<float> grown;
   grown.alloc(std::max(need_f, c.d_reps.n * 3 / 2 + 1));
   if (c.rep_rows) HMI_CUDA(cudaMemcpy(grown.p, c.d_reps.p, c.rep_rows * c.d * 4, cudaMemcpyDeviceToDevice));
@@ -1778,7 +1741,8 @@ static void commit_version(Ctx& c, uint32_t version_id, uint32_t parent_id, uint
   c.rep_rows += rows;
   c.h_parent[version_id] = parent_id == kNoParent ? -1 : static_cast<int32_t>(parent_id);
   c.upload_plot_hash();
-  ++c.tables_epoch;  // retrieval pointers / hash mask may have changed: recapture decode graphs
+  c.drop_decode_graphs();  // retrieval pointers / hash mask may have changed: recapture
+  ++c.tables_epoch;
 }
 }  // namespace hmi_b200
 
@@ -2309,6 +2273,7 @@ int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, ui
     if (c.h_head_kind[head_idx] >= 0) throw HmiError(HMI_CONFLICT_ERROR, "head already registered");
     const size_t n = static_cast<size_t>(c.d) * labels + labels;
     if (c.head_floats + n > c.d_head_arena.n) {
+      c.drop_decode_graphs();  // graphs read the head arena by address
       DevBuf<float> grown;
       grown.alloc(std::max(c.head_floats + n, c.d_head_arena.n * 3 / 2 + 1024));
       if (c.head_floats)
@@ -2353,6 +2318,7 @@ int hmi_gpu_register_head(hmi_gpu_ctx* ctx, uint32_t head_idx, uint32_t kind, ui
       HMI_CUDA(cudaMemcpy(h.bias, bp.data(), bp.size() * 4, cudaMemcpyHostToDevice));
       const size_t need = static_cast<size_t>(c.Bp) * h.V_pad;
       if (c.lm_logits.n < need) {
+        c.drop_decode_graphs();  // graphs write the logits buffer by address
         c.lm_logits.alloc(need);
         for (auto& [id, o] : c.lm_heads) c.build_lm_plan(o);  // logits buffer moved
       }
@@ -2449,6 +2415,7 @@ int hmi_gpu_infer_batch(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instan
       }
     }
     const int err = *st.err;
+    *st.err = 0;
     std::memcpy(scores, st.scores, static_cast<size_t>(n_req) * c.opt.max_labels * 4);
     std::memcpy(labels, st.labels, n_req * 4);
     if (c.prof) c.prof_collect();
@@ -2565,6 +2532,7 @@ int hmi_gpu_wait_batch(hmi_gpu_ctx* ctx, uint64_t ticket, float* scores, int32_t
     HMI_CUDA(cudaEventSynchronize(st->done));
     st->held = false;
     const int err = *st->err;
+    *st->err = 0;
     if (scores) std::memcpy(scores, st->scores, static_cast<size_t>(st->n_req) * c.opt.max_labels * 4);
     if (labels) std::memcpy(labels, st->labels, st->n_req * 4);
     if (c.prof) c.prof_collect();
@@ -2594,6 +2562,7 @@ int hmi_gpu_generate(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t* instance_
                             cudaMemcpyDeviceToHost));
     }
     const int err = *st.err;
+    *st.err = 0;
     if (c.prof) c.prof_collect();
     c.reap(false);
     if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
@@ -2609,6 +2578,8 @@ int hmi_gpu_infer_batch_device(hmi_gpu_ctx* ctx, uint32_t n_req, const uint32_t*
     Ctx& c = ctx->impl;
     std::lock_guard<std::mutex> lock(c.mu);
     HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(false);
+    c.raise_sticky();
     c.submit(n_req, instance_idx, nullptr, d_tokens, stride, nullptr, d_lens, max_len, d_scores,
              d_labels, nullptr, nullptr);
   });
@@ -2620,15 +2591,10 @@ int hmi_gpu_synchronize(hmi_gpu_ctx* ctx) {
     Ctx& c = ctx->impl;
     std::lock_guard<std::mutex> lock(c.mu);
     HMI_CUDA(cudaSetDevice(c.device));
-    int err = 0;
-    for (auto& f : c.inflight) {
-      HMI_CUDA(cudaEventSynchronize(f.done));
-      if (!err) err = *c.stg[f.staging].err;
-    }
-    c.reap(true);
+    c.reap(true);  // latches the first device-side error of the retired batches
     HMI_CUDA(cudaStreamSynchronize(c.compute));
     if (c.prof) c.prof_collect();
-    if (err) throw HmiError(err, "device-side error in batch (status " + std::to_string(err) + ")");
+    c.raise_sticky();
   });
 }
 
@@ -2794,10 +2760,17 @@ int hmi_pool_op(hmi_pool* pool, int op, uint32_t n, const uint32_t* tasks, uint3
     std::vector<PoolRecord> recs;
     if (n_trace) *n_trace = 0;
     switch (op) {
-      case 0: recs = pool->p->ensure_resident(v); break;
+      case 0:
+        try {
+          recs = pool->p->ensure_resident(v);
+        } catch (...) {
+          pool->p->take_partial();
+          throw;
+        }
+        break;
       case 1: {
         auto r = pool->p->try_ensure_layer_resident(v, layer);
-        pool->p->take_pending_freed();
+        pool->p->take_partial();
         if (!r) {
           if (n_trace) *n_trace = -1;
           return;

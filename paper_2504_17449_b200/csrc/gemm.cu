@@ -57,20 +57,6 @@ KernelFn pick_epi_t(int epi) {
       default: break;
     }
   }
-  if constexpr (!C2) {
-    switch (epi) {
-      case kEpiRes1 | kEpiLN: return kernel_ptr<BN, T | kEpiRes1 | kEpiLN, false>();
-      case kEpiRes2 | kEpiLN: return kernel_ptr<BN, T | kEpiRes2 | kEpiLN, false>();
-      case kEpiRes1 | kEpiLN | kEpiOut2F32:
-        return kernel_ptr<BN, T | kEpiRes1 | kEpiLN | kEpiOut2F32, false>();
-      case kEpiRes2 | kEpiLN | kEpiOut2F32:
-        return kernel_ptr<BN, T | kEpiRes2 | kEpiLN | kEpiOut2F32, false>();
-      case kEpiRes2 | kEpiLN | kEpiResTma:
-        if constexpr (BN <= 192) return kernel_ptr<BN, T | kEpiRes2 | kEpiLN | kEpiResTma, false>();
-        return nullptr;
-      default: break;
-    }
-  }
   return nullptr;
 }
 
@@ -89,13 +75,9 @@ KernelFn pick_kernel(int bn, int epi, bool c2, int* smem_bytes) {
       default: return nullptr;
     }
   }
-  const bool ln = (epi & kEpiLN) != 0;
   const bool rt = (epi & kEpiResTma) != 0;
-#define HMI_SMEM(B)                                                                   \
-  (rt ? (B <= 192 ? (ln ? GemmSmem<(B <= 192 ? B : 64), true, true>::kTotal              \
-                        : GemmSmem<(B <= 192 ? B : 64), false, true>::kTotal)            \
-                  : 0)                                                                    \
-      : ln ? GemmSmem<B, true>::kTotal : GemmSmem<B>::kTotal)
+#define HMI_SMEM(B) \
+  (rt ? (B <= 192 ? GemmSmem<(B <= 192 ? B : 64), true>::kTotal : 0) : GemmSmem<B>::kTotal)
   switch (bn) {
     case 64: *smem_bytes = HMI_SMEM(64); return pick_epi<64, false>(epi);
     case 128: *smem_bytes = HMI_SMEM(128); return pick_epi<128, false>(epi);
@@ -116,14 +98,7 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   HMI_CHECK(s.a_rows % kBlockM == 0, HMI_CONFIG_ERROR, "gemm: A rows must be a multiple of 128");
   GemmPlan p;
   const int epi = s.epi | (s.precision == 1 ? kEpiBf16 : 0);
-  const bool ln = (s.epi & kEpiLN) != 0;
-  const bool c2 = s.cta2 && !ln && s.groups == 1 && s.tile_slot == nullptr && s.bn >= 128;
-  if (ln) {
-    HMI_CHECK(s.N / s.bn >= 1 && s.N / s.bn <= 8, HMI_CONFIG_ERROR,
-              "gemm: LayerNorm epilogue needs N / BN in [1, 8] (one cluster per row block)");
-    HMI_CHECK(s.bn % 64 == 0 && s.ln_gamma && s.ln_beta, HMI_CONFIG_ERROR, "gemm: LN epilogue args");
-    p.cluster_n = s.N / s.bn;
-  }
+  const bool c2 = s.cta2 && s.groups == 1 && s.tile_slot == nullptr && s.bn >= 128;
   p.two_cta = c2;
   p.fn = reinterpret_cast<void*>(pick_kernel(s.bn, epi, c2, &p.smem_bytes));
   HMI_CHECK(p.fn != nullptr, HMI_CONFIG_ERROR, "gemm: unsupported epilogue");
@@ -133,11 +108,10 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
                          CU_TENSOR_MAP_SWIZZLE_128B);
   p.maps.b = make_tmap_3d(s.b, t16, s.K, s.N, s.groups, s.b_ld * 2ull, s.b_group_stride_bytes,
                          kBlockK, c2 ? s.bn / 2 : s.bn, CU_TENSOR_MAP_SWIZZLE_128B);
-  const bool f32 = (s.epi & kEpiOutF32) != 0 && !ln;
+  const bool f32 = (s.epi & kEpiOutF32) != 0;
   p.maps.c = make_tmap_2d(s.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : t16, s.N, s.a_rows,
                          s.c_ld * (f32 ? 4ull : 2ull), f32 ? 32 : 64, 32,
                          CU_TENSOR_MAP_SWIZZLE_128B);
-  p.maps.c2 = p.maps.c;
   p.maps.r0 = p.maps.c;
   p.maps.r1 = p.maps.c;
   if (s.epi & kEpiResTma) {
@@ -149,8 +123,6 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   }
   p.precision = s.precision;
   p.bn = s.bn;
-  p.tail_enabled = std::getenv("HMI_GEMM_TAIL") == nullptr ||
-                   std::string(std::getenv("HMI_GEMM_TAIL")) != "0";
   if (c2) {
     // wave-tail sub-tile widths must stay multiples of 64 columns (the epilogue's store chunk)
     const int g = s.bn / 64;
@@ -163,11 +135,6 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
                                kBlockK, s.bn / (2 * p.tail_s1), CU_TENSOR_MAP_SWIZZLE_128B);
     }
   }
-  if (s.epi & kEpiOut2F32) {
-    HMI_CHECK(s.c2 != nullptr, HMI_CONFIG_ERROR, "gemm: f32 copy output missing");
-    p.maps.c2 = make_tmap_2d(s.c2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, s.N, s.a_rows, s.c2_ld * 4ull,
-                            32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-  }
   p.args = GemmArgs{};
   p.args.N = s.N;
   p.args.K = s.K;
@@ -178,8 +145,6 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.res0 = reinterpret_cast<const __half*>(s.res0);
   p.args.res1 = reinterpret_cast<const __half*>(s.res1);
   p.args.res_ld = s.res_ld;
-  p.args.ln_gamma = s.ln_gamma;
-  p.args.ln_beta = s.ln_beta;
   p.args.stats_out = s.stats_out;
   p.args.stats_ld = s.stats_ld;
   p.args.a_stats = s.a_stats;
@@ -221,31 +186,6 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
                    p.smem_bytes, n);
     }
   }
-  if (ln) {
-    // how many clusters of cluster_n CTAs (each ~210 KB smem) fit at once: GPCs do not
-    // divide evenly, so asking for sms / cluster_n would leave a second wave
-    HMI_CUDA(cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes));
-    if (p.cluster_n > 1) {
-      HMI_CUDA(cudaFuncSetAttribute(p.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.cluster_n * (device_sm_count() / p.cluster_n));
-    cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = p.smem_bytes;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.cluster_n;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, p.fn, &cfg) != cudaSuccess || n <= 0) {
-      cudaGetLastError();
-      n = device_sm_count() / p.cluster_n;
-    }
-    p.max_clusters = n;
-  }
   return p;
 }
 
@@ -269,27 +209,6 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
   a.M = M;
   a.num_m_tiles = M / kBlockM;
   int grid;
-  if (p.cluster_n > 1 || (p.args.ln_gamma && p.cluster_n == 1)) {
-    // LN epilogue: one cluster of cluster_n CTAs per M tile
-    const int per = p.cluster_n;
-    const int clusters_max = p.max_clusters > 0 ? p.max_clusters : device_sm_count() / per;
-    const int clusters = a.num_m_tiles < clusters_max ? a.num_m_tiles : clusters_max;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(clusters * per);
-    cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = p.smem_bytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = per;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    KernelFn fn = reinterpret_cast<KernelFn>(p.fn);
-    HMI_CUDA(cudaLaunchKernelEx(&cfg, fn, p.maps, a));
-    return;
-  }
   a.n_main = 0;
   a.tail_split = 1;
   a.idesc_tail = a.idesc;

@@ -305,196 +305,21 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
   }
 }
 
-// LayerNorm epilogue (kEpiLN): the CTA owns BN of the row's N = cluster_n * BN columns.
-// Pass 1 adds bias (+ residuals) and writes the pre-norm value back into TMEM while
-// accumulating per-row (sum, sum of squares); the two column halves combine in smem,
-// every CTA pushes (mean_c, M2_c) to all cluster peers over DSMEM, and the exact
-// parallel-variance merge gives the row's mean / variance (layer_norm, ops.cpp:92-116,
-// epsilon 1e-5, biased variance). Pass 2 re-reads TMEM, normalises with gamma/beta and
-// TMA-stores 16-bit (and optionally f32) rows.
-template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile_ln(uint32_t t_acc, int mt, int nt, int grp,
-                                                 const GemmArgs& args, const CUtensorMap* map_c,
-                                                 const CUtensorMap* map_c2, uint8_t* stg,
-                                                 uint32_t q, int half, uint32_t lane,
-                                                 float2* partial, float2* stats,
-                                                 uint64_t* stats_bar, uint32_t iter,
-                                                 uint32_t cs, uint32_t rank,
-                                                 const uint8_t* res_smem, uint64_t* res_empty) {
-  constexpr bool kBf16 = (EPI & kEpiBf16) != 0;
-  constexpr bool kResTma = (EPI & kEpiResTma) != 0;
-  constexpr int kCW = 64;
-  static_assert(BN % kCW == 0, "LN epilogue works in 64-column chunks");
-  const float* bias = args.bias + grp * args.bias_slot_stride + nt * BN;
-  const int row_local = static_cast<int>(q) * 32 + static_cast<int>(lane);
-  const int row0 = mt * kBlockM + static_cast<int>(q) * 32;
-  const int row = row0 + static_cast<int>(lane);
-  const bool row_ok = row < args.M;
-  const uint32_t t_row = t_acc + ((q * 32) << 16);
-  // ---- pass 1 (32-column chunks, alternating between the two warps of a lane quarter)
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll 1
-  for (int c = half * 32; c < BN; c += 64) {
-    float v[32];
-    float rv[32];
-    if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
-      // issue the residual loads before touching TMEM
-#pragma unroll
-      for (int i = 0; i < 32; ++i) rv[i] = 0.f;
-      if constexpr (kResTma) {
-        // residual tiles staged by TMA: [res][BN/64 boxes][128 rows x 128 B], SWIZZLE_128B
-        const uint8_t* box = res_smem + (c >> 6) * 16384 + row_local * 128;
-        const int ch0 = (c & 63) >> 3;
-        add_res16_smem<kBf16>(rv, box, ch0, row_local & 7);
-        if constexpr ((EPI & kEpiRes2) != 0) {
-          add_res16_smem<kBf16>(rv, box + (BN / 64) * 16384, ch0, row_local & 7);
-        }
-      } else if (row_ok) {
-        const long long off = static_cast<long long>(row) * args.res_ld + nt * BN + c;
-        add_res16<kBf16, 32>(rv, reinterpret_cast<const uint16_t*>(args.res0) + off);
-        if constexpr ((EPI & kEpiRes2) != 0) {
-          add_res16<kBf16, 32>(rv, reinterpret_cast<const uint16_t*>(args.res1) + off);
-        }
-      }
-    }
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(t_row + c, r);
-    tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
-      v[i] = __uint_as_float(r[i]) + b4.x;
-      v[i + 1] = __uint_as_float(r[i + 1]) + b4.y;
-      v[i + 2] = __uint_as_float(r[i + 2]) + b4.z;
-      v[i + 3] = __uint_as_float(r[i + 3]) + b4.w;
-    }
-    if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += rv[i];
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      s1 += v[i];
-      s2 += v[i] * v[i];
-      r[i] = __float_as_uint(v[i]);
-    }
-    tmem_st_32x32b_x32(t_row + c, r);
-  }
-  tmem_st_wait();
-  if constexpr (kResTma) {  // residual tiles consumed: the producer may stage the next tile's
-    __syncwarp();
-    if (lane == 0) mbar_arrive(res_empty);
-  }
-  // ---- row statistics: halves -> CTA -> cluster
-  if (half == 1) partial[row_local] = make_float2(s1, s2);
-  named_bar_sync(1, 256);
-  const uint32_t buf = iter & 1;
-  if (half == 0) {
-    s1 += partial[row_local].x;
-    s2 += partial[row_local].y;
-    const float mean_c = s1 * (1.0f / BN);
-    const float m2_c = fmaxf(s2 - s1 * mean_c, 0.0f);
-    const uint32_t dst = smem_u32(&stats[(buf * 8 + rank) * 128 + row_local]);
-    const uint32_t bar = smem_u32(&stats_bar[buf]);
-    for (uint32_t p = 0; p < cs; ++p) {
-      st_cluster_f32x2(mapa_shared(dst, p), mean_c, m2_c);
-      mbar_arrive_cluster(mapa_shared(bar, p));
-    }
-  }
-  mbar_wait(&stats_bar[buf], (iter >> 1) & 1);
-  float mean = 0.f;
-  for (uint32_t p = 0; p < cs; ++p) mean += stats[(buf * 8 + p) * 128 + row_local].x;
-  mean /= static_cast<float>(cs);
-  float m2 = 0.f;
-  for (uint32_t p = 0; p < cs; ++p) {
-    const float2 st = stats[(buf * 8 + p) * 128 + row_local];
-    const float dm = st.x - mean;
-    m2 += st.y + static_cast<float>(BN) * dm * dm;
-  }
-  const float inv = 1.0f / sqrtf(m2 / static_cast<float>(cs * BN) + 1e-5f);
-  // ---- pass 2
-  const float* gam = args.ln_gamma + nt * BN;
-  const float* bet = args.ln_beta + nt * BN;
-#pragma unroll 1
-  for (int c = half * kCW; c < BN; c += 2 * kCW) {
-    float v[kCW];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < kCW; i += 4) {
-      const float4 g4 = __ldg(reinterpret_cast<const float4*>(gam + c + i));
-      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bet + c + i));
-      v[i] = (v[i] - mean) * inv * g4.x + b4.x;
-      v[i + 1] = (v[i + 1] - mean) * inv * g4.y + b4.y;
-      v[i + 2] = (v[i + 2] - mean) * inv * g4.z + b4.z;
-      v[i + 3] = (v[i + 3] - mean) * inv * g4.w + b4.w;
-    }
-    uint32_t packed[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
-    if (lane == 0) tma_store_wait_read<0>();
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int phys = i ^ (lane & 7);
-      *reinterpret_cast<uint4*>(stg + lane * 128 + phys * 16) =
-          make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-    }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0 && mt < args.num_m_tiles) {
-      tma_store_2d(map_c, stg, nt * BN + c, row0);
-      tma_store_commit();
-    }
-    if constexpr ((EPI & kEpiOut2F32) != 0) {
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        if (lane == 0) tma_store_wait_read<0>();
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int phys = i ^ (lane & 7);
-          *reinterpret_cast<float4*>(stg + lane * 128 + phys * 16) =
-              make_float4(v[32 * h2 + 4 * i], v[32 * h2 + 4 * i + 1], v[32 * h2 + 4 * i + 2],
-                          v[32 * h2 + 4 * i + 3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0 && mt < args.num_m_tiles) {
-          tma_store_2d(map_c2, stg, nt * BN + c + 32 * h2, row0);
-          tma_store_commit();
-        }
-      }
-    }
-  }
-}
-
-template <int BN, bool LN = false, bool RT = false>
-struct GemmSmem;
-
-template <int BN, bool LN, bool RT>
+template <int BN, bool RT = false>
 struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // 8 epilogue warps x (32 rows x 128 B), double-buffered except for the LN epilogue
-  static constexpr int kEpiBytes = (LN || RT) ? 8 * 4096 : 8 * 2 * 4096;
-  // LN: stats[2 buffers][8 ranks][128 rows] float2 + partial[128] float2
-  static constexpr int kLnBytes = LN ? (2 * 8 * 128 + 128) * 8 : 0;
+  // 8 epilogue warps x (32 rows x 128 B), double-buffered except with staged residuals
+  static constexpr int kEpiBytes = RT ? 8 * 4096 : 8 * 2 * 4096;
   // RT: two residual tiles of 128 rows x BN (BN/64 SWIZZLE_128B boxes of 16 KB each)
   static constexpr int kResBytes = RT ? 2 * (BN / 64) * 16384 : 0;
   static constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 256 /*barriers*/;
-  static constexpr int kStagesRaw = (kBudget - kEpiBytes - kLnBytes - kResBytes) / kStageBytes;
+  static constexpr int kStagesRaw = (kBudget - kEpiBytes - kResBytes) / kStageBytes;
   static constexpr int kStagesCap = RT ? 2 : 6;  // RT GEMMs have a single K block (K = r)
   static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
   static constexpr int kTotal =
-      1024 + kStages * kStageBytes + kEpiBytes + kLnBytes + kResBytes + 256;
+      1024 + kStages * kStageBytes + kEpiBytes + kResBytes + 256;
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                  : 2 * BN <= 256 ? 256 : 512;
 };
@@ -505,10 +330,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const CUtensorMap& map_a = maps.a;
   const CUtensorMap& map_b = maps.b;
   const CUtensorMap& map_c = maps.c;
-  const CUtensorMap& map_c2 = maps.c2;
-  constexpr bool kLN = (EPI & kEpiLN) != 0;
   constexpr bool kRT = (EPI & kEpiResTma) != 0;
-  using L = GemmSmem<BN, kLN, kRT>;
+  using L = GemmSmem<BN, kRT>;
   constexpr int kStages = L::kStages;
   static_assert(kStages >= 2, "smem budget too small");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
@@ -519,15 +342,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * L::kABytes;
   uint8_t* sEpi = smem + kStages * L::kStageBytes;
-  float2* ln_stats = reinterpret_cast<float2*>(sEpi + L::kEpiBytes);      // kLN only
-  float2* ln_partial = ln_stats + 2 * 8 * 128;
-  uint8_t* sRes = sEpi + L::kEpiBytes + L::kLnBytes;                       // kRT only
+  uint8_t* sRes = sEpi + L::kEpiBytes;  // kRT only
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRes + L::kResBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tfull = bars + 2 * kStages;
   uint64_t* tempty = bars + 2 * kStages + 2;
-  uint64_t* stats_bar = bars + 2 * kStages + 4;  // kLN: [2]
   uint64_t* res_full = bars + 2 * kStages + 6;   // kRT
   uint64_t* res_empty = bars + 2 * kStages + 7;  // kRT
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
@@ -536,16 +356,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t lane = lane_id();
   const int num_tiles = args.num_m_tiles * args.num_n_tiles;
   const int num_kb = args.K / kBlockK;
-  // tile schedule: persistent grid-stride, or (kLN) one cluster per M tile with
-  // CTA rank r owning N tile r, so each cluster covers whole rows
-  uint32_t cs = 1, crank = 0;
-  int t_first = blockIdx.x, t_step = gridDim.x;
-  if constexpr (kLN) {
-    cs = cluster_nctarank();
-    crank = cluster_ctarank();
-    t_first = static_cast<int>(cluster_id_x()) * args.num_n_tiles + static_cast<int>(crank);
-    t_step = static_cast<int>(ncluster_x()) * args.num_n_tiles;
-  }
+  // tile schedule: persistent grid-stride
+  const int t_first = blockIdx.x, t_step = gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -558,7 +370,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8);
-      if constexpr (kLN) mbar_init(&stats_bar[s], 4 * 32 * cs);
     }
     if constexpr (kRT) {
       mbar_init(res_full, 1);
@@ -570,11 +381,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
   tc_fence_before();
-  if constexpr (kLN) {
-    cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
-  } else {
-    __syncthreads();
-  }
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
@@ -643,7 +450,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = static_cast<int>(warp - 2) >> 2;
-    uint8_t* stg = sEpi + (warp - 2) * ((kLN || kRT) ? 4096 : 2 * 4096);
+    uint8_t* stg = sEpi + (warp - 2) * (kRT ? 4096 : 2 * 4096);
     uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0, iter = 0;
     for (int t = t_first; t < num_tiles; t += t_step, ++iter) {
@@ -654,19 +461,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       epi_row_stats<EPI>(args, mt, q, lane, a_st, r_st);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if constexpr (kLN) {
-        if constexpr (kRT) mbar_wait(res_full, iter & 1);
-        epilogue_tile_ln<BN, EPI>(tmem_base + acc * BN, mt, nt, grp, args, &map_c, &map_c2, stg,
-                                  q, half, lane, ln_partial, ln_stats, stats_bar, iter, cs, crank,
-                                  kRT ? sRes : nullptr, kRT ? res_empty : nullptr);
-      } else {
-        if constexpr (kRT) mbar_wait(res_full, iter & 1);
-        epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt * BN, BN, grp, args, &map_c, stg,
-                               sbuf, q, half, lane, a_st, r_st, sRes);
-        if constexpr (kRT) {  // residual tiles consumed: the producer may stage the next tile's
-          __syncwarp();
-          if (lane == 0) mbar_arrive(res_empty);
-        }
+      if constexpr (kRT) mbar_wait(res_full, iter & 1);
+      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt * BN, BN, grp, args, &map_c, stg, sbuf,
+                             q, half, lane, a_st, r_st, sRes);
+      if constexpr (kRT) {  // residual tiles consumed: the producer may stage the next tile's
+        __syncwarp();
+        if (lane == 0) mbar_arrive(res_empty);
       }
       // all TMEM reads of this accumulator by this warp are done: hand it back
       tc_fence_before();
@@ -680,11 +480,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   tc_fence_before();
-  if constexpr (kLN) {
-    cluster_sync();
-  } else {
-    __syncthreads();
-  }
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<L::kTmemCols>(tmem_base);

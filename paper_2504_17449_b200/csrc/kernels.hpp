@@ -82,8 +82,6 @@ struct AttnPlan {
   int precision = 0;
 };
 AttnPlan make_attention_plan(const void* qkv, void* ctx, int max_rows, int d, int precision);
-void launch_attention_s128(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
-                           cudaStream_t stream);
 // Same, on tcgen05 (S and O in TMEM, softmax warps write P to smem): attention_tc.cu
 void launch_attention_tc(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
                          cudaStream_t stream);

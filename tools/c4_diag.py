@@ -1,6 +1,6 @@
 # SPDX-License-Identifier: Apache-2.0
 """C4 swap diagnostics: host submit time per batch, device step time, bytes copied per batch,
-and a copy-only bandwidth probe (pinned host -> HBM slots).  python tools_c4_diag.py [mode]"""
+and a copy-only bandwidth probe (pinned host -> HBM slots).  python tools/c4_diag.py [mode]"""
 import sys
 import time
 

@@ -1,5 +1,5 @@
 # SPDX-License-Identifier: Apache-2.0
-"""Adapter-slot H2D transfer rates: python tools_copy_probe.py"""
+"""Adapter-slot H2D transfer rates: python tools/copy_probe.py"""
 import ctypes
 import sys
 

@@ -1,5 +1,5 @@
 # SPDX-License-Identifier: Apache-2.0
-"""Runs one K1 GEMM probe launch pair (for ncu): python tools_gemm_probe.py M N K bn epi"""
+"""Runs one K1 GEMM probe launch pair (for ncu): python tools/gemm_probe.py M N K bn epi"""
 import sys
 
 import numpy as np

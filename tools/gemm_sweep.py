@@ -1,6 +1,6 @@
 # SPDX-License-Identifier: Apache-2.0
 """K1 shapes of the C2 step: our tcgen05 GEMM (1-CTA / cta_group::2, each N tile) against
-torch.matmul (cuBLAS) on the same fp16 operands.  python tools_gemm_sweep.py [--ncu]"""
+torch.matmul (cuBLAS) on the same fp16 operands.  python tools/gemm_sweep.py [--ncu]"""
 import sys
 
 import numpy as np

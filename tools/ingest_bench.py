@@ -4,7 +4,7 @@
 (hmi_gpu_upload_plt1: pinned chunks shipped whole, rows scattered on the device) and by the
 host path (hmi_plot_table_load into host memory, then hmi_gpu_upload_plot_table). The file is
 in the page cache (just written) for both: this measures the ingest, not the disk.
-    python tools_ingest_bench.py [rows] [dir]"""
+    python tools/ingest_bench.py [rows] [dir]"""
 import json
 import os
 import sys

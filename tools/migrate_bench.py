@@ -3,7 +3,7 @@
 moved between two engines by export / import (device-to-device slot copies; on one GPU the
 "peer" is the same device, so this measures the copy path and bookkeeping, not NVLink) against
 the PCIe path a migration would otherwise take: register_task on the destination followed by
-the H2D residency load of its first batch.   python tools_migrate_bench.py [tasks]"""
+the H2D residency load of its first batch.   python tools/migrate_bench.py [tasks]"""
 import json
 import sys
 import time

@@ -6,5 +6,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$2"
 echo "ncu rc $?"
 ncu -i $OUT/prof.ncu-rep --page details --csv > $OUT/details.csv 2>/dev/null
 ncu -i $OUT/prof.ncu-rep --page source --csv --print-source sass > $OUT/source.csv 2>/dev/null
-python tools_ncu_details.py $OUT/details.csv
-python tools_ncu_hot.py $OUT/source.csv "" 14
+python tools/ncu_details.py $OUT/details.csv
+python tools/ncu_hot.py $OUT/source.csv "" 14

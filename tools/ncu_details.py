@@ -1,5 +1,5 @@
 # SPDX-License-Identifier: Apache-2.0
-"""Key metrics per kernel from an `ncu --page details --csv` export: python tools_ncu_details.py details.csv"""
+"""Key metrics per kernel from an `ncu --page details --csv` export: python tools/ncu_details.py details.csv"""
 import csv
 import sys
 

@@ -1,6 +1,6 @@
 # SPDX-License-Identifier: Apache-2.0
 """Top stalled SASS instructions per kernel from `ncu --page source --csv --print-source sass`.
-python tools_ncu_hot.py source.csv [kernel-substring] [top]"""
+python tools/ncu_hot.py source.csv [kernel-substring] [top]"""
 import csv
 import sys
 

@@ -1,5 +1,5 @@
 #!/usr/bin/env bash
-# ncu --set full of selected kernels inside the C2 step:  bash tools_ncu_kernel.sh OUT REGEX COUNT [skip]
+# ncu --set full of selected kernels inside the C2 step:  bash tools/ncu_kernel.sh OUT REGEX COUNT [skip]
 OUT=gpurun_out/${1:-ncuk}
 mkdir -p $OUT
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$2" -s ${4:-20} -c ${3:-2} \

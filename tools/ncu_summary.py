@@ -1,7 +1,7 @@
 # SPDX-License-Identifier: Apache-2.0
 """Summarise an `ncu --set full` capture of one C2 layer into profiles/ (text + json).
 
-The capture (tools_profile.sh) holds, in launch order: retrieve, then higher
+The capture (tools/profile.sh) holds, in launch order: retrieve, then higher
 layers 0 and 1 (gemm_qkv, attention, gemm_oproj, adapter (fused down+up),
 gemm_ffn1, gemm_ffn2 each; layer 1's QKV is the LN-folded variant). Keys
 without a suffix are layer 1 (the steady-state layer).

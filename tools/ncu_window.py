@@ -1,5 +1,5 @@
 # SPDX-License-Identifier: Apache-2.0
-"""SASS window with stall samples: python tools_ncu_window.py source.csv kernel-substr lo hi [lo hi ...]"""
+"""SASS window with stall samples: python tools/ncu_window.py source.csv kernel-substr lo hi [lo hi ...]"""
 import csv
 import sys
 

@@ -15,8 +15,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"gemm|attention|retrieve|adapter" -s 370 -c 13 -o $OUT/prof \
   python bench.py --quick --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_run.log 2>&1
-python tools_ncu_summary.py $OUT/prof.ncu-rep $OUT/ncu_layer.txt $OUT/ncu_layer.json > /dev/null 2>&1
+python tools/ncu_summary.py $OUT/prof.ncu-rep $OUT/ncu_layer.txt $OUT/ncu_layer.json > /dev/null 2>&1
 ncu -i $OUT/prof.ncu-rep --page details --csv > $OUT/details.csv 2>/dev/null
-python tools_ncu_details.py $OUT/details.csv > $OUT/details.txt 2>/dev/null
-python tools_launch_summary.py $OUT/launches.csv $OUT/launches_summary.txt > /dev/null 2>&1
+python tools/ncu_details.py $OUT/details.csv > $OUT/details.txt 2>/dev/null
+python tools/launch_summary.py $OUT/launches.csv $OUT/launches_summary.txt > /dev/null 2>&1
 ls -la $OUT

@@ -1,7 +1,7 @@
 # SPDX-License-Identifier: Apache-2.0
 """Adapter registration throughput ("10k adapters need fast load"):
 C2 adapters (d 768, r 64, 6 higher layers) registered one call at a time, in bulk on host
-threads, and in bulk from ADP1 files (page cache warm).   python tools_register_bench.py [n]"""
+threads, and in bulk from ADP1 files (page cache warm).   python tools/register_bench.py [n]"""
 import json
 import os
 import sys

@@ -4,7 +4,7 @@ half of them, `batches` mixed 256-request batches via the pipelined submit / wai
 adapter replacements, tenant migrations between two engines and table uploads interleaved.
 Checks: every batch returns, no device error, pool residency within capacity, device memory
 flat after warm-up, and a fixed probe batch scores identically at the start and the end.
-    python tools_soak.py [tenants] [batches]"""
+    python tools/soak.py [tenants] [batches]"""
 import json
 import sys
 import time

@@ -3,7 +3,7 @@
 Table 12): hBERT-base, `n_tenants` tenants whose adapters swap through an HBM slot pool holding
 `pool` of them, 256-request batches, sync / coarse / fine. Per mode: requests/s over the
 makespan of the traced batches, io (adapter H2D) and compute busy time, and how much of the io
-time overlaps compute.   python tools_stage_ablation.py [n_tenants] [pool] [batches]"""
+time overlaps compute.   python tools/stage_ablation.py [n_tenants] [pool] [batches]"""
 import json
 import sys
 import time
