@@ -2,6 +2,9 @@
 # Builds the B200 product library (sm_100a) and the CPU oracle.
 #   make            -> paper_2504_17449_b200/_lib/libhmi_b200.so + oracle/_build/liboracle.so
 #   make ref        -> oracle/_ref/libhmiref.so (needs /root/reference; see oracle/build_ref.sh)
+#   make cppapi     -> cpp_api/_build/libhmi_cuda_backend.a (hmi::sched::CudaBackend, compiled
+#                      against the reference's public headers) + its test program, linked with
+#                      the reference library oracle/_ref builds (needs /root/reference)
 NVCC     ?= /usr/local/cuda/bin/nvcc
 CXX      ?= g++
 ARCH     := -gencode arch=compute_100a,code=sm_100a
@@ -36,7 +39,26 @@ oracle:
 ref:
 	bash oracle/build_ref.sh
 
+REF_INC  ?= /root/reference/proj/include
+CPP_OUT  := cpp_api/_build
+CPPFLAGS_API := -std=c++20 -O2 -Wall -include mutex -I$(REF_INC) -Icpp_api -Iinclude
+
+cppapi: $(CPP_OUT)/libhmi_cuda_backend.a $(CPP_OUT)/test_cuda_backend
+
+$(CPP_OUT)/cuda_backend.o: cpp_api/cuda_backend.cpp cpp_api/hmi/scheduler/cuda_backend.hpp include/hmi_gpu.h
+	@mkdir -p $(CPP_OUT)
+	$(CXX) $(CPPFLAGS_API) -fPIC -c $< -o $@
+
+$(CPP_OUT)/libhmi_cuda_backend.a: $(CPP_OUT)/cuda_backend.o
+	ar rcs $@ $^
+
+$(CPP_OUT)/test_cuda_backend: tests/cpp/test_cuda_backend.cpp $(CPP_OUT)/libhmi_cuda_backend.a \
+		$(LIBDIR)/libhmi_b200.so oracle/_ref/libhmiref.so
+	$(CXX) $(CPPFLAGS_API) $< -o $@ $(CPP_OUT)/libhmi_cuda_backend.a -Loracle/_ref -lhmiref \
+		-L$(LIBDIR) -lhmi_b200 -Wl,-rpath,'$$ORIGIN/../../oracle/_ref' \
+		-Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
+
 clean:
 	rm -rf build $(LIBDIR)
 
-.PHONY: all oracle ref clean
+.PHONY: all oracle ref cppapi clean

@@ -84,3 +84,34 @@ def logit_error(gpu_scores, ref_scores):
     L = ref_scores.shape[1]
     d = np.abs(gpu_scores[:, :L].astype(np.float64) - ref_scores).max(axis=1)
     return float((d / np.abs(ref_scores).max(axis=1)).max())
+
+
+def token_tag_check(world, inst, toks, lens, gpu_tags, gpu_hidden):
+    """Per-token argmax check of a token_tag batch (apply_head, model.cpp:158-163) with every
+    disagreement classified. Reference rows: the oracle's final (post-LN2) rows of each request;
+    GPU rows: the engine's normalised final rows (debug flag 2). For each row p < len, scores
+    are rows @ W + b in f64; a mismatched tag is a near-tie when the reference's margin between
+    its tag and the GPU's (relative to the row's max |score|) is within twice that row's
+    measured score error, else decisive. Returns (agreement, n_tokens, decisive, near_ties)."""
+    agree = total = 0
+    decisive, ties = [], []
+    for i in range(len(inst)):
+        k, n = int(inst[i]), int(lens[i])
+        w, b = world.heads[0 if world.shared_head else k]
+        h0, _, _, _ = world.tree.retrieve(int(world.inst_version[k]), toks[i, :n], world.cfg.mode)
+        _, _, tags, h = oracle.higher_forward(world.cfg, world.higher, h0, n, world.adapters[k],
+                                              world.r, w, b, head_kind=1)
+        W, B = np.asarray(w, np.float64), np.asarray(b, np.float64)
+        ref_s = h[:n] @ W + B
+        gpu_s = gpu_hidden[i, :n].astype(np.float64) @ W + B
+        scale = np.abs(ref_s).max(axis=1)
+        err = np.abs(gpu_s - ref_s).max(axis=1) / scale
+        for p in range(n):
+            total += 1
+            g, r = int(gpu_tags[i, p]), int(tags[p])
+            if g == r:
+                agree += 1
+                continue
+            m = float((ref_s[p, r] - ref_s[p, g]) / scale[p])
+            (ties if m <= 2 * err[p] else decisive).append((i, p, m, float(err[p])))
+    return agree / max(total, 1), total, decisive, ties
