@@ -98,6 +98,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    """Host CPU model name and socket count (the CPU arm states its hardware)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            names = [ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")]
+        with open("/proc/cpuinfo") as f:
+            sockets = {ln.split(":", 1)[1].strip() for ln in f if ln.startswith("physical id")}
+        return f"{names[0]} ({len(names)} logical CPUs, {max(len(sockets), 1)} socket(s))"
+    except Exception:
+        return "unknown"
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -129,6 +141,18 @@ def barrier(world):
         import torch.distributed as dist
 
         dist.barrier()
+
+
+def gather_over_ranks(x: float, world: int) -> list:
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if _BACKEND == "nccl" else "cpu"
+    out = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(out, torch.tensor([x], dtype=torch.float64, device=dev))
+    return [float(t.item()) for t in out]
 
 
 def max_over_ranks(x: float, world: int) -> float:
@@ -190,7 +214,7 @@ def cpu_baseline(wl, world, steps=1, threads=None, sample=None):
     for s in range(steps):
         secs += run_reference_sample(ref, world, wl, sample, 9000 + s, threads)
     v = steps * sample / secs
-    return {"value": v, "unit": "req/s", "cores": threads, "kind": kind,
+    return {"value": v, "unit": "req/s", "cores": threads, "kind": kind, "cpu": cpu_model(),
             "sample": f"{steps}x{sample} {wl.name} requests (seq {wl.seq}) through "
                       f"retrieve_sequence + higher_stack_forward (HMI_KERNELS="
                       f"{oracle.ref().ref_active_kernels().decode()}), {threads} threads"}
@@ -226,6 +250,7 @@ def bench_reference(args, wl):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": cfgd, "impl": "reference",
         "cpu_baseline": {"value": v, "unit": "req/s", "cores": threads, "kind": "reference",
+                         "cpu": cpu_model(),
                          "sample": f"each step {sample} requests, {threads} host threads, "
                                    f"HMI_KERNELS={oracle.ref().ref_active_kernels().decode()}"},
         "e2e": {"value": v, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -386,6 +411,13 @@ def bench_ours(args, wl):
     prof = eng.profile_read()
     eng.profile(False)
 
+    # ---- concurrent host -> HBM copy rate per rank (all ranks at once after a barrier), from
+    # NUMA-local pinned memory as the adapter store: whether PCIe or the socket link caps the
+    # swap of C4 / C5 on a full box
+    barrier(world_size)
+    h2d_rate = gather_over_ranks(E.h2d_probe(eng), world_size)
+    numa = gather_over_ranks(float(-1 if c1["numa_node"] is None else c1["numa_node"]), world_size)
+
     hbm, peak_burst, peak_sust, peak_src = peaks()
     T = wl.batch * wl.seq
     d, f, r = wl.hidden_size, wl.ffn_size, wl.r
@@ -434,6 +466,8 @@ def bench_ours(args, wl):
         "kernels": kernels,
         "clocks": clk,
         "pool": eng.pool_stats(),
+        "h2d_gbps_per_rank": [round(x, 2) for x in h2d_rate],
+        "pinned_numa_node_per_rank": [int(x) for x in numa],
     }
     if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, world)
@@ -587,7 +621,7 @@ def bench_plot(args):
             list(ex.map(lambda i: oracle.lower_forward(cfg, m, keys[i, :key_len[i]]), sample))
         cs = time.perf_counter() - t0
         line["cpu_baseline"] = {"value": int(key_len[sample].sum()) / cs, "unit": "rows/s",
-                                "cores": threads, "kind": "port",
+                                "cores": threads, "kind": "port", "cpu": cpu_model(),
                                 "sample": f"{len(sample)} root-table fragments through the C oracle's "
                                           f"lower_stack_forward (bit-exact to the reference's scalar "
                                           f"kernels), {threads} threads"}

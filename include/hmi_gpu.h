@@ -260,8 +260,13 @@ int hmi_generate_adapter(const hmi_model_config* cfg, uint32_t bottleneck, uint6
 /* generate_output_head (weights.cpp:105-118): w [d x labels], b [labels].    */
 int hmi_generate_head(uint32_t hidden_size, uint32_t labels, uint64_t seed, float* w, float* b);
 
-/* Engine counters: out[0] kernel launches, [1] batches, [2] adapter copies. */
+/* Engine counters: out[0] kernel launches, [1] batches, [2] adapter copies,
+ * [3] host NUMA node the pinned adapter store is bound to (UINT64_MAX: unknown). */
 int hmi_gpu_counters(hmi_gpu_ctx* ctx, uint64_t* out);
+/* Pinned-host (NUMA-local, as the adapter store) -> HBM copy rate on the copy stream:
+ * `reps` copies of `bytes`; *gbps = GB/s. No reference counterpart (the reference's
+ * transfer model is one PCIe link, device_pool.hpp:18-25); bench.py reports it per rank. */
+int hmi_gpu_h2d_probe(hmi_gpu_ctx* ctx, uint64_t bytes, uint32_t reps, double* gbps);
 
 /* ---- standalone slot-pool policy (host only; trace parity tests) ---------- */
 typedef struct hmi_pool hmi_pool;

@@ -191,6 +191,7 @@ def _sig(L):
     L.hmi_generate_adapter.argtypes = [P(ModelConfig), u32, u64, f32p]
     L.hmi_generate_head.argtypes = [u32, u32, u64, f32p, f32p]
     L.hmi_gpu_counters.argtypes = [vp, u64p]
+    L.hmi_gpu_h2d_probe.argtypes = [vp, u64, u32, P(ctypes.c_double)]
 
 
 def lib() -> ctypes.CDLL:

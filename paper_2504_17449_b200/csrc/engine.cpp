@@ -28,6 +28,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <immintrin.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -37,6 +39,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <fstream>
 #include <functional>
 #include <map>
 #include <memory>
@@ -211,6 +214,45 @@ void fold_weights(const float* w, size_t in, size_t out, const float* bias, cons
 
 }  // namespace
 
+// Pinned adapter store placed on the GPU's own NUMA node: on a two-socket 8-GPU box the
+// adapter misses then cross PCIe only, not the socket link as well. Pages are mmap'd, bound
+// with mbind(MPOL_PREFERRED, node) (falls back to other nodes when that one is full), faulted
+// in, then page-locked with cudaHostRegister (portable: any device may copy from them).
+static int gpu_numa_node(int device) {
+  char bus[64] = {};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return -1;
+  std::string id(bus);
+  for (auto& ch : id) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+  for (const std::string& cand : {id, id.size() > 4 && id.rfind("0000", 0) == 0 ? id.substr(4) : id}) {
+    std::ifstream in("/sys/bus/pci/devices/" + cand + "/numa_node");
+    int node = -1;
+    if (in >> node) return node;
+  }
+  return -1;
+}
+
+static uint8_t* host_alloc_local(size_t bytes, int node) {
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  HMI_CHECK(p != MAP_FAILED, HMI_CAPACITY_ERROR, "pinned adapter store: mmap failed");
+  if (node >= 0 && node < 64) {
+    const unsigned long mask = 1ul << node;
+    constexpr int kMpolPreferred = 1;
+    syscall(SYS_mbind, p, bytes, kMpolPreferred, &mask, 64ul, 0u);  // best effort
+  }
+  std::memset(p, 0, bytes);  // fault the pages in under the policy
+  const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    munmap(p, bytes);
+    HMI_CUDA(e);
+  }
+  return static_cast<uint8_t*>(p);
+}
+
+static void host_free_local(uint8_t* p, size_t bytes) {
+  cudaHostUnregister(p);
+  munmap(p, bytes);
+}
+
 struct Ctx {
   int device = 0;
   hmi_model_config cfg{};
@@ -256,7 +298,8 @@ struct Ctx {
   std::unique_ptr<SlotPool> pool;
   DevBuf<uint8_t> arena;
   std::vector<uint8_t*> store;  // per task, L * slot_bytes pinned, or null
-  std::vector<uint8_t*> pinned_chunks;
+  std::vector<std::pair<uint8_t*, size_t>> pinned_chunks;  // mmap'd + cudaHostRegister'ed
+  int numa_node = -1;  // host NUMA node of the GPU's PCIe root (sysfs), -1 if unknown
   std::vector<uint8_t*> free_blocks;
   uint8_t* chunk_cur = nullptr;
   size_t chunk_left = 0;
@@ -436,9 +479,8 @@ struct Ctx {
     const size_t need = static_cast<size_t>(L) * slot_bytes;
     if (chunk_left < need) {
       const size_t chunk = std::max<size_t>(need, size_t(256) << 20);
-      uint8_t* p = nullptr;
-      HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), chunk, cudaHostAllocPortable));
-      pinned_chunks.push_back(p);
+      uint8_t* p = host_alloc_local(chunk, numa_node);
+      pinned_chunks.push_back({p, chunk});
       chunk_cur = p;
       chunk_left = chunk;
     }
@@ -486,7 +528,7 @@ Ctx::~Ctx() {
       if (p) cudaFreeHost(p);
     if (s.done) cudaEventDestroy(s.done);
   }
-  for (auto* p : pinned_chunks) cudaFreeHost(p);
+  for (auto& [p, n] : pinned_chunks) host_free_local(p, n);
   for (auto& [k, p] : ipc_open) cudaIpcCloseMemHandle(p);
   for (auto& [k, g] : dec_graphs) cudaGraphExecDestroy(g);
   for (auto st : dec_aux) cudaStreamDestroy(st);
@@ -1409,6 +1451,7 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     if (c.opt.max_heads == 0) c.opt.max_heads = c.opt.max_tasks;
     if (c.opt.max_versions == 0) c.opt.max_versions = 64;
     HMI_CUDA(cudaSetDevice(device));
+    c.numa_node = gpu_numa_node(device);
     c.d = static_cast<int>(cfg->hidden_size);
     c.f = static_cast<int>(cfg->ffn_size);
     c.L = static_cast<int>(cfg->higher_layers);
@@ -1815,7 +1858,8 @@ int hmi_gpu_upload_plt1(hmi_gpu_ctx* ctx, const char* path, uint32_t* version_ou
     HMI_CHECK(ngram == static_cast<uint32_t>(c.ngram) && d == static_cast<uint32_t>(c.d),
               HMI_DIMENSION_ERROR, "PLT1 table (ngram " + std::to_string(ngram) + ", d " +
                                        std::to_string(d) + ") does not match the model");
-    check_new_version(c, version, parent);
+    // the tree checks (free id, existing parent) come after the whole file parsed, as the
+    // reference's load() then VersionTree::add_branch: a truncated file is a FormatError first
     const bool dbg = std::getenv("HMI_DEBUG_INGEST") != nullptr;
     auto now = [] { return std::chrono::duration<double, std::milli>(
                         std::chrono::steady_clock::now().time_since_epoch()).count(); };
@@ -1922,6 +1966,7 @@ int hmi_gpu_upload_plt1(hmi_gpu_ctx* ctx, const char* path, uint32_t* version_ou
       k ^= 1;
     }
     if (chunk_at != file_size) fail("trailing bytes after payload", chunk_at);
+    check_new_version(c, version, parent);
     double t0 = now();
     HMI_CUDA(cudaStreamSynchronize(c.copy));
     t_wait += now() - t0;
@@ -2813,5 +2858,45 @@ extern "C" int hmi_gpu_counters(hmi_gpu_ctx* ctx, uint64_t* out) {
     out[0] = c.n_launches;
     out[1] = c.n_batches;
     out[2] = c.n_copies;
+    out[3] = c.numa_node < 0 ? ~uint64_t(0) : static_cast<uint64_t>(c.numa_node);
+  });
+}
+
+// Host -> HBM bandwidth from the pinned adapter store's memory (the source adapter misses
+// are copied from) into a scratch buffer, on the context's copy stream. Ranks run it at the
+// same time after a barrier, so it measures the concurrent per-GPU rate of the box.
+extern "C" int hmi_gpu_h2d_probe(hmi_gpu_ctx* ctx, uint64_t bytes, uint32_t reps, double* gbps) {
+  using namespace hmi_b200;
+  return guarded([&] {
+    HMI_CHECK(ctx != nullptr && gbps != nullptr && bytes > 0 && reps > 0, HMI_CONFIG_ERROR,
+              "h2d_probe: bad argument");
+    Ctx& c = ctx->impl;
+    std::lock_guard<std::mutex> lock(c.mu);
+    HMI_CUDA(cudaSetDevice(c.device));
+    c.reap(true);
+    uint8_t* src = host_alloc_local(bytes, c.numa_node);
+    void* dst = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    struct Cleanup {
+      uint8_t* src; size_t n; void** dst; cudaEvent_t* a; cudaEvent_t* b;
+      ~Cleanup() {
+        if (*a) cudaEventDestroy(*a);
+        if (*b) cudaEventDestroy(*b);
+        if (*dst) cudaFree(*dst);
+        host_free_local(src, n);
+      }
+    } cleanup{src, bytes, &dst, &a, &b};
+    HMI_CUDA(cudaMalloc(&dst, bytes));
+    HMI_CUDA(cudaEventCreate(&a));
+    HMI_CUDA(cudaEventCreate(&b));
+    HMI_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.copy));  // warm
+    HMI_CUDA(cudaEventRecord(a, c.copy));
+    for (uint32_t i = 0; i < reps; ++i)
+      HMI_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.copy));
+    HMI_CUDA(cudaEventRecord(b, c.copy));
+    HMI_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    HMI_CUDA(cudaEventElapsedTime(&ms, a, b));
+    *gbps = static_cast<double>(bytes) * reps / (ms * 1e-3) / 1e9;
   });
 }

@@ -455,4 +455,12 @@ def generate_head(d: int, labels: int, seed: int):
 def engine_counters(eng: GpuEngine) -> dict:
     o = np.zeros(4, np.uint64)
     check(_native.lib().hmi_gpu_counters(eng.h, _p(o, ctypes.c_uint64)))
-    return {"launches": int(o[0]), "batches": int(o[1]), "adapter_copies": int(o[2])}
+    return {"launches": int(o[0]), "batches": int(o[1]), "adapter_copies": int(o[2]),
+            "numa_node": None if int(o[3]) == 2**64 - 1 else int(o[3])}
+
+
+def h2d_probe(eng: GpuEngine, nbytes: int = 256 << 20, reps: int = 8) -> float:
+    """GB/s of pinned (NUMA-local) host -> HBM copies on the engine's copy stream."""
+    g = ctypes.c_double(0.0)
+    check(_native.lib().hmi_gpu_h2d_probe(eng.h, ctypes.c_uint64(nbytes), reps, ctypes.byref(g)))
+    return g.value

@@ -294,16 +294,16 @@ def test_max_length_s512_ragged(mode):
 def test_token_tag_head():
     """token_tag (model.cpp:158-163): every valid row's argmax; each disagreement with the
     oracle must be a near-tie within that row's measured score error."""
-    w = World(oracle.TINY, n_tasks=4, r=16, labels=5, head_kind=E.HEAD_TAG, max_batch=32)
-    inst, toks, lens = w.requests(5, 32, 128, min_len=3)
+    w = World(oracle.TINY, n_tasks=4, r=16, labels=5, head_kind=E.HEAD_TAG, max_batch=64)
+    inst, toks, lens = w.requests(5, 64, 128, min_len=3)
     w.eng.set_debug(2)
     res = w.eng.infer_batch(inst, toks, lens, want_tags=True)
     hidden = w.eng.debug_hidden(len(inst), 128)  # padded length of the batch
     agree, n, decisive, ties = token_tag_check(w, inst, toks, lens, res.tags, hidden)
     print(f"token_tag: {n} tokens, agreement {agree:.4f}, near-ties {len(ties)}")
-    assert n > 2000
+    assert n > 3000
     assert not decisive, decisive
-    assert agree >= 0.99
+    assert agree >= 0.999
     assert (res.labels == -1).all()
     w.eng.close()
 

@@ -20,7 +20,7 @@ class World:
                  head_kind: int = 0, branches=((0, 40), (0, 40), (1, 30)), max_batch=32,
                  max_seq=128, pool_bytes=0, pipeline_mode=E.MODE_FINE, precision=0,
                  table_seed=1, n_hot=24, n_bi=80, n_tri=60, engine=True, shared_head=False,
-                 max_new_tokens=0, max_labels=None):
+                 max_new_tokens=0, max_labels=None, tasks=None, device=0):
         self.cfg, self.r, self.labels, self.head_kind = cfg, r, labels, head_kind
         self.higher = oracle.generate_higher(cfg)
         self.tables, self.hot = make_tree(table_seed, cfg.vocab_size, cfg.hidden_size,
@@ -42,7 +42,8 @@ class World:
             mc = E.model_config(cfg.hidden_size, cfg.heads, cfg.lower_layers, cfg.higher_layers,
                                 cfg.ffn_size, cfg.vocab_size, cfg.mode, cfg.max_fragment,
                                 cfg.seed)
-            self.eng = E.GpuEngine(mc, self.higher, precision=precision, max_batch=max_batch,
+            self.eng = E.GpuEngine(mc, self.higher, device=device, precision=precision,
+                                   max_batch=max_batch,
                                    max_seq=max_seq, bottleneck=r,
                                    max_labels=labels if max_labels is None else max_labels,
                                    pipeline_mode=pipeline_mode, pool_bytes=pool_bytes,
@@ -50,7 +51,8 @@ class World:
                                    max_new_tokens=max_new_tokens)
             for t in self.tables:
                 self.eng.upload_table(t["version"], t["parent"], t["key_len"], t["keys"], t["reps"])
-            for t in range(n_tasks):
+            # tasks: the subset this engine serves (a tenant shard), default all
+            for t in (range(n_tasks) if tasks is None else tasks):
                 self.eng.register_task(t, self.adapters[t])
                 if not shared_head or t == 0:
                     w, b = self.heads[t]
