@@ -258,6 +258,29 @@ def bench_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def _union(iv):
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def _overlap(x, y):
+    """Total length of the intersection of two sorted disjoint interval lists."""
+    tot, j = 0.0, 0
+    for a, b in x:
+        while j < len(y) and y[j][1] <= a:
+            j += 1
+        k = j
+        while k < len(y) and y[k][0] < b:
+            tot += max(0.0, min(b, y[k][1]) - max(a, y[k][0]))
+            k += 1
+    return tot
+
+
 def config_dict(wl, args, world_size):
     return {
         "workload": f"{args.config.upper()} {wl.name}: {wl.n_tenants} tenants, "
@@ -312,8 +335,9 @@ def bench_ours(args, wl):
     K, W = args.steps, args.warmup
     # W warm-up batches, K timed device-resident batches, K fresh batches for the e2e pass
     # (fresh so a swapping pool sees the same miss rate in both passes)
+    # (and, when the pool swaps, K more fresh batches for the StageTrace pass)
     batches = [world.requests(10_000 * (rank + 1) + s, wl.batch, tenants=my_tenants)
-               for s in range(W + 2 * K)]
+               for s in range(W + 3 * K)]
     dev = torch.device("cuda", local)
     d_tok = [torch.from_numpy(b[1].astype(np.int32)).to(dev) for b in batches]
     d_len = [torch.from_numpy(b[2].astype(np.int32)).to(dev) for b in batches]
@@ -345,6 +369,7 @@ def bench_ours(args, wl):
 
     # ---- timed: inputs resident in HBM, L2 flushed before each step
     c0 = E.engine_counters(eng)
+    p0 = eng.pool_stats()
     barrier(world_size)
     torch.cuda.synchronize()
     evs = []
@@ -362,6 +387,7 @@ def bench_ours(args, wl):
     barrier(world_size)
     clk = clocks.stop()
     c1 = E.engine_counters(eng)
+    p1 = eng.pool_stats()
     local_ms = sum(a.elapsed_time(b) for a, b in evs)
     max_ms = max_over_ranks(local_ms, world_size)
     value = world_size * wl.batch * K / (max_ms / 1e3)
@@ -410,6 +436,30 @@ def bench_ours(args, wl):
     eng.synchronize()
     prof = eng.profile_read()
     eng.profile(False)
+
+    # ---- adapter swap (pool below all of this rank's tenants): bytes copied per timed step,
+    # and from a StageTrace of K more device-resident batches the io (H2D) busy time and the
+    # share of it that overlaps compute
+    swap = None
+    if frac < 1.0:
+        eng.trace(True)
+        for k in range(K):
+            run_device(W + 2 * K + k)
+        eng.synchronize()
+        recs = eng.stage_trace()
+        eng.trace(False)
+        io = _union([(r["start_ms"], r["end_ms"]) for r in recs if r["worker"] == "io"])
+        comp = _union([(r["start_ms"], r["end_ms"]) for r in recs if r["worker"] == "compute"])
+        io_busy = sum(b - a for a, b in io)
+        comp_busy = sum(b - a for a, b in comp)
+        span = comp[-1][1] - comp[0][0] if comp else 0.0
+        copied = (p1["bytes_copied"] - p0["bytes_copied"]) / K
+        swap = {"bytes_copied_per_step": copied,
+                "loads_per_step": (p1["loads"] - p0["loads"]) / K,
+                "io_busy_ms_per_step": io_busy / K, "compute_busy_ms_per_step": comp_busy / K,
+                "compute_idle_ms_per_step": (span - comp_busy) / K,
+                "io_hidden_frac": _overlap(io, comp) / io_busy if io_busy > 0 else 1.0,
+                "hide_threshold_gbps": copied / (max_ms / K * 1e-3) / 1e9}
 
     # ---- concurrent host -> HBM copy rate per rank (all ranks at once after a barrier), from
     # NUMA-local pinned memory as the adapter store: whether PCIe or the socket link caps the
@@ -467,6 +517,7 @@ def bench_ours(args, wl):
         "clocks": clk,
         "pool": eng.pool_stats(),
         "h2d_gbps_per_rank": [round(x, 2) for x in h2d_rate],
+        "swap": swap,
         "pinned_numa_node_per_rank": [int(x) for x in numa],
     }
     if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
@@ -530,7 +581,42 @@ def bench_generate(args, wl):
     ms = max_over_ranks(ms, world_size)
     c1 = E.engine_counters(eng)
     value = world_size * wl.batch * K / (ms / 1e3)
-    _, peak_burst, _, _ = peaks()
+    hbm, peak_burst, _, _ = peaks()
+
+    # ---- decode-step roofline (HBM-bound): the same K batches generating one
+    # token (prompt forward + lm head) time the prefill; the remaining gen_tokens - 1 single-row
+    # steps take the difference. Algorithmic bytes of one step at this batch: every shared
+    # weight, the lm head, each distinct tenant's adapter slots, the KV cache up to the step's
+    # context, and the f32 logits written and read once.
+    torch.cuda.synchronize()
+    a1 = torch.cuda.Event(enable_timing=True)
+    b1 = torch.cuda.Event(enable_timing=True)
+    a1.record(stream)
+    for k in range(K):
+        inst, toks, lens = batches[W + k]
+        eng.generate(inst, toks, lens, 1)
+    b1.record(stream)
+    torch.cuda.synchronize()
+    ms1 = max_over_ranks(a1.elapsed_time(b1), world_size)
+    step_ms = (ms - ms1) / K / (wl.gen_tokens - 1)
+    d, f, r, L, V, B = wl.hidden_size, wl.ffn_size, wl.r, wl.higher_layers, wl.labels, wl.batch
+    w_shared = L * (4 * d * d + 2 * d * f) * 2
+    w_lm = V * d * 2
+    tenants = float(np.mean([len(set(batches[W + k][0].tolist())) for k in range(K)]))
+    slot = (2 * r * d) * 2 + (r + d) * 4
+    w_adapt = tenants * L * slot
+    ctx_mean = float(np.mean([batches[W + k][2].mean() for k in range(K)])) + wl.gen_tokens / 2
+    kv = B * ctx_mean * L * 2 * d * 2
+    logits = 2 * B * V * 4
+    step_bytes = w_shared + w_lm + w_adapt + kv + logits
+    roof = {"bound": "hbm", "kernel": "decode step (all kernels of one generated token)",
+            "achieved": step_bytes / (step_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": step_bytes / (step_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+            "step_ms": step_ms, "prefill_ms": ms1 / K,
+            "bytes_per_step": {"shared_weights": w_shared, "lm_head": w_lm,
+                               "adapters": w_adapt, "kv_cache": kv, "logits": logits,
+                               "total": step_bytes, "distinct_tenants": tenants,
+                               "mean_context": ctx_mean}}
     line = {
         "metric": f"{wl.name} mixed-tenant generated requests/s (prompt {wl.seq} + {wl.gen_tokens} tokens)",
         "value": value, "unit": "req/s", "n_gpus": world_size, "steps": K, "warmup": W,
@@ -541,6 +627,7 @@ def bench_generate(args, wl):
         "e2e": {"value": value, "unit": "req/s", "h2d_bytes_per_step": wl.batch * (wl.seq * 4 + 8),
                 "d2h_bytes_per_step": wl.batch * wl.gen_tokens * 8},
         "gpu_launches": int(c1["launches"] - c0["launches"]),
+        "roofline": roof,
         "tensor_frac": value / world_size * wl.generate_flops_per_request() / 1e12 / peak_burst,
         "flops_per_request": wl.generate_flops_per_request(),
         "note": "host API timed (hmi_gpu_generate, synchronous per batch); a side config, the "

@@ -31,6 +31,7 @@
 #include <cstdint>
 
 #include "adapter.hpp"
+#include "kernels.hpp"
 #include "sm100.cuh"
 
 namespace hmi_b200 {
@@ -131,6 +132,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
+  if (args.ready != nullptr) {
+    // fine pipeline: wait on the device for this layer's adapter copies (the copy stream
+    // writes the batch's sequence number after them) instead of a stream-level event wait,
+    // which would cut the programmatic-launch chain O-proj -> adapter
+    if (threadIdx.x == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_gpu(args.ready) - args.ready_seq > 0x7fffffffu) {  // wrap-safe <
+        if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) {  // 20 s: never, unless broken
+          atomicExch(args.err, HMI_SCHEDULING_BUG);
+          break;
+        }
+        __nanosleep(256);
+      }
+      fence_proxy_async_global();
+    }
+    __syncthreads();
+  }
   // TMEM columns: mid acc 0..63, y acc[0] 128..255, y acc[1] 256..383
 
   if (warp == 0) {
@@ -422,7 +440,8 @@ AdapterPlan make_adapter_plan(const AdapterSpec& s) {
   return p;
 }
 
-void launch_adapter(const AdapterPlan& p, int rows, cudaStream_t stream) {
+void launch_adapter(const AdapterPlan& p, int rows, cudaStream_t stream, const uint32_t* ready,
+                    uint32_t ready_seq, int32_t* err) {
   if (rows <= 0) return;
   HMI_CHECK(rows % 128 == 0 && rows <= p.max_rows, HMI_DIMENSION_ERROR,
             "fused adapter: rows must be a multiple of 128 within the plan");
@@ -439,6 +458,9 @@ void launch_adapter(const AdapterPlan& p, int rows, cudaStream_t stream) {
     configured[bf] = true;
   }
   AdapterArgs a = p.args;
+  a.ready = ready;
+  a.ready_seq = ready_seq;
+  a.err = err;
   a.M = rows;
   a.num_m_tiles = rows / 128;
   const int grid = a.num_m_tiles < device_sm_count() ? a.num_m_tiles : device_sm_count();

@@ -28,6 +28,11 @@ struct AdapterArgs {
   const float* r_gamma = nullptr;   // LN applied to h on the fly
   const float* r_beta = nullptr;
   float inv_n = 0.f;
+  // fine pipeline: this layer's adapter slots are resident once *ready >= ready_seq (written
+  // by the copy stream after the layer's H2D copies, cuStreamWriteValue32); null: no wait
+  const uint32_t* ready = nullptr;
+  uint32_t ready_seq = 0;
+  int32_t* err = nullptr;           // HMI_SCHEDULING_BUG if the flag never arrives
 };
 
 struct AdapterSpec {
@@ -54,6 +59,7 @@ struct AdapterPlan {
 };
 
 AdapterPlan make_adapter_plan(const AdapterSpec& s);
-void launch_adapter(const AdapterPlan& p, int rows, cudaStream_t stream);
+void launch_adapter(const AdapterPlan& p, int rows, cudaStream_t stream,
+                    const uint32_t* ready = nullptr, uint32_t ready_seq = 0, int32_t* err = nullptr);
 
 }  // namespace hmi_b200

@@ -310,6 +310,12 @@ struct Ctx {
   std::vector<size_t> cp_size;
   bool use_batch_copy = true;  // cleared if the driver lacks cudaMemcpyBatchAsync
   std::vector<cudaEvent_t> ev_layer;
+  // fine mode: d_ready[l] = sequence number of the last batch whose layer-l adapter copies are
+  // complete, written by the copy stream (cuStreamWriteValue32); the fused adapter kernel waits
+  // on it on the device, so the compute stream carries no cross-stream event wait
+  DevBuf<uint32_t> d_ready;
+  StreamWriteValue32Fn write_value32 = nullptr;
+  uint32_t ready_seq = 0;
   // decode step captured once per (batch shape, head, tables) and replayed with cudaGraphLaunch
   // (debug flag 4: eager launches every step)
   std::map<std::tuple<int, int, int, uint64_t>, cudaGraphExec_t> dec_graphs;
@@ -536,6 +542,7 @@ Ctx::~Ctx() {
   dec_part.free();
   dec_zero.free();
   for (auto e : ev_layer) cudaEventDestroy(e);
+  d_ready.free();
   for (auto& [c, e] : prof_pending) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -995,6 +1002,9 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     }
   }
 
+  // fine mode with the fused adapter: device-side readiness flags (see d_ready)
+  const bool device_ready = fine && adapter_fused && write_value32 != nullptr;
+  const uint32_t seq = ++ready_seq;
   // ---- copy stream: adapter H2D into HBM slots, one event per layer
   // One cudaMemcpyBatchAsync per layer: a miss-heavy batch issues hundreds of
   // slot-sized copies, and per-call submission cost (not PCIe) bounded them.
@@ -1031,6 +1041,11 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
       n_copies += n;
     }
     HMI_CUDA(cudaEventRecord(ev_layer[l], copy));
+    if (device_ready) {
+      const CUresult r = write_value32(reinterpret_cast<CUstream>(copy),
+                                       reinterpret_cast<CUdeviceptr>(d_ready.p + l), seq, 0);
+      HMI_CHECK(r == CUDA_SUCCESS, HMI_CUDA_ERROR, "cuStreamWriteValue32 failed");
+    }
   });
 
   // ---- compute stream
@@ -1101,9 +1116,11 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
       }
     });
     timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
-    if (fine) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
+    if (fine && !device_ready) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
     if (adapter_fused) {
-      timed(P_AD_UP, s, [&] { launch_adapter(w.adapter, rows, s); });
+      timed(P_AD_UP, s, [&] {
+        launch_adapter(w.adapter, rows, s, device_ready ? d_ready.p + l : nullptr, seq, d_err.p);
+      });
     } else {  // r > 64 or d not a multiple of 128: the two tenant-grouped GEMMs
       timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
       timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
@@ -1468,6 +1485,9 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     HMI_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
     c.ev_layer.resize(c.L);
     for (auto& e : c.ev_layer) HMI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.d_ready.alloc(c.L);
+    HMI_CUDA(cudaMemset(c.d_ready.p, 0, c.L * sizeof(uint32_t)));
+    c.write_value32 = stream_write_value32();
 
     // ---- shared weights: [in x out] f32 -> [out][in] 16-bit, biases / LN f32
     const size_t d = c.d, f = c.f;

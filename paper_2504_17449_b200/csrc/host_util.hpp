@@ -56,6 +56,22 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
+// cuStreamWriteValue32 (stream memory operations), or null when the driver does not offer it.
+using StreamWriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+inline StreamWriteValue32Fn stream_write_value32() {
+  static StreamWriteValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const cudaError_t e = cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+      (void)cudaGetLastError();
+      return static_cast<StreamWriteValue32Fn>(nullptr);
+    }
+    return reinterpret_cast<StreamWriteValue32Fn>(p);
+  }();
+  return fn;
+}
+
 // Row-major 2-D tensor [rows][cols] with an explicit row pitch (bytes).
 inline CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dtype, uint64_t cols,
                                 uint64_t rows, uint64_t row_pitch_bytes, uint32_t box_cols,

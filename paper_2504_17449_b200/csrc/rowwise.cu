@@ -147,7 +147,66 @@ __device__ __forceinline__ int32_t plot_lookup(const PlotDev& P, int32_t version
   return -1;
 }
 
-__global__ void __launch_bounds__(256, 6) retrieve_kernel(PlotDev P, const uint32_t* __restrict__ tokens,
+// Phase 2 of K5 for one position: the mean of its cnt rep rows (ascending window order, f64,
+// retrieval.cpp:114-122) for lane columns (lane + 32 i) * 4, i < V. GV float4 columns of every
+// row are loaded before any is summed, so a warp keeps cnt * GV * 512 B in flight.
+template <int V, int NG, int GV>
+__device__ __forceinline__ void gather_mean(const float* __restrict__ reps, const int32_t* rows,
+                                            int cnt, int d, int lane, long long orow, void* h16,
+                                            int bf16, double* h64) {
+  const double inv = cnt > 0 ? 1.0 / static_cast<double>(cnt) : 0.0;
+  const float4* src[NG];
+#pragma unroll
+  for (int k = 0; k < NG; ++k)
+    src[k] = reinterpret_cast<const float4*>(reps + static_cast<long long>(rows[k] < 0 ? 0 : rows[k]) * d) + lane;
+#pragma unroll
+  for (int g = 0; g < V; g += GV) {
+    float4 xs[NG][GV];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      if (k < cnt) {
+#pragma unroll
+        for (int j = 0; j < GV; ++j)
+          if (g + j < V) xs[k][j] = __ldg(src[k] + 32 * (g + j));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < GV; ++j) {
+      if (g + j < V) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+          if (k < cnt) {
+            a0 = a0 + static_cast<double>(xs[k][j].x);
+            a1 = a1 + static_cast<double>(xs[k][j].y);
+            a2 = a2 + static_cast<double>(xs[k][j].z);
+            a3 = a3 + static_cast<double>(xs[k][j].w);
+          }
+        }
+        a0 *= inv; a1 *= inv; a2 *= inv; a3 *= inv;
+        const int col = (lane + 32 * (g + j)) * 4;
+        if (h64) {
+          double* o = h64 + orow * d + col;
+          o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+        }
+        const float f0 = __double2float_rn(a0), f1 = __double2float_rn(a1);
+        const float f2 = __double2float_rn(a2), f3 = __double2float_rn(a3);
+        uint2 pk;
+        if (bf16) {
+          pk.x = pack16x2<true>(f0, f1);
+          pk.y = pack16x2<true>(f2, f3);
+        } else {
+          pk.x = pack16x2<false>(f0, f1);
+          pk.y = pack16x2<false>(f2, f3);
+        }
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(h16) + orow * d + col) = pk;
+      }
+    }
+  }
+}
+
+template <int V, int NG, int GV, int MINB>
+__global__ void __launch_bounds__(256, MINB) retrieve_kernel(PlotDev P, const uint32_t* __restrict__ tokens,
                                                        const int* __restrict__ lens,
                                                        const int* __restrict__ req_version,
                                                        int S, int causal, void* __restrict__ h16,
@@ -265,11 +324,10 @@ __global__ void __launch_bounds__(256, 6) retrieve_kernel(PlotDev P, const uint3
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int d = P.d;
-  const int V = d / 128;  // float4 per lane
   for (int p = p0 + warp; p < p1; p += nwarps) {
     const long long orow = dec_pos ? static_cast<long long>(b) : static_cast<long long>(b) * S + p;
-    int32_t rows[kMaxNgram];
-    int32_t levs[kMaxNgram];
+    int32_t rows[kMaxNgram] = {};
+    int32_t levs[kMaxNgram] = {};
     int cnt = 0;
     if (p < len) {
       if (causal) {
@@ -296,49 +354,49 @@ __global__ void __launch_bounds__(256, 6) retrieve_kernel(PlotDev P, const uint3
       gather[orow * n + lane] = gr;
       levels[orow * n + lane] = gl;
     }
-    const double inv = cnt > 0 ? 1.0 / static_cast<double>(cnt) : 0.0;
-    for (int i = 0; i < V; ++i) {
-      const int col = (lane + 32 * i) * 4;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      float4 xs[kMaxNgram];
+    if constexpr (V > 0) {
+      gather_mean<V, NG, GV>(P.reps, rows, cnt, d, lane, orow, h16, bf16, h64);
+    } else {
+      const double inv = cnt > 0 ? 1.0 / static_cast<double>(cnt) : 0.0;
+      for (int i = 0; i < d / 128; ++i) {
+        const int col = (lane + 32 * i) * 4;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        float4 xs[kMaxNgram];
 #pragma unroll
-      for (int k = 0; k < kMaxNgram; ++k) {
-        if (k < cnt) {
-          const int32_t r = rows[k] < 0 ? 0 : rows[k];
-          xs[k] = __ldg(reinterpret_cast<const float4*>(P.reps + static_cast<long long>(r) * d + col));
+        for (int k = 0; k < kMaxNgram; ++k) {
+          if (k < cnt) {
+            const int32_t r = rows[k] < 0 ? 0 : rows[k];
+            xs[k] = __ldg(reinterpret_cast<const float4*>(P.reps + static_cast<long long>(r) * d + col));
+          }
         }
-      }
 #pragma unroll
-      for (int k = 0; k < kMaxNgram; ++k) {  // ascending window order (add_f64 sweep)
-        if (k < cnt) {
-          a0 = a0 + static_cast<double>(xs[k].x);
-          a1 = a1 + static_cast<double>(xs[k].y);
-          a2 = a2 + static_cast<double>(xs[k].z);
-          a3 = a3 + static_cast<double>(xs[k].w);
+        for (int k = 0; k < kMaxNgram; ++k) {  // ascending window order (add_f64 sweep)
+          if (k < cnt) {
+            a0 = a0 + static_cast<double>(xs[k].x);
+            a1 = a1 + static_cast<double>(xs[k].y);
+            a2 = a2 + static_cast<double>(xs[k].z);
+            a3 = a3 + static_cast<double>(xs[k].w);
+          }
         }
+        a0 *= inv; a1 *= inv; a2 *= inv; a3 *= inv;
+        if (h64) {
+          double* o = h64 + orow * d + col;
+          o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+        }
+        // f64 -> f32 -> 16-bit with hardware conversions (the f64 values are the exact
+        // Eq. 2 result; the 16-bit copy is the GEMM operand)
+        const float f0 = __double2float_rn(a0), f1 = __double2float_rn(a1);
+        const float f2 = __double2float_rn(a2), f3 = __double2float_rn(a3);
+        uint2 pk;
+        if (bf16) {
+          pk.x = pack16x2<true>(f0, f1);
+          pk.y = pack16x2<true>(f2, f3);
+        } else {
+          pk.x = pack16x2<false>(f0, f1);
+          pk.y = pack16x2<false>(f2, f3);
+        }
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(h16) + orow * d + col) = pk;
       }
-      a0 *= inv; a1 *= inv; a2 *= inv; a3 *= inv;
-      if (h64) {
-        double* o = h64 + orow * d + col;
-        o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
-      }
-      uint2 pk;
-      // f64 -> f32 -> 16-bit with hardware conversions (the f64 values are the exact
-      // Eq. 2 result; the 16-bit copy is the GEMM operand)
-      const float f0 = __double2float_rn(a0), f1 = __double2float_rn(a1);
-      const float f2 = __double2float_rn(a2), f3 = __double2float_rn(a3);
-      if (bf16) {
-        __nv_bfloat162 x = __floats2bfloat162_rn(f0, f1);
-        __nv_bfloat162 y = __floats2bfloat162_rn(f2, f3);
-        pk.x = *reinterpret_cast<uint32_t*>(&x);
-        pk.y = *reinterpret_cast<uint32_t*>(&y);
-      } else {
-        __half2 x = __floats2half2_rn(f0, f1);
-        __half2 y = __floats2half2_rn(f2, f3);
-        pk.x = *reinterpret_cast<uint32_t*>(&x);
-        pk.y = *reinterpret_cast<uint32_t*>(&y);
-      }
-      *reinterpret_cast<uint2*>(static_cast<uint16_t*>(h16) + orow * d + col) = pk;
     }
   }
 }
@@ -634,9 +692,26 @@ void launch_retrieve(const PlotDev& plot, const uint32_t* tokens, const int* len
   const int n = plot.ngram;
   const size_t smem = static_cast<size_t>(kRetrieveChunk + kMaxNgram) * (n * (n + 1) / 2) *
                       plot.max_depth * sizeof(int32_t);
-  retrieve_kernel<<<grid, 256, smem, stream>>>(plot, tokens, lens, req_version, S, causal, h16,
-                                                precision, h64_debug, gather, levels, err,
-                                                dec_pos, tok_stride);
+  // phase 2 specialised for the hidden sizes of BASELINE's configs (d = 256 / 768 / 1024) and
+  // the window count per position (encoder: n windows; causal: 1): two float4 columns of every
+  // row in flight per lane at 5 CTAs per SM (C2 in-step 107 -> 82 us; all six columns in flight
+  // at 2 CTAs per SM: 126 us, one column at 6 CTAs: 88 us, three at 4: 96 us — same box)
+  const int V = plot.d / 128;
+  const int NG = causal ? 1 : plot.ngram;
+  auto go = [&](auto kern) {
+    kern<<<grid, 256, smem, stream>>>(plot, tokens, lens, req_version, S, causal, h16, precision,
+                                      h64_debug, gather, levels, err, dec_pos, tok_stride);
+  };
+#define HMI_RETR_CASE(VV, NN)                   \
+  if (V == VV && NG == NN) {                    \
+    go(retrieve_kernel<VV, NN, 2, 5>);          \
+    HMI_CUDA(cudaGetLastError());               \
+    return;                                     \
+  }
+  HMI_RETR_CASE(6, 3) HMI_RETR_CASE(6, 1) HMI_RETR_CASE(8, 3) HMI_RETR_CASE(8, 1)
+  HMI_RETR_CASE(2, 3) HMI_RETR_CASE(2, 1)
+#undef HMI_RETR_CASE
+  go(retrieve_kernel<0, kMaxNgram, 1, 6>);
   HMI_CUDA(cudaGetLastError());
 }
 
