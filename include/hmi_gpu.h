@@ -414,8 +414,8 @@ int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups, const uint16
                        int precision, void* out, float* elapsed_ms);
 
 /* host -> HBM copy probe for adapter-slot transfers (n pieces of `bytes`): mode 0 one
- * contiguous copy, 1 n cudaMemcpyAsync, 2 one cudaMemcpyBatchAsync, 3 zero-copy gather
- * kernel over mapped pinned memory with `ctas` CTAs; *gbps = achieved rate */
+ * contiguous copy, 1 n cudaMemcpyAsync, 3 zero-copy gather kernel over mapped pinned
+ * memory with `ctas` CTAs; *gbps = achieved rate */
 int hmi_gpu_copy_probe(int device, int n, size_t bytes, int mode, int ctas, double* gbps);
 
 #ifdef __cplusplus

@@ -541,11 +541,13 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
 }
 
 // ---------------------------------------------------------------------------
-// One CTA per decode row: y = relu(a.Wd + bd).Wu + bu + a + h, x = LN1(y).
+// One CTA per decode row: y = relu(ctx.Wc + bc).Wu + bu + a + h, x = LN1(y), where the slot's
+// folded down projection Wc = Wo.Wd, bc = bo.Wd + bd (adapter.cu) makes relu(ctx.Wc + bc) the
+// reference's relu(a.Wd + bd).
 // RP > 0: bottleneck fixed at compile time (all weight loads of a unit / an output in flight)
 template <int RP>
 __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A) {
-  extern __shared__ float sm[];  // a[d], y[d], mid[r_pad]
+  extern __shared__ float sm[];  // ctx[d] (the down projection's input), y[d], mid[r_pad]
   __shared__ float red[32];
   const int b = blockIdx.x;
   const int d = A.d, rp = RP > 0 ? RP : A.r_pad;
@@ -563,7 +565,8 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   const uint16_t* wu = wd + static_cast<size_t>(rp) * d;                 // [d][r_pad]
   const float* bd = reinterpret_cast<const float*>(wu + static_cast<size_t>(d) * rp);
   const float* bu = bd + rp;
-  const uint16_t* arow = A.a16 + static_cast<long long>(b) * d;
+  const uint16_t* arow = A.ctx16 + static_cast<long long>(b) * d;
+  const uint16_t* skiprow = A.a16 + static_cast<long long>(b) * d;  // the adapter's skip input
   const uint16_t* hrow = A.h16 + static_cast<long long>(b) * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) a[i] = ld16(arow, i, A.bf16);
   __syncthreads();
@@ -646,7 +649,7 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
       }
-      const float v = acc + bu[i] + a[i] + ld16(hrow, i, A.bf16);
+      const float v = acc + bu[i] + ld16(skiprow, i, A.bf16) + ld16(hrow, i, A.bf16);
       y[i] = v;
       s1 += v;
     }
@@ -673,7 +676,7 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
         for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
       }
     }
-    const float v = acc + bu[i] + a[i] + ld16(hrow, i, A.bf16);
+    const float v = acc + bu[i] + ld16(skiprow, i, A.bf16) + ld16(hrow, i, A.bf16);
     y[i] = v;
     s1 += v;
   }

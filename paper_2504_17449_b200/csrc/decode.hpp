@@ -75,6 +75,7 @@ void launch_attn_decode_tma(const AttnDecodeArgs& a, const AttnDecodeMaps& m, in
                             int heads, cudaStream_t stream);
 
 struct AdapterRowsArgs {
+  const uint16_t* ctx16 = nullptr;  // [n][d] attention context (input of the folded down proj.)
   const uint16_t* a16 = nullptr;  // [n][d] attention output (after Wo, bo)
   const uint16_t* h16 = nullptr;  // [n][d] layer input (residual)
   const int32_t* req_task = nullptr;

@@ -122,7 +122,6 @@ struct LayerDev {
   uint16_t *wqkv, *wo, *w1, *w2;  // [N][K] 16-bit (transposed from [in x out])
   float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
   GemmPlan qkv, oproj, ad_down, ad_up, ffn1, ffn2;
-  AdapterPlan adapter;         // fused down + up + skip + residual (adapter.cu), folded LN mode
   // LayerNorm folding (default mode): gamma folded into the consumer's weights, beta.W into
   // its bias, and the per-column sums of the folded 16-bit weights for the mean correction
   void* mem_fold = nullptr;
@@ -306,9 +305,6 @@ struct Ctx {
   uint64_t bytes_copied = 0;
   uint64_t n_launches = 0, n_batches = 0, n_copies = 0;
   uint64_t next_ticket = 0;
-  std::vector<void*> cp_dst, cp_src;
-  std::vector<size_t> cp_size;
-  bool use_batch_copy = true;  // cleared if the driver lacks cudaMemcpyBatchAsync
   std::vector<cudaEvent_t> ev_layer;
   // fine mode: d_ready[l] = sequence number of the last batch whose layer-l adapter copies are
   // complete, written by the copy stream (cuStreamWriteValue32); the fused adapter kernel waits
@@ -358,9 +354,14 @@ struct Ctx {
   // last batch (introspection)
   uint32_t last_n = 0, last_S = 0;
   uint32_t debug_flags = 0;
-  // one fused adapter kernel per layer when r <= 64 and d % 128 == 0, else the two
-  // tenant-grouped GEMMs
-  bool adapter_fused = true;
+  // adapter up projection as tenant K blocks of the O projection (kEpiExt) when r <= 64 and
+  // d % 128 == 0, else a separate tenant-grouped up GEMM (+ skip + residual)
+  bool oproj_ext = true;
+  // adapter fold (adapter.cu): the layers' f32 Wo / bo, and device staging for slot images
+  DevBuf<float> wo32, bo32;
+  DevBuf<uint8_t> fold_in, fold_out;
+  size_t fold_cap = 0;  // tasks per staging pass
+  cudaStream_t fold_stream = nullptr;
   DevBuf<float2> d_stats1, d_stats2;  // partial row (sum, sumsq) of y1 / y2, [rows][kStatsLd]
   static constexpr int kStatsLd = kStatsStride;
   int stats1_bn = 0, stats2_bn = 0, stats1_n = 0, stats2_n = 0;
@@ -500,6 +501,8 @@ struct Ctx {
   void build_plans();
   void upload_plot_hash();
   void convert_adapter(const float* src, uint8_t* dst) const;
+  // re-associate the down projections of converted host blocks onto ctx (adapter.cu); in place
+  void fold_adapters(uint8_t* const* blocks, size_t n);
   int submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_host,
              const uint32_t* tokens_dev, uint32_t stride, const uint32_t* lens_host,
              const uint32_t* lens_dev, uint32_t max_len, float* d_scores_out,
@@ -556,6 +559,8 @@ Ctx::~Ctx() {
   d_inst_version.free(); d_inst_task.free(); d_inst_head.free(); d_slot_of.free();
   d_slots.free(); d_parent.free(); d_reps.free(); d_head_arena.free(); d_head_off.free();
   d_head_labels.free(); d_head_kind.free(); arena.free();
+  wo32.free(); bo32.free(); fold_in.free(); fold_out.free();
+  if (fold_stream) cudaStreamDestroy(fold_stream);
   if (compute) cudaStreamDestroy(compute);
   if (copy) cudaStreamDestroy(copy);
 }
@@ -594,6 +599,36 @@ void Ctx::convert_adapter(const float* src, uint8_t* dst) const {
   }
 }
 
+void Ctx::fold_adapters(uint8_t* const* blocks, size_t n) {
+  if (n == 0) return;
+  HMI_CUDA(cudaSetDevice(device));
+  const size_t per = static_cast<size_t>(L) * slot_bytes;
+  if (fold_cap == 0) {
+    fold_cap = std::max<size_t>(1, (64ull << 20) / per);
+    fold_in.alloc(fold_cap * per);
+    fold_out.alloc(fold_cap * per);
+    HMI_CUDA(cudaStreamCreateWithFlags(&fold_stream, cudaStreamNonBlocking));
+  }
+  const size_t off_bd = static_cast<size_t>(r_pad) * d * 2 * 2;
+  for (size_t b0 = 0; b0 < n; b0 += fold_cap) {
+    const size_t nb = std::min(fold_cap, n - b0);
+    for (size_t k = 0; k < nb; ++k)
+      HMI_CUDA(cudaMemcpyAsync(fold_in.p + k * per, blocks[b0 + k], per, cudaMemcpyHostToDevice,
+                               fold_stream));
+    launch_adapter_fold(fold_in.p, fold_out.p, static_cast<int>(nb * L), wo32.p, bo32.p, L, d,
+                        r_pad, slot_bytes, off_bd, static_cast<int>(opt.precision), fold_stream);
+    for (size_t k = 0; k < nb; ++k) {  // Wc^T and bc of every layer back into the host block
+      HMI_CUDA(cudaMemcpy2DAsync(blocks[b0 + k], slot_bytes, fold_out.p + k * per, slot_bytes,
+                                 static_cast<size_t>(r_pad) * d * 2, L, cudaMemcpyDeviceToHost,
+                                 fold_stream));
+      HMI_CUDA(cudaMemcpy2DAsync(blocks[b0 + k] + off_bd, slot_bytes, fold_out.p + k * per + off_bd,
+                                 slot_bytes, static_cast<size_t>(r_pad) * 4, L,
+                                 cudaMemcpyDeviceToHost, fold_stream));
+    }
+    HMI_CUDA(cudaStreamSynchronize(fold_stream));
+  }
+}
+
 void Ctx::build_plans() {
   attn.clear();
   for (int l = 0; l < (kv ? L : 1); ++l)
@@ -604,7 +639,7 @@ void Ctx::build_plans() {
     const int mt = max_rows / 128;
     stats1_bn = pick_bn(d, mt, sms);
     stats2_bn = pick_bn(d, mt, sms, true);
-    stats1_n = adapter_fused ? 2 : d / 64;
+    stats1_n = d / 64;
     stats2_n = d / 64;
     HMI_CHECK(d % 64 == 0 && d / 64 <= kStatsLd, HMI_CONFIG_ERROR,
               "hidden size too wide for the LayerNorm statistics buffer");
@@ -633,8 +668,8 @@ void Ctx::build_plans() {
     s.b = w.wo; s.N = d; s.b_ld = d; s.b_group_stride_bytes = size_t(d) * d * 2;
     s.bias = w.bo; s.c = a16.p; s.c_ld = d; s.epi = 0; s.bn = pick_bn(d, m_tiles, sms, true);
     w.oproj = make_gemm_plan(s);
-    // adapter down (grouped): mid = relu(a . Wd + bd)
-    s.a = a16.p; s.a_ld = d; s.K = d;
+    // adapter down (grouped, folded weights): mid = relu(ctx . Wc + bc) = relu(a . Wd + bd)
+    s.a = ctx16.p; s.a_ld = d; s.K = d;
     s.b = arena.p; s.N = r_pad; s.groups = static_cast<int>(n_slots); s.b_ld = d;
     s.b_group_stride_bytes = slot_bytes;
     s.bias = reinterpret_cast<const float*>(arena.p + off_bd);
@@ -701,20 +736,28 @@ void Ctx::build_plans() {
         }
         u.bn = stats1_bn;
         w.ad_up = make_gemm_plan(u);
-        if (adapter_fused) {
-          AdapterSpec as;
-          as.a = a16.p; as.h = h16.p; as.out = x16.p;
-          as.arena = arena.p; as.slot_bytes = slot_bytes;
-          as.off_wu = off_wu; as.off_bd = off_bd; as.off_bu = off_bu;
-          as.n_slots = static_cast<int>(n_slots); as.d = d; as.r_pad = r_pad;
-          as.rows = max_rows; as.precision = prec;
-          as.tile_slot = u.tile_slot;
-          as.stats_out = d_stats1.p; as.stats_ld = kStatsLd;
+        if (oproj_ext) {
+          // y1 = [ctx | mid] . [Wo ; Wu_tenant] + bo + bu + LN2_{l-1}(y2)  (+ partial stats of y1)
+          GemmSpec o;
+          o.precision = prec;
+          o.a_rows = max_rows;
+          o.a = ctx16.p; o.a_ld = d; o.K = d;
+          o.b = w.wo; o.N = d; o.groups = 1; o.b_ld = d; o.b_group_stride_bytes = size_t(d) * d * 2;
+          o.bias = w.bo; o.tile_slot = u.tile_slot;
+          o.res0 = h16.p; o.res_ld = d; o.c = x16.p; o.c_ld = d;
+          o.epi = kEpiExt | kEpiRes1 | kEpiStats | (prev ? kEpiRes0LN : 0); o.cta2 = true;
+          o.stats_out = d_stats1.p; o.stats_ld = kStatsLd;
           if (prev) {
-            as.r_stats = d_stats2.p; as.r_stats_n = stats2_n;
-            as.r_gamma = prev->ln2g; as.r_beta = prev->ln2b;
+            o.r_stats = d_stats2.p; o.r_stats_n = stats2_n;
+            o.r_gamma = prev->ln2g; o.r_beta = prev->ln2b; o.inv_n = inv_d;
           }
-          w.adapter = make_adapter_plan(as);
+          o.ext_a = mid16.p; o.ext_k = r_pad;
+          o.ext_b = arena.p + off_wu; o.ext_b_ld = r_pad; o.ext_groups = static_cast<int>(n_slots);
+          o.ext_b_stride = slot_bytes;
+          o.ext_bias = reinterpret_cast<const float*>(arena.p + off_bu);
+          o.ext_bias_stride = static_cast<long long>(slot_bytes / 4);
+          o.bn = pick_bn(d, m_tiles, sms, true);
+          w.oproj = make_gemm_plan(o);
         }
       }
       {  // FFN1 on LN1(y1)
@@ -1002,40 +1045,20 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
     }
   }
 
-  // fine mode with the fused adapter: device-side readiness flags (see d_ready)
-  const bool device_ready = fine && adapter_fused && write_value32 != nullptr;
+  // fine mode: device-side readiness flags (see d_ready), waited on by the first reader of
+  // the layer's slots (the tenant-grouped down GEMM)
+  const bool device_ready = fine && write_value32 != nullptr;
   const uint32_t seq = ++ready_seq;
   // ---- copy stream: adapter H2D into HBM slots, one event per layer
-  // One cudaMemcpyBatchAsync per layer: a miss-heavy batch issues hundreds of
-  // slot-sized copies, and per-call submission cost (not PCIe) bounded them.
+  // One cudaMemcpyAsync per (task, layer) slot image, in layer order; each layer's event
+  // (and device flag) follows its copies.
   for (int l = 0; l < L; ++l) traced(kStagePrefetch, l, kWorkerIo, copy, [&] {
     const size_t n = loads[l].size();
     if (n != 0) {
-      cp_dst.resize(n);
-      cp_src.resize(n);
-      cp_size.assign(n, slot_bytes);
       for (size_t i = 0; i < n; ++i) {
-        cp_dst[i] = arena.p + static_cast<size_t>(loads[l][i].second) * slot_bytes;
-        cp_src[i] = store[loads[l][i].first] + static_cast<size_t>(l) * slot_bytes;
-      }
-      bool batched = false;
-      if (n > 1 && use_batch_copy) {
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-        size_t attr_idx = 0, fail_idx = 0;
-        const cudaError_t e = cudaMemcpyBatchAsync(cp_dst.data(), cp_src.data(), cp_size.data(),
-                                                   n, &attr, &attr_idx, 1, &fail_idx, copy);
-        if (e == cudaSuccess) {
-          batched = true;
-        } else {
-          (void)cudaGetLastError();
-          use_batch_copy = false;  // driver without batch copies: per-copy path from now on
-        }
-      }
-      if (!batched) {
-        for (size_t i = 0; i < n; ++i)
-          HMI_CUDA(cudaMemcpyAsync(cp_dst[i], cp_src[i], slot_bytes, cudaMemcpyHostToDevice, copy));
+        HMI_CUDA(cudaMemcpyAsync(arena.p + static_cast<size_t>(loads[l][i].second) * slot_bytes,
+                                 store[loads[l][i].first] + static_cast<size_t>(l) * slot_bytes,
+                                 slot_bytes, cudaMemcpyHostToDevice, copy));
       }
       bytes_copied += n * slot_bytes;
       n_copies += n;
@@ -1115,14 +1138,15 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
                          prec, s);
       }
     });
-    timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
     if (fine && !device_ready) HMI_CUDA(cudaStreamWaitEvent(s, ev_layer[l], 0));
-    if (adapter_fused) {
-      timed(P_AD_UP, s, [&] {
-        launch_adapter(w.adapter, rows, s, device_ready ? d_ready.p + l : nullptr, seq, d_err.p);
-      });
-    } else {  // r > 64 or d not a multiple of 128: the two tenant-grouped GEMMs
-      timed(P_AD_DOWN, s, [&] { launch_gemm(w.ad_down, rows, s); });
+    // mid = ReLU(ctx . Wc + bc): the first reader of this layer's slots
+    timed(P_AD_DOWN, s, [&] {
+      launch_gemm(w.ad_down, rows, s, device_ready ? d_ready.p + l : nullptr, seq, d_err.p);
+    });
+    if (oproj_ext) {  // O projection with the tenants' up projections as extra K blocks
+      timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
+    } else {  // r > 64 or d not a multiple of 128: O projection, then the grouped up GEMM
+      timed(P_OPROJ, s, [&] { launch_gemm(w.oproj, rows, s); });
       timed(P_AD_UP, s, [&] { launch_gemm(w.ad_up, rows, s); });
     }
     timed(P_FFN1, s, [&] { launch_gemm(w.ffn1, rows, s); });
@@ -1180,7 +1204,7 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
   inflight.push_back(Inflight{st.done, si, uniq});
   undo.armed = false;
   last_n = n_req;
-  const uint64_t per_layer = adapter_fused ? 6ull : 7ull;
+  const uint64_t per_layer = oproj_ext ? 6ull : 7ull;
   // fetch_inputs + route + retrieve (+ apply_deltas) + layers + head
   n_launches += (delta.empty() ? 0 : 1) + 3 + (gen ? 0 : 1) + per_layer * L;
   if (wide_head >= 0) n_launches += 3 + (gen ? (n_new - 1ull) * (3 + 7ull * L) : 0);
@@ -1305,6 +1329,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
       timed(P_OPROJ, s, [&] { launch_gemm(dp.oproj, Mp, s); });
       timed(P_AD_UP, s, [&] {
         AdapterRowsArgs a;
+        a.ctx16 = ctx16.p;
         a.a16 = a16.p;
         a.h16 = h16.p;
         a.req_task = d_req_task.p;
@@ -1494,6 +1519,8 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     const size_t lf = 4 * (d * d + d) + (d * f + f) + (f * d + d) + 4 * d;
     const int prec = static_cast<int>(c.opt.precision);
     c.layers.resize(c.L);
+    c.wo32.alloc(static_cast<size_t>(c.L) * d * d);
+    c.bo32.alloc(static_cast<size_t>(c.L) * d);
     std::vector<uint16_t> tmp;
     for (int l = 0; l < c.L; ++l) {
       const float* w = higher_f32 + l * lf;
@@ -1519,6 +1546,8 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       transpose(wk, d, d, tmp.data() + d * d);
       transpose(wv, d, d, tmp.data() + 2 * d * d);
       transpose(wo, d, d, tmp.data() + 3 * d * d);
+      HMI_CUDA(cudaMemcpy(c.wo32.p + l * d * d, wo, d * d * 4, cudaMemcpyHostToDevice));
+      HMI_CUDA(cudaMemcpy(c.bo32.p + l * d, bo, d * 4, cudaMemcpyHostToDevice));
       transpose(w1, d, f, tmp.data() + 4 * d * d);
       transpose(w2, f, d, tmp.data() + 4 * d * d + f * d);
       HMI_CUDA(cudaMemcpy(p16, tmp.data(), n16 * 2, cudaMemcpyHostToDevice));
@@ -1610,7 +1639,9 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
         for (auto& e : c.dec_ev) HMI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
     }
-    c.mid16.alloc(R * c.r_pad); c.x16.alloc(R * d); c.ffn16.alloc(R * f);
+    // + 128 zero rows: the other CTA's half of the O projection's tenant K blocks
+    c.mid16.alloc((R + 128) * c.r_pad);
+    HMI_CUDA(cudaMemset(c.mid16.p, 0, c.mid16.n * 2)); c.x16.alloc(R * d); c.ffn16.alloc(R * f);
     c.y32.alloc(R * d); c.h32.alloc(R * d);
     const size_t B = c.opt.max_batch;
     c.d_inst.alloc(B); c.d_tokens.alloc(B * c.S_max); c.d_lens.alloc(B);
@@ -1673,7 +1704,7 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
     c.pool = std::make_unique<SlotPool>(pool_bytes, static_cast<uint32_t>(n_slots64));
     c.arena.alloc(static_cast<size_t>(n_slots64) * c.slot_bytes);
     HMI_CUDA(cudaMemset(c.arena.p, 0, c.arena.n));
-    c.adapter_fused = c.r_pad == 64 && c.d % 128 == 0;
+    c.oproj_ext = c.r_pad == 64 && c.d % 128 == 0;
     c.d_stats1.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.d_stats2.alloc(static_cast<size_t>(c.max_rows) * Ctx::kStatsLd);
     c.build_plans();
@@ -2013,7 +2044,13 @@ int hmi_gpu_register_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adap
     HMI_CHECK(task_idx < c.store.size(), HMI_CONFIG_ERROR, "task index exceeds max_tasks");
     if (c.store[task_idx]) throw HmiError(HMI_CONFLICT_ERROR, "adapter set for task already registered");
     uint8_t* p = c.store_alloc();
-    c.convert_adapter(adapter_f32, p);
+    try {
+      c.convert_adapter(adapter_f32, p);
+      c.fold_adapters(&p, 1);
+    } catch (...) {
+      c.free_blocks.push_back(p);
+      throw;
+    }
     c.store[task_idx] = p;
     c.pool->set_task(task_idx, static_cast<uint32_t>(c.L), c.ref_layer_bytes);
   });
@@ -2065,6 +2102,12 @@ static int register_many(hmi_gpu_ctx* ctx, uint32_t n, const uint32_t* task_idx,
         for (uint8_t* b : blocks) c.free_blocks.push_back(b);
         throw HmiError(code[k], "task " + std::to_string(task_idx[k]) + ": " + msg[k]);
       }
+    }
+    try {
+      c.fold_adapters(blocks.data(), blocks.size());
+    } catch (...) {
+      for (uint8_t* b : blocks) c.free_blocks.push_back(b);
+      throw;
     }
     for (uint32_t k = 0; k < n; ++k) {
       c.store[task_idx[k]] = blocks[k];
@@ -2131,6 +2174,7 @@ int hmi_gpu_replace_task(hmi_gpu_ctx* ctx, uint32_t task_idx, const float* adapt
       throw HmiError(HMI_ROUTING_ERROR, "no adapter set registered for task");
     HMI_CHECK(!c.exported.count(task_idx), HMI_CONFLICT_ERROR, "task is exported to a peer engine");
     c.convert_adapter(adapter_f32, c.store[task_idx]);
+    c.fold_adapters(&c.store[task_idx], 1);
     evict_task_slots(c, task_idx, false);
   });
 }
@@ -2276,6 +2320,7 @@ int hmi_gpu_import_task(hmi_gpu_ctx* dst, uint32_t task_idx, const hmi_task_expo
       write_slot_entries(c, recs);
       if (adapter_f32) {
         c.convert_adapter(adapter_f32, p);
+        c.fold_adapters(&p, 1);
       } else {
         // the host copy (for later refills after eviction) is the slot image itself
         for (int l = 0; l < c.L; ++l)

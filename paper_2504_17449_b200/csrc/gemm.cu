@@ -48,6 +48,15 @@ KernelFn pick_epi_t(int epi) {
       return kernel_ptr<BN, T | kEpiRes2 | kEpiRes1LN | kEpiStats, C2>();
     default: break;
   }
+  if constexpr (C2) {  // O projection + tenant up projection (+ LN'd residual) + statistics
+    switch (epi) {
+      case kEpiExt | kEpiRes1 | kEpiStats:
+        return kernel_ptr<BN, T | kEpiExt | kEpiRes1 | kEpiStats, true>();
+      case kEpiExt | kEpiRes1 | kEpiRes0LN | kEpiStats:
+        return kernel_ptr<BN, T | kEpiExt | kEpiRes1 | kEpiRes0LN | kEpiStats, true>();
+      default: break;
+    }
+  }
   if constexpr (!C2 && BN <= 192) {  // adapter up with TMA-staged residuals
     switch (epi) {
       case kEpiRes2 | kEpiStats | kEpiResTma:
@@ -69,9 +78,15 @@ KernelFn pick_epi(int epi) {
 KernelFn pick_kernel(int bn, int epi, bool c2, int* smem_bytes) {
   if (c2) {
     switch (bn) {
-      case 128: *smem_bytes = Gemm2Smem<128>::kTotal; return pick_epi<128, true>(epi);
-      case 192: *smem_bytes = Gemm2Smem<192>::kTotal; return pick_epi<192, true>(epi);
-      case 256: *smem_bytes = Gemm2Smem<256>::kTotal; return pick_epi<256, true>(epi);
+      case 128:
+        *smem_bytes = pair_staged(epi) ? Gemm2Smem<128, true>::kTotal : Gemm2Smem<128>::kTotal;
+        return pick_epi<128, true>(epi);
+      case 192:
+        *smem_bytes = pair_staged(epi) ? Gemm2Smem<192, true>::kTotal : Gemm2Smem<192>::kTotal;
+        return pick_epi<192, true>(epi);
+      case 256:
+        *smem_bytes = pair_staged(epi) ? Gemm2Smem<256, true>::kTotal : Gemm2Smem<256>::kTotal;
+        return pick_epi<256, true>(epi);
       default: return nullptr;
     }
   }
@@ -98,7 +113,11 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   HMI_CHECK(s.a_rows % kBlockM == 0, HMI_CONFIG_ERROR, "gemm: A rows must be a multiple of 128");
   GemmPlan p;
   const int epi = s.epi | (s.precision == 1 ? kEpiBf16 : 0);
-  const bool c2 = s.cta2 && s.groups == 1 && s.tile_slot == nullptr && s.bn >= 128;
+  const bool ext = (s.epi & kEpiExt) != 0;
+  const bool c2 = s.cta2 && s.groups == 1 && (s.tile_slot == nullptr || ext) && s.bn >= 128;
+  HMI_CHECK(!ext || (c2 && s.tile_slot && s.ext_a && s.ext_b && s.ext_bias && s.ext_k > 0 &&
+                     s.ext_k % kBlockK == 0),
+            HMI_CONFIG_ERROR, "gemm: tenant extension needs the pair kernel and its operands");
   p.two_cta = c2;
   p.fn = reinterpret_cast<void*>(pick_kernel(s.bn, epi, c2, &p.smem_bytes));
   HMI_CHECK(p.fn != nullptr, HMI_CONFIG_ERROR, "gemm: unsupported epilogue");
@@ -135,6 +154,26 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
                                kBlockK, s.bn / (2 * p.tail_s1), CU_TENSOR_MAP_SWIZZLE_128B);
     }
   }
+  p.maps.xa = p.maps.xb = p.maps.xb0 = p.maps.xb1 = p.maps.res = p.maps.c;
+  if (c2 && (s.epi & kEpiRes1) && !(s.epi & (kEpiRes2 | kEpiOutF32))) {
+    HMI_CHECK(s.res0 != nullptr, HMI_CONFIG_ERROR, "gemm: residual missing");
+    p.maps.res = make_tmap_2d(s.res0, t16, s.N, s.a_rows, s.res_ld * 2ull, 64, 32,
+                              CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (ext) {
+    // ext rows: a_rows + 128 (the last 128 are the zero rows of the other CTA's half)
+    p.maps.xa = make_tmap_2d(s.ext_a, t16, s.ext_k, s.a_rows + kBlockM, s.ext_k * 2ull, kBlockK,
+                             kBlockM, CU_TENSOR_MAP_SWIZZLE_128B);
+    auto xb = [&](int width) {
+      return make_tmap_3d(s.ext_b, t16, s.ext_k, s.N, s.ext_groups, s.ext_b_ld * 2ull,
+                          s.ext_b_stride, kBlockK, width, CU_TENSOR_MAP_SWIZZLE_128B);
+    };
+    p.maps.xb = xb(s.bn / 2);
+    if (p.tail_s0) {
+      p.maps.xb0 = xb(s.bn / (2 * p.tail_s0));
+      p.maps.xb1 = xb(s.bn / (2 * p.tail_s1));
+    }
+  }
   p.args = GemmArgs{};
   p.args.N = s.N;
   p.args.K = s.K;
@@ -155,6 +194,12 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   p.args.r_gamma = s.r_gamma;
   p.args.r_beta = s.r_beta;
   p.args.inv_n = s.inv_n;
+  if (ext) {
+    p.args.ext_kb = s.ext_k / kBlockK;
+    p.args.ext_zero_row = s.a_rows;
+    p.args.bias2 = s.ext_bias;
+    p.args.bias2_stride = s.ext_bias_stride;
+  }
   if (s.epi & kEpiStats) HMI_CHECK(s.stats_out && s.stats_ld == kStatsStride && s.N % 64 == 0 && s.N / 64 <= kStatsStride, HMI_CONFIG_ERROR, "gemm: stats buffer");
   if (s.epi & kEpiFoldLN) HMI_CHECK(s.a_stats && s.colsum && s.inv_n > 0.f, HMI_CONFIG_ERROR, "gemm: fold args");
   if (s.epi & (kEpiRes0LN | kEpiRes1LN))
@@ -189,7 +234,8 @@ GemmPlan make_gemm_plan(const GemmSpec& s) {
   return p;
 }
 
-void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
+void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream, const uint32_t* ready,
+                 uint32_t ready_seq, int32_t* err) {
   if (M <= 0) return;
   HMI_CHECK(M % kBlockM == 0 && M <= p.max_rows, HMI_DIMENSION_ERROR,
             "gemm: M must be a multiple of 128 within the planned buffer");
@@ -213,6 +259,11 @@ void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream) {
   a.tail_split = 1;
   a.idesc_tail = a.idesc;
   a.tail_r1 = 0;
+  a.ready = ready;
+  a.ready_seq = ready_seq;
+  a.err = err;
+  HMI_CHECK(ready == nullptr || (!p.two_cta && err != nullptr), HMI_CONFIG_ERROR,
+            "gemm: readiness wait needs the 1-CTA kernel and an error word");
   if (p.two_cta) {
     const int rows = 2;  // M tiles per pair unit
     const int units = (a.num_m_tiles + rows - 1) / rows * a.num_n_tiles;
@@ -322,7 +373,7 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
 // ---------------------------------------------------------------------------
 // C ABI: host -> HBM copy probe (adapter slot transfers): n pieces of `bytes` each from
 // pinned host memory into scattered device slots. mode 0: one contiguous copy of n * bytes;
-// 1: n cudaMemcpyAsync; 2: one cudaMemcpyBatchAsync; 3: zero-copy gather kernel (device reads
+// 1: n cudaMemcpyAsync; 3: zero-copy gather kernel (device reads
 // mapped pinned memory, `ctas` CTAs). Returns GB/s of the timed (second) repetition.
 // ---------------------------------------------------------------------------
 namespace {
@@ -346,13 +397,13 @@ extern "C" int hmi_gpu_copy_probe(int device, int n, size_t bytes, int mode, int
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   int status = HMI_OK;
   try {
+    HMI_CHECK(mode == 0 || mode == 1 || mode == 3, HMI_CONFIG_ERROR, "copy probe: mode 0, 1 or 3");
     HMI_CUDA(cudaSetDevice(device));
     HMI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     HMI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h), static_cast<size_t>(n) * bytes, cudaHostAllocMapped));
     std::memset(h, 1, static_cast<size_t>(n) * bytes);
     HMI_CUDA(cudaMalloc(&dbuf, static_cast<size_t>(2 * n) * bytes));
     std::vector<void*> src(n), dst(n), hs(n);
-    std::vector<size_t> sz(n, bytes);
     for (int i = 0; i < n; ++i) {
       hs[i] = h + static_cast<size_t>(i) * bytes;
       dst[i] = dbuf + static_cast<size_t>((i * 7919) % (2 * n)) * bytes;  // scattered slots
@@ -374,12 +425,6 @@ extern "C" int hmi_gpu_copy_probe(int device, int n, size_t bytes, int mode, int
       } else if (mode == 1) {
         for (int i = 0; i < n; ++i)
           HMI_CUDA(cudaMemcpyAsync(dst[i], hs[i], bytes, cudaMemcpyHostToDevice, st));
-      } else if (mode == 2) {
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-        size_t ai = 0, fi = 0;
-        HMI_CUDA(cudaMemcpyBatchAsync(dst.data(), hs.data(), sz.data(), n, &attr, &ai, 1, &fi, st));
       } else {
         zero_copy_gather_kernel<<<ctas, 512, 0, st>>>(reinterpret_cast<const uint4* const*>(d_src),
                                                       reinterpret_cast<uint4* const*>(d_dst), n,

@@ -39,6 +39,22 @@ struct GemmArgs {
   int tail_split;
   uint32_t idesc_tail;
   int tail_r1;                 // tail B boxes through maps.r1 (else maps.r0)
+  // tenant extension (kEpiExt, pair kernel): after the K / 64 shared blocks, 2 x ext_kb more
+  // per unit. Block (e, k) multiplies the ext rows (maps.xa: the bottleneck activations mid,
+  // [rows][64 ext_kb]) of pair tile e -- zero rows (ext_zero_row) in the other CTA's half -- by
+  // tile e's tenant slot (maps.xb: Wu^T [N][64 ext_kb] per slot), so the two requests of a
+  // 256-row pair unit each meet their own up projection. The epilogue adds bias2 of the CTA
+  // tile's slot (b_u).
+  int ext_kb;
+  int ext_zero_row;
+  const float* bias2;
+  long long bias2_stride;      // floats per slot
+  // device-side readiness wait before the first operand load (1-CTA grouped kernel, fine
+  // pipeline): proceed once *ready - ready_seq (wrap-safe) is non-negative; err latches
+  // HMI_SCHEDULING_BUG if the flag never comes
+  const uint32_t* ready;
+  uint32_t ready_seq;
+  int32_t* err;
 };
 
 // Epilogue flags
@@ -55,10 +71,13 @@ constexpr int kStatsStride = 16; // float2 entries per row of a partial-statisti
 constexpr int kEpiFoldLN = 512;  // A is pre-norm y: out = inv*(acc - mean*colsum) + bias
 constexpr int kEpiRes0LN = 1024; // residual res0 is pre-norm: add LN(res0) (r_* args)
 constexpr int kEpiRes1LN = 2048; // residual res1 is pre-norm: add LN(res1)
+constexpr int kEpiExt = 4096;    // pair kernel: tenant extension blocks + bias2 (see GemmArgs)
 
 // All tensor maps of one GEMM (passed as one __grid_constant__ kernel parameter).
 struct GemmMaps {
   CUtensorMap a, b, c, r0, r1;
+  CUtensorMap xa, xb, xb0, xb1;  // kEpiExt: ext rows, tenant B (main / tail widths r0 / r1)
+  CUtensorMap res;               // pair kernel, one 16-bit residual: 64 x 32 boxes of res0
 };
 
 // Everything needed to bind one GEMM to fixed device buffers.
@@ -90,6 +109,16 @@ struct GemmSpec {
   const float* r_gamma = nullptr;
   const float* r_beta = nullptr;
   float inv_n = 0.f;
+  // kEpiExt (pair kernel): ext rows [a_rows + 128][ext_k] 16-bit whose last 128 rows are zero,
+  // tenant B [slots][N][ext_b_ld] at ext_b (slot stride ext_b_stride bytes), tenant bias
+  // ext_bias + slot * ext_bias_stride; the slot of each 128-row tile is tile_slot[tile]
+  const void* ext_a = nullptr;
+  int ext_k = 0;
+  const void* ext_b = nullptr;
+  int ext_b_ld = 0, ext_groups = 0;
+  size_t ext_b_stride = 0;
+  const float* ext_bias = nullptr;
+  long long ext_bias_stride = 0;
 };
 
 struct GemmPlan {
@@ -106,6 +135,7 @@ struct GemmPlan {
 };
 
 GemmPlan make_gemm_plan(const GemmSpec& s);
-void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream);
+void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream, const uint32_t* ready = nullptr,
+                 uint32_t ready_seq = 0, int32_t* err = nullptr);
 
 }  // namespace hmi_b200

@@ -184,13 +184,21 @@ __device__ __forceinline__ void epi_row_stats(const GemmArgs& args, int mt, uint
 // LayerNorm folding: kEpiFoldLN rescales the accumulator of a pre-norm A operand by its
 // row statistics; kEpiRes{0,1}LN normalise a pre-norm residual on the fly; kEpiStats
 // emits this thread's partial row (sum, sumsq) for the next consumer.
-template <int BN, int EPI>
+//
+// kStaged (pair kernel, one 16-bit residual): this warp's k-th chunk of the tile has its
+// residual box (32 rows x 64 columns) TMA-loaded into staging buffer k, completing on
+// rbar[k] (parity bit k of rph); the output is written back over it and stored from there.
+// The unit's column vectors come from shared memory: svec[0, BN) bias (+ the tenant bias),
+// [BN, 2 BN) LN gamma, [2 BN, 3 BN) LN beta of the residual.
+template <int BN, int EPI, bool kStaged = false>
 __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_base, int ncols,
                                               int grp, const GemmArgs& args,
                                               const CUtensorMap* map_c, uint8_t* stg,
                                               uint32_t& sbuf, uint32_t q, int half,
                                               uint32_t lane, float2 a_st, float2 r_st,
-                                              const uint8_t* res_smem) {
+                                              const uint8_t* res_smem, uint64_t* rbar = nullptr,
+                                              uint32_t* rph = nullptr,
+                                              const float* svec = nullptr) {
   constexpr bool kResTma = (EPI & kEpiResTma) != 0;  // residual tiles staged in smem by TMA
   constexpr bool kOutF32 = (EPI & kEpiOutF32) != 0;
   constexpr bool kBf16 = (EPI & kEpiBf16) != 0;  // 16-bit tensors are bf16 (else fp16)
@@ -202,8 +210,11 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
   const int row = row0 + static_cast<int>(lane);
   const bool row_ok = row < args.M;
   const uint32_t t_row = t_acc + ((q * 32) << 16);
+  static_assert(!kStaged || (!kOutF32 && (EPI & kEpiRes1) != 0 && (EPI & kEpiRes2) == 0),
+                "staged residuals: one 16-bit residual, 16-bit output");
+  int kc = 0;  // this warp's chunk index within the tile (kStaged: its staging buffer)
 #pragma unroll 1
-  for (int c = half * kCW; c < ncols; c += 2 * kCW) {
+  for (int c = half * kCW; c < ncols; c += 2 * kCW, ++kc) {
     float v[kCW];
 #pragma unroll
     for (int j = 0; j < kCW / 32; ++j) {
@@ -224,12 +235,65 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
         v[i + 3] = a_st.y * (v[i + 3] - a_st.x * c4.w);
       }
     }
+    if constexpr (kStaged) {
 #pragma unroll
-    for (int i = 0; i < kCW; i += 4) {
-      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
-      v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+      for (int i = 0; i < kCW; i += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(svec + c + i);
+        v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kCW; i += 4) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c + i));
+        v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+      }
     }
-    if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
+    if constexpr (!kStaged && (EPI & kEpiExt) != 0) {  // the tile's tenant bias (b_u of its slot)
+      const float* b2 = args.bias2 + grp * args.bias2_stride + col_base + c;
+#pragma unroll
+      for (int i = 0; i < kCW; i += 4) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(b2 + i));
+        v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+      }
+    }
+    if constexpr (kStaged) {
+      mbar_wait(&rbar[kc], (*rph >> kc) & 1u);
+      *rph ^= 1u << kc;
+      const uint8_t* rowp = stg + kc * 4096 + lane * 128;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // 16-byte chunks, consumed as they are read
+        const uint4 u = *reinterpret_cast<const uint4*>(rowp + ((k ^ (lane & 7)) << 4));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 t;
+          if constexpr (kBf16) {
+            t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+          } else {
+            t = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+          }
+          f[2 * e] = t.x;
+          f[2 * e + 1] = t.y;
+        }
+        if constexpr ((EPI & kEpiRes0LN) != 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 g = *reinterpret_cast<const float4*>(svec + BN + c + 8 * k + 4 * h);
+            const float4 b = *reinterpret_cast<const float4*>(svec + 2 * BN + c + 8 * k + 4 * h);
+            float* vv = v + 8 * k + 4 * h;
+            const float* ff = f + 4 * h;
+            vv[0] += (ff[0] - r_st.x) * r_st.y * g.x + b.x;
+            vv[1] += (ff[1] - r_st.x) * r_st.y * g.y + b.y;
+            vv[2] += (ff[2] - r_st.x) * r_st.y * g.z + b.z;
+            vv[3] += (ff[3] - r_st.x) * r_st.y * g.w + b.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[8 * k + e] += f[e];
+        }
+      }
+    } else if constexpr ((EPI & (kEpiRes1 | kEpiRes2)) != 0) {
       const int col = col_base + c;
       if constexpr (kResTma) {
         const int row_local = static_cast<int>(q) * 32 + static_cast<int>(lane);
@@ -284,12 +348,16 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
 #pragma unroll
       for (int i = 0; i < 32; ++i) packed[i] = pack_16x2<kBf16>(v[2 * i], v[2 * i + 1]);
     }
-    // staging buffer reuse: this warp's previous TMA store must have read it
-    // double-buffered staging: the store issued from this buffer two chunks ago is read
-    if (lane == 0) tma_store_wait_read<1>();
-    __syncwarp();
-    uint8_t* buf = stg + sbuf * 4096;
-    sbuf ^= 1;
+    uint8_t* buf;
+    if constexpr (kStaged) {
+      buf = stg + kc * 4096;  // over this chunk's residual (each thread rewrites its own row)
+    } else {
+      // double-buffered staging: the store issued from this buffer two chunks ago is read
+      if (lane == 0) tma_store_wait_read<1>();
+      __syncwarp();
+      buf = stg + sbuf * 4096;
+      sbuf ^= 1;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int phys = i ^ (lane & 7);  // SWIZZLE_128B: 16 B chunk ^= row % 8
@@ -303,6 +371,25 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
       tma_store_commit();
     }
   }
+}
+
+// Fine pipeline: block until the copy stream has published this layer's adapter slots
+// (*ready reaches ready_seq, written by cuStreamWriteValue32 after the layer's H2D copies), so
+// a stream-level event wait does not cut the programmatic-launch chain. Whole CTA.
+__device__ __forceinline__ void wait_ready(const GemmArgs& args) {
+  if (args.ready == nullptr) return;
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_gpu(args.ready) - args.ready_seq > 0x7fffffffu) {  // wrap-safe <
+      if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) {  // 20 s: never, unless broken
+        atomicExch(args.err, HMI_SCHEDULING_BUG);
+        break;
+      }
+      __nanosleep(256);
+    }
+    fence_proxy_async_global();  // the slots are read through TMA (async proxy)
+  }
+  __syncthreads();
 }
 
 template <int BN, bool RT = false>
@@ -386,6 +473,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // inputs of the previous kernel are complete and visible from here on
+  wait_ready(args);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -525,16 +613,24 @@ __device__ __forceinline__ int pair_units_total(const GemmArgs& a, int num_units
   return a.tail_split > 1 ? a.n_main + (num_units - a.n_main) * a.tail_split : num_units;
 }
 
-template <int BN>
+// Pair-kernel epilogues with one 16-bit residual and a 16-bit output stage that residual by
+// TMA through the epilogue buffers and the unit's column vectors in shared memory.
+constexpr bool pair_staged(int epi) {
+  return (epi & kEpiRes1) != 0 && (epi & (kEpiRes2 | kEpiOutF32)) == 0;
+}
+
+template <int BN, bool kVec = false>
 struct Gemm2Smem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;          // this CTA's 128 rows of A
   static constexpr int kBBytes = (BN / 2) * kBlockK * 2;         // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kEpiBytes = 8 * 2 * 4096;
-  static constexpr int kBudget = 227 * 1024 - 1024 - 256;
-  static constexpr int kStagesRaw = (kBudget - kEpiBytes) / kStageBytes;
+  static constexpr int kVecBytes = kVec ? 2 * 3 * BN * 4 : 0;    // two units' column vectors
+  static constexpr int kBarBytes = 512;  // ring, accumulator and staged-residual barriers
+  static constexpr int kBudget = 227 * 1024 - 1024 - kBarBytes;
+  static constexpr int kStagesRaw = (kBudget - kEpiBytes - kVecBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kTotal = 1024 + kStages * kStageBytes + kEpiBytes + 256;
+  static constexpr int kTotal = 1024 + kStages * kStageBytes + kEpiBytes + kVecBytes + kBarBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
 };
 
@@ -544,7 +640,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const CUtensorMap& map_a = maps.a;
   const CUtensorMap& map_b = maps.b;
   const CUtensorMap& map_c = maps.c;
-  using L = Gemm2Smem<BN>;
+  constexpr bool kStaged = pair_staged(EPI);
+  using L = Gemm2Smem<BN, kStaged>;
   constexpr int kStages = L::kStages;
   static_assert(kStages >= 3, "smem budget too small");
   static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "BN");
@@ -555,12 +652,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * L::kABytes;
   uint8_t* sEpi = smem + kStages * L::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes);
+  float* sVec = reinterpret_cast<float*>(sEpi + L::kEpiBytes);  // kStaged: [2][3][BN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes + L::kVecBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tfull = bars + 2 * kStages;
   uint64_t* tempty = bars + 2 * kStages + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* rbars = bars + 2 * kStages + 4;  // [8 epilogue warps][2] staged residual boxes
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 20);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -570,7 +669,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int total = pair_units_total(args, num_units);
   const int cluster = blockIdx.x >> 1;
   const int n_clusters = gridDim.x >> 1;
+  constexpr bool kExt = (EPI & kEpiExt) != 0;
   const int num_kb = args.K / kBlockK;
+  const int all_kb = num_kb + (kExt ? 2 * args.ext_kb : 0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -584,6 +685,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 16);  // 8 epilogue warps x 2 CTAs (leader's copy is the one used)
     }
+    for (int s = 0; s < 16; ++s) mbar_init(&rbars[s], 1);
+    if constexpr (kStaged) tma_prefetch_desc(&maps.res);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_2cta<L::kTmemCols>(tmem_slot);
@@ -606,14 +709,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         // wave-tail sub-tiles load B through the narrower-box maps r0 / r1
         const CUtensorMap* mb = !pu.tail ? &map_b : args.tail_r1 ? &maps.r1 : &maps.r0;
         const uint32_t bytes = 2 * (L::kABytes + (pu.width / 2) * kBlockK * 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < all_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
           const uint32_t leader_full = mapa_shared(smem_u32(&full[stage]), 0);
-          tma_load_2d_2sm(sA + stage * L::kABytes, &map_a, leader_full, kb * kBlockK,
-                          mt * kBlockM, pol_a);
-          tma_load_3d_2sm(sB + stage * L::kBBytes, mb, leader_full, kb * kBlockK,
-                          pu.col0 + static_cast<int>(rank) * (pu.width / 2), 0, pol_b);
+          const int col = pu.col0 + static_cast<int>(rank) * (pu.width / 2);
+          if (!kExt || kb < num_kb) {
+            tma_load_2d_2sm(sA + stage * L::kABytes, &map_a, leader_full, kb * kBlockK,
+                            mt * kBlockM, pol_a);
+            tma_load_3d_2sm(sB + stage * L::kBBytes, mb, leader_full, kb * kBlockK, col, 0, pol_b);
+          } else {
+            // tenant block: tile e's ext rows against tile e's slot; the other CTA's A half
+            // is the zero rows, so rows of the other request gain nothing
+            const int x = kb - num_kb;
+            const int e = x / args.ext_kb, kx = (x - e * args.ext_kb) * kBlockK;
+            const int mte = 2 * pu.mp + e;
+            const int slot = mte < args.num_m_tiles ? __ldg(&args.tile_slot[mte]) : 0;
+            const CUtensorMap* xb = !pu.tail ? &maps.xb : args.tail_r1 ? &maps.xb1 : &maps.xb0;
+            tma_load_2d_2sm(sA + stage * L::kABytes, &maps.xa, leader_full, kx,
+                            e == static_cast<int>(rank) ? mt * kBlockM : args.ext_zero_row, pol_a);
+            tma_load_3d_2sm(sB + stage * L::kBBytes, xb, leader_full, kx, col, slot, pol_b);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -627,7 +743,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < all_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t a_desc = sdesc_k_sw128(smem_u32(sA + stage * L::kABytes));
@@ -649,20 +765,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const uint32_t q = warp & 3;
     const int half = static_cast<int>(warp - 2) >> 2;
     uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
-    uint32_t sbuf = 0;
+    uint64_t* rbar = rbars + (warp - 2) * 2;
+    uint32_t sbuf = 0, rph = 0;
     uint32_t acc = 0, acc_phase = 0;
-    for (int v = cluster; v < total; v += n_clusters) {
+    // kStaged: residual boxes of unit v's chunks for this warp (32 rows x 64 columns each)
+    // into its two staging buffers, once the stores issued from them have read them
+    auto stage_res = [&](int v) {
+      if (v >= total) return;
+      const PairUnit pn = pair_unit<BN>(args, v);
+      const int row0 = (2 * pn.mp + static_cast<int>(rank)) * kBlockM + static_cast<int>(q) * 32;
+      tma_store_wait_read<0>();
+      int k = 0;
+      for (int c = half * 64; c < pn.width; c += 128, ++k) {
+        mbar_arrive_expect_tx(&rbar[k], 4096);
+        tma_load_2d(stg + k * 4096, &maps.res, &rbar[k], pn.col0 + c, row0);
+      }
+    };
+    if constexpr (kStaged) {
+      if (lane == 0) stage_res(cluster);
+    }
+    uint32_t iter = 0;
+    for (int v = cluster; v < total; v += n_clusters, ++iter) {
       const PairUnit pu = pair_unit<BN>(args, v);
       const int mt = 2 * pu.mp + static_cast<int>(rank);
+      const int grp = kExt && mt < args.num_m_tiles ? __ldg(&args.tile_slot[mt]) : 0;
+      float* sv = sVec + (iter & 1) * 3 * BN;
+      if constexpr (kStaged) {
+        // this unit's column vectors, one column per epilogue thread; the buffer written here
+        // was last read two units ago, before every warp passed the previous unit's barrier
+        const int t = static_cast<int>(warp - 2) * 32 + static_cast<int>(lane);
+        if (t < pu.width) {
+          const int col = pu.col0 + t;
+          float b = __ldg(args.bias + col);
+          if constexpr (kExt) b += __ldg(args.bias2 + grp * args.bias2_stride + col);
+          sv[t] = b;
+          if constexpr ((EPI & kEpiRes0LN) != 0) {
+            sv[BN + t] = __ldg(args.r_gamma + col);
+            sv[2 * BN + t] = __ldg(args.r_beta + col);
+          }
+        }
+        named_bar_sync(1, 256);
+      }
       float2 a_st, r_st;
       epi_row_stats<EPI>(args, mt, q, lane, a_st, r_st);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, pu.col0, pu.width, 0, args, &map_c, stg,
-                             sbuf, q, half, lane, a_st, r_st, nullptr);
+      epilogue_tile<BN, EPI, kStaged>(tmem_base + acc * BN, mt, pu.col0, pu.width, grp, args,
+                                      &map_c, stg, sbuf, q, half, lane, a_st, r_st, nullptr, rbar,
+                                      &rph, sv);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+      if constexpr (kStaged) {
+        if (lane == 0) stage_res(v + n_clusters);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }

@@ -306,9 +306,12 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// Arrive on a barrier of a CTA of this cluster (default .release.cta semantics). It orders
+// this thread's tcgen05.ld (behind tcgen05.fence::before_thread_sync) before the peer MMA's
+// reuse of the accumulator; a .cluster-scope release would also drain the thread's pending
+// global stores (MEMBAR) on every accumulator hand-back.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 template <uint32_t kCols>

@@ -8,7 +8,7 @@ from paper_2504_17449_b200 import _native  # noqa: E402
 
 L = _native.lib()
 for n, b in ((600, 200704), (100, 1204224)):
-    for mode, name in ((0, "one copy"), (1, "n memcpyAsync"), (2, "memcpyBatchAsync"), (3, "zero-copy 16"),
+    for mode, name in ((0, "one copy"), (1, "n memcpyAsync"), (3, "zero-copy 16"),
                        (4, "zero-copy 32"), (5, "zero-copy 64")):
         g = ctypes.c_double(0)
         m = min(mode, 3)
