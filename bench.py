@@ -456,6 +456,7 @@ def bench_ours(args, wl):
         copied = (p1["bytes_copied"] - p0["bytes_copied"]) / K
         swap = {"bytes_copied_per_step": copied,
                 "loads_per_step": (p1["loads"] - p0["loads"]) / K,
+                "transfers_per_step": (c1["adapter_copies"] - c0["adapter_copies"]) / K,
                 "io_busy_ms_per_step": io_busy / K, "compute_busy_ms_per_step": comp_busy / K,
                 "compute_idle_ms_per_step": (span - comp_busy) / K,
                 "io_hidden_frac": _overlap(io, comp) / io_busy if io_busy > 0 else 1.0,

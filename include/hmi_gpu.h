@@ -260,7 +260,8 @@ int hmi_generate_adapter(const hmi_model_config* cfg, uint32_t bottleneck, uint6
 /* generate_output_head (weights.cpp:105-118): w [d x labels], b [labels].    */
 int hmi_generate_head(uint32_t hidden_size, uint32_t labels, uint64_t seed, float* w, float* b);
 
-/* Engine counters: out[0] kernel launches, [1] batches, [2] adapter copies,
+/* Engine counters: out[0] kernel launches, [1] batches, [2] host -> HBM adapter transfers
+ * (one per run of consecutive slot images of a task),
  * [3] host NUMA node the pinned adapter store is bound to (UINT64_MAX: unknown). */
 int hmi_gpu_counters(hmi_gpu_ctx* ctx, uint64_t* out);
 /* Pinned-host (NUMA-local, as the adapter store) -> HBM copy rate on the copy stream:

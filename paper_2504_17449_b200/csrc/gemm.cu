@@ -79,13 +79,13 @@ KernelFn pick_kernel(int bn, int epi, bool c2, int* smem_bytes) {
   if (c2) {
     switch (bn) {
       case 128:
-        *smem_bytes = pair_staged(epi) ? Gemm2Smem<128, true>::kTotal : Gemm2Smem<128>::kTotal;
+        *smem_bytes = pair_svec(epi) ? Gemm2Smem<128, true>::kTotal : Gemm2Smem<128>::kTotal;
         return pick_epi<128, true>(epi);
       case 192:
-        *smem_bytes = pair_staged(epi) ? Gemm2Smem<192, true>::kTotal : Gemm2Smem<192>::kTotal;
+        *smem_bytes = pair_svec(epi) ? Gemm2Smem<192, true>::kTotal : Gemm2Smem<192>::kTotal;
         return pick_epi<192, true>(epi);
       case 256:
-        *smem_bytes = pair_staged(epi) ? Gemm2Smem<256, true>::kTotal : Gemm2Smem<256>::kTotal;
+        *smem_bytes = pair_svec(epi) ? Gemm2Smem<256, true>::kTotal : Gemm2Smem<256>::kTotal;
         return pick_epi<256, true>(epi);
       default: return nullptr;
     }

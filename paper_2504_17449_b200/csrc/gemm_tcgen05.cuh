@@ -160,6 +160,44 @@ __device__ __forceinline__ void add_res_vals(float* v, const float* r, float2 st
   }
 }
 
+// Partial-statistics row of the one LN input an epilogue folds (A's for kEpiFoldLN, the
+// residual's for kEpiRes{0,1}LN), loaded a unit ahead so its latency is off the epilogue's path.
+template <int EPI>
+struct StatsPrefetch {
+  static constexpr bool kA = (EPI & kEpiFoldLN) != 0;
+  static constexpr bool kR = (EPI & (kEpiRes0LN | kEpiRes1LN)) != 0;
+  static_assert(!(kA && kR), "one folded LayerNorm input per epilogue");
+  float4 q[kStatsStride / 2];
+  __device__ __forceinline__ void load(const GemmArgs& args, int row) {
+    if constexpr (kA || kR) {
+      const float2* part = (kA ? args.a_stats : args.r_stats) + static_cast<long long>(row) * kStatsStride;
+      const int n = kA ? args.a_stats_n : args.r_stats_n;
+#pragma unroll
+      for (int i = 0; i < kStatsStride / 2; ++i) {
+        q[i] = row < args.M && 2 * i < n ? __ldg(reinterpret_cast<const float4*>(part) + i)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  // (mean, 1 / sqrt(var + eps)) into a_st or r_st
+  __device__ __forceinline__ void finish(const GemmArgs& args, float2& a_st, float2& r_st) const {
+    a_st = make_float2(0.f, 1.f);
+    r_st = make_float2(0.f, 1.f);
+    if constexpr (kA || kR) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < kStatsStride / 2; ++i) {  // entries beyond n were loaded as zero
+        s1 += q[i].x + q[i].z;
+        s2 += q[i].y + q[i].w;
+      }
+      const float mean = s1 * args.inv_n;
+      const float var = fmaxf(s2 * args.inv_n - mean * mean, 0.0f);
+      const float2 st = make_float2(mean, 1.0f / sqrtf(var + 1e-5f));
+      if constexpr (kA) a_st = st; else r_st = st;
+    }
+  }
+};
+
 // Row statistics the LN-folding epilogue modes need (fetched before the accumulator wait)
 template <int EPI>
 __device__ __forceinline__ void epi_row_stats(const GemmArgs& args, int mt, uint32_t q,
@@ -188,9 +226,9 @@ __device__ __forceinline__ void epi_row_stats(const GemmArgs& args, int mt, uint
 // kStaged (pair kernel, one 16-bit residual): this warp's k-th chunk of the tile has its
 // residual box (32 rows x 64 columns) TMA-loaded into staging buffer k, completing on
 // rbar[k] (parity bit k of rph); the output is written back over it and stored from there.
-// The unit's column vectors come from shared memory: svec[0, BN) bias (+ the tenant bias),
-// [BN, 2 BN) LN gamma, [2 BN, 3 BN) LN beta of the residual.
-template <int BN, int EPI, bool kStaged = false>
+// kSVec: the unit's column vectors come from shared memory: svec[0, BN) bias (+ the tenant
+// bias), [BN, 2 BN) LN gamma and [2 BN, 3 BN) LN beta of the residual, or colsum (kEpiFoldLN).
+template <int BN, int EPI, bool kStaged = false, bool kSVec = false, int kBufs = 2>
 __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_base, int ncols,
                                               int grp, const GemmArgs& args,
                                               const CUtensorMap* map_c, uint8_t* stg,
@@ -216,26 +254,29 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
 #pragma unroll 1
   for (int c = half * kCW; c < ncols; c += 2 * kCW, ++kc) {
     float v[kCW];
+    {
+      uint32_t r[kCW];  // both TMEM loads in flight, one wait
 #pragma unroll
-    for (int j = 0; j < kCW / 32; ++j) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(t_row + c + 32 * j, r);
+      for (int j = 0; j < kCW / 32; ++j) {
+        tmem_ld_32x32b_x32(t_row + c + 32 * j, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * j));
+      }
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(r[i]);
+      for (int i = 0; i < kCW; ++i) v[i] = __uint_as_float(r[i]);
     }
     if constexpr ((EPI & kEpiFoldLN) != 0) {
       const float* cs = args.colsum + col_base + c;
 #pragma unroll
       for (int i = 0; i < kCW; i += 4) {
-        const float4 c4 = __ldg(reinterpret_cast<const float4*>(cs + i));
+        const float4 c4 = kSVec ? *reinterpret_cast<const float4*>(svec + BN + c + i)
+                                : __ldg(reinterpret_cast<const float4*>(cs + i));
         v[i] = a_st.y * (v[i] - a_st.x * c4.x);
         v[i + 1] = a_st.y * (v[i + 1] - a_st.x * c4.y);
         v[i + 2] = a_st.y * (v[i + 2] - a_st.x * c4.z);
         v[i + 3] = a_st.y * (v[i + 3] - a_st.x * c4.w);
       }
     }
-    if constexpr (kStaged) {
+    if constexpr (kSVec) {
 #pragma unroll
       for (int i = 0; i < kCW; i += 4) {
         const float4 b4 = *reinterpret_cast<const float4*>(svec + c + i);
@@ -248,7 +289,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
         v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
       }
     }
-    if constexpr (!kStaged && (EPI & kEpiExt) != 0) {  // the tile's tenant bias (b_u of its slot)
+    if constexpr (!kSVec && (EPI & kEpiExt) != 0) {  // the tile's tenant bias (b_u of its slot)
       const float* b2 = args.bias2 + grp * args.bias2_stride + col_base + c;
 #pragma unroll
       for (int i = 0; i < kCW; i += 4) {
@@ -353,10 +394,10 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
       buf = stg + kc * 4096;  // over this chunk's residual (each thread rewrites its own row)
     } else {
       // double-buffered staging: the store issued from this buffer two chunks ago is read
-      if (lane == 0) tma_store_wait_read<1>();
+      if (lane == 0) tma_store_wait_read<kBufs - 1>();
       __syncwarp();
       buf = stg + sbuf * 4096;
-      sbuf ^= 1;
+      sbuf = (sbuf + 1) % kBufs;
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -614,17 +655,19 @@ __device__ __forceinline__ int pair_units_total(const GemmArgs& a, int num_units
 }
 
 // Pair-kernel epilogues with one 16-bit residual and a 16-bit output stage that residual by
-// TMA through the epilogue buffers and the unit's column vectors in shared memory.
+// TMA through the epilogue buffers; they and the LN-folding epilogues read the unit's column
+// vectors from shared memory.
 constexpr bool pair_staged(int epi) {
   return (epi & kEpiRes1) != 0 && (epi & (kEpiRes2 | kEpiOutF32)) == 0;
 }
+constexpr bool pair_svec(int epi) { return pair_staged(epi); }
 
 template <int BN, bool kVec = false>
 struct Gemm2Smem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;          // this CTA's 128 rows of A
   static constexpr int kBBytes = (BN / 2) * kBlockK * 2;         // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = 8 * 2 * 4096;
+  static constexpr int kEpiBytes = 8 * 2 * 4096;  // 8 epilogue warps x 2 staging buffers
   static constexpr int kVecBytes = kVec ? 2 * 3 * BN * 4 : 0;    // two units' column vectors
   static constexpr int kBarBytes = 512;  // ring, accumulator and staged-residual barriers
   static constexpr int kBudget = 227 * 1024 - 1024 - kBarBytes;
@@ -641,7 +684,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const CUtensorMap& map_b = maps.b;
   const CUtensorMap& map_c = maps.c;
   constexpr bool kStaged = pair_staged(EPI);
-  using L = Gemm2Smem<BN, kStaged>;
+  constexpr bool kSVec = pair_svec(EPI);
+  using L = Gemm2Smem<BN, kSVec>;
   constexpr int kStages = L::kStages;
   static_assert(kStages >= 3, "smem budget too small");
   static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "BN");
@@ -652,7 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * L::kABytes;
   uint8_t* sEpi = smem + kStages * L::kStageBytes;
-  float* sVec = reinterpret_cast<float*>(sEpi + L::kEpiBytes);  // kStaged: [2][3][BN]
+  float* sVec = reinterpret_cast<float*>(sEpi + L::kEpiBytes);  // kSVec: [2][3][BN]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + L::kEpiBytes + L::kVecBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
@@ -770,6 +814,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t acc = 0, acc_phase = 0;
     // kStaged: residual boxes of unit v's chunks for this warp (32 rows x 64 columns each)
     // into its two staging buffers, once the stores issued from them have read them
+    StatsPrefetch<EPI> spf;
+    auto fetch_stats = [&](int v) {
+      if (v >= total) return;
+      const PairUnit pn = pair_unit<BN>(args, v);
+      spf.load(args, (2 * pn.mp + static_cast<int>(rank)) * kBlockM + static_cast<int>(q) * 32 +
+                         static_cast<int>(lane));
+    };
+    fetch_stats(cluster);
     auto stage_res = [&](int v) {
       if (v >= total) return;
       const PairUnit pn = pair_unit<BN>(args, v);
@@ -790,7 +842,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int mt = 2 * pu.mp + static_cast<int>(rank);
       const int grp = kExt && mt < args.num_m_tiles ? __ldg(&args.tile_slot[mt]) : 0;
       float* sv = sVec + (iter & 1) * 3 * BN;
-      if constexpr (kStaged) {
+      if constexpr (kSVec) {
         // this unit's column vectors, one column per epilogue thread; the buffer written here
         // was last read two units ago, before every warp passed the previous unit's barrier
         const int t = static_cast<int>(warp - 2) * 32 + static_cast<int>(lane);
@@ -803,14 +855,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             sv[BN + t] = __ldg(args.r_gamma + col);
             sv[2 * BN + t] = __ldg(args.r_beta + col);
           }
+          if constexpr ((EPI & kEpiFoldLN) != 0) sv[BN + t] = __ldg(args.colsum + col);
         }
         named_bar_sync(1, 256);
       }
       float2 a_st, r_st;
-      epi_row_stats<EPI>(args, mt, q, lane, a_st, r_st);
+      spf.finish(args, a_st, r_st);
+      fetch_stats(v + n_clusters);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, EPI, kStaged>(tmem_base + acc * BN, mt, pu.col0, pu.width, grp, args,
+      epilogue_tile<BN, EPI, kStaged, kSVec>(tmem_base + acc * BN, mt, pu.col0, pu.width, grp, args,
                                       &map_c, stg, sbuf, q, half, lane, a_st, r_st, nullptr, rbar,
                                       &rph, sv);
       tc_fence_before();

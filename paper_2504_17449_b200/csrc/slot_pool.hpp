@@ -14,6 +14,11 @@
 //     returns nullopt when only pinned tasks block (:93-136).
 // In addition every resident (task, layer) owns one physical slot of the HBM
 // arena; slots are recycled from evicted tasks. This is the part the GPU adds.
+// Placement prefers blocks: the arena's first (slots / block_len) * block_len slots form
+// blocks of block_len (= the model's layer count); a task claims a free block with its
+// first resident layer and its layer l then goes to slot block * block_len + l, so a
+// whole-task miss is one contiguous host -> HBM copy. Any free slot is used when no
+// block is free (the byte budget, not the placement, decides residency).
 #pragma once
 
 #include <cstdint>
@@ -47,7 +52,7 @@ struct PoolRecord {
 
 class SlotPool {
  public:
-  SlotPool(uint64_t capacity_bytes, uint32_t physical_slots);
+  SlotPool(uint64_t capacity_bytes, uint32_t physical_slots, uint32_t block_len = 1);
 
   // AdapterStore registration mirror: a task's layer count and per-layer bytes.
   void set_task(uint32_t task, uint32_t layers, uint64_t layer_bytes);
@@ -107,11 +112,21 @@ class SlotPool {
   void stash_partial(std::vector<PoolRecord>& done, PoolRecord& failing);
   bool make_room(uint64_t needed, const std::set<uint32_t>& protect, PoolRecord& rec);
   void release(uint32_t task, Residency& r, std::vector<PoolFree>* freed);
-  int32_t take_slot();
+  int32_t take_slot(uint32_t task, uint32_t layer);
+  void free_slot(int32_t slot);
+  void drop_claim(uint32_t task);
 
   uint64_t capacity_;
   size_t n_slots_;
-  std::vector<int32_t> free_slots_;
+  uint32_t block_len_;
+  int32_t n_blocks_;                    // full blocks; slots >= n_blocks_ * block_len_ are loose
+  std::vector<uint8_t> slot_free_;
+  std::vector<uint32_t> block_free_;    // free slots per block
+  std::vector<int64_t> block_owner_;    // claiming task, or -1
+  std::map<uint32_t, int32_t> claim_;   // task -> claimed block
+  std::set<int32_t> free_blocks_;       // fully free, unclaimed blocks
+  std::set<int32_t> loose_free_;        // free slots usable when no block is free
+  size_t n_free_ = 0;
   std::map<uint32_t, TaskInfo> tasks_;
   std::map<uint32_t, Residency> resident_;
   // (last_used, task) of every resident record: the reference scans all residents for the
