@@ -290,6 +290,236 @@ __global__ void __launch_bounds__(kTcThreads, 1) attention_tc_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Padded lengths 256..512 (2..4 key blocks of 128) on tcgen05. One work item = (request,
+// head, 128-query block); the item's Q, every K and V block sit in shared memory. Two passes
+// over the key blocks share two TMEM score buffers: pass 1 takes the row maximum over the
+// keys the reference reads (j < limit, model.cpp:48-56), pass 2 recomputes each score block,
+// writes P = exp2(s - max) as 16-bit into one of two smem P buffers and accumulates
+// O += P V in TMEM, then O / sum is stored. Same arithmetic as the padded-128 kernel above.
+//
+//   warp 0 (lane 0): TMA   Q, K[0..nb), V[0..nb) of an item (one stage)
+//   warp 1 (lane 0): MMA   S(t) for t = 0 .. 2 nb - 1 into TMEM buffer t % 2, PV(j) behind
+//   warps 2..5     : one query row per thread: max pass, exp / sum / P pass, epilogue
+constexpr int kLThreads = 192;
+constexpr int kLMaxBlocks = 4;
+constexpr int kLSmem = 1024 + kT /*Q*/ + 2 * kLMaxBlocks * kT /*K, V*/ + 2 * 2 * kT /*P[2]*/ +
+                       kT /*O staging*/ + 256;
+
+template <bool kBf16>
+__global__ void __launch_bounds__(kLThreads, 1) attention_long_kernel(
+    const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_ctx,
+    const int* __restrict__ lens, int n_items, int heads, int nb, int d, int causal,
+    float scale_log2) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* base = raw + ((1024 - (smem_u32(raw) & 1023)) & 1023);
+  uint8_t* sQ = base;
+  uint8_t* sK = sQ + kT;                            // [kLMaxBlocks] 128 keys x 64
+  uint8_t* sV = sK + kLMaxBlocks * kT;              // [kLMaxBlocks]
+  uint8_t* sP = sV + kLMaxBlocks * kT;              // [2] 128 rows x 128 keys (two 64-key tiles)
+  uint8_t* sO = sP + 4 * kT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sO + kT);
+  uint64_t* ld_full = bar;        // item operands landed (TMA tx)
+  uint64_t* ld_empty = bar + 1;   // item operands consumed (MMA commit)
+  uint64_t* s_full = bar + 2;     // [2] score buffer written (MMA commit)
+  uint64_t* s_empty = bar + 4;    // [2] score buffer read (4 warps)
+  uint64_t* p_full = bar + 6;     // [2] P buffer written (4 warps)
+  uint64_t* p_empty = bar + 8;    // [2] P buffer read by the PV MMA (commit)
+  uint64_t* o_full = bar + 10;    // O complete (commit)
+  uint64_t* o_empty = bar + 11;   // O read (4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_qkv);
+    tma_prefetch_desc(&map_ctx);
+    mbar_init(ld_full, 1);
+    mbar_init(ld_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 4);
+      mbar_init(&p_full[b], 4);
+      mbar_init(&p_empty[b], 1);
+    }
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+  // TMEM columns: S buffers 0..127 and 128..255, O 256..319
+  const int S = nb * 128;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t ph = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ph ^= 1) {
+        const int qb = item % nb, rh = item / nb, h = rh % heads, req = rh / heads;
+        mbar_wait(ld_empty, ph ^ 1);
+        mbar_arrive_expect_tx(ld_full, (1 + 2 * nb) * kT);
+        const int row0 = req * S;
+        tma_load_2d(sQ, &map_qkv, ld_full, h * 64, row0 + qb * 128);
+        for (int j = 0; j < nb; ++j) {
+          tma_load_2d(sK + j * kT, &map_qkv, ld_full, d + h * 64, row0 + j * 128);
+          tma_load_2d(sV + j * kT, &map_qkv, ld_full, 2 * d + h * 64, row0 + j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = idesc_f16(128, 128, kBf16 ? 1u : 0u);
+      const uint32_t id_o = idesc_f16(128, 64, kBf16 ? 1u : 0u) | (1u << 16);  // B MN-major
+      uint32_t ld_ph = 0, o_ph = 0, s_use[2] = {0, 0}, p_use[2] = {0, 0};
+      const uint64_t qd = sdesc_k_sw128(smem_u32(sQ));
+      auto pv = [&](int j) {
+        const int b = j & 1;
+        mbar_wait(&p_full[b], p_use[b] & 1);
+        ++p_use[b];
+        tc_fence_after();
+        const uint32_t p0 = smem_u32(sP + b * 2 * kT), vb = smem_u32(sV + j * kT);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // 16 keys per step
+          const uint64_t pd = sdesc_k_sw128(p0 + (kk >> 2) * kT) + 2 * (kk & 3);
+          const uint64_t vd = sdesc_mn_sw128(vb + kk * 2048);
+          umma_f16(tmem + 256, pd, vd, id_o, (j | kk) != 0);
+        }
+        umma_commit(&p_empty[b]);
+      };
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        mbar_wait(ld_full, ld_ph);
+        ld_ph ^= 1;
+        tc_fence_after();
+        for (int t = 0; t < 2 * nb; ++t) {
+          const int b = t & 1;
+          mbar_wait(&s_empty[b], (s_use[b] & 1) ^ 1);
+          ++s_use[b];
+          tc_fence_after();
+          const uint64_t kd = sdesc_k_sw128(smem_u32(sK + (t % nb) * kT));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) umma_f16(tmem + b * 128, qd + 2 * kk, kd + 2 * kk, id_s, kk);
+          umma_commit(&s_full[b]);
+          if (t == nb) {  // first PV of the item: the previous item's O has been read
+            mbar_wait(o_empty, o_ph ^ 1);
+            o_ph ^= 1;
+          }
+          if (t > nb) pv(t - nb - 1);
+        }
+        pv(nb - 1);
+        umma_commit(o_full);
+        umma_commit(ld_empty);  // Q, K, V of this item consumed
+      }
+    }
+  } else {
+    const uint32_t q = warp & 3;                    // TMEM lane quarter
+    const int r = static_cast<int>(q * 32 + lane);  // query row of the block
+    const uint32_t lane_off = (q * 32) << 16;
+    uint32_t s_use[2] = {0, 0}, p_use[2] = {0, 0}, o_ph = 0;
+    const bool storer = warp == 2 && lane == 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int qb = item % nb, rh = item / nb, h = rh % heads, req = rh / heads;
+      const int valid = __ldg(&lens[req]);
+      const int lim = causal ? qb * 128 + r + 1 : valid;  // keys j < lim (model.cpp:48-51)
+      auto read_s = [&](int t, float (&sv)[128]) {
+        const int b = t & 1;
+        mbar_wait(&s_full[b], s_use[b] & 1);
+        ++s_use[b];
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(tmem + lane_off + b * 128 + 32 * c, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[32 * c + i] = __uint_as_float(u[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[b]);
+      };
+      float mx = -INFINITY;
+      for (int t = 0; t < nb; ++t) {  // pass 1: row maximum of the scaled scores
+        float sv[128];
+        read_s(t, sv);
+        const int kl = lim - t * 128;  // keys of this block below the limit
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 128; ++c) m4[c & 3] = fmaxf(m4[c & 3], c < kl ? sv[c] * scale_log2 : -INFINITY);
+        mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+      }
+      const float mb = mx == -INFINITY ? 0.f : mx;
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < nb; ++j) {  // pass 2: P blocks and their sum
+        float sv[128];
+        read_s(nb + j, sv);
+        const int kl = lim - j * 128;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          sv[c] = c < kl ? ex2_ftz(sv[c] * scale_log2 - mb) : 0.f;
+          l4[c & 3] += sv[c];
+        }
+        const int b = j & 1;
+        mbar_wait(&p_empty[b], (p_use[b] & 1) ^ 1);  // the PV two blocks back read this buffer
+        ++p_use[b];
+        uint8_t* P = sP + b * 2 * kT;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          uint4 v;
+          v.x = pk2<kBf16>(sv[8 * c + 0], sv[8 * c + 1]);
+          v.y = pk2<kBf16>(sv[8 * c + 2], sv[8 * c + 3]);
+          v.z = pk2<kBf16>(sv[8 * c + 4], sv[8 * c + 5]);
+          v.w = pk2<kBf16>(sv[8 * c + 6], sv[8 * c + 7]);
+          *reinterpret_cast<uint4*>(P + (c >> 3) * kT + sw(r, c & 7)) = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[b]);
+      }
+      const float l = (l4[0] + l4[1]) + (l4[2] + l4[3]);
+      // epilogue: O / l -> 16-bit -> staging -> TMA store
+      mbar_wait(o_full, o_ph);
+      o_ph ^= 1;
+      tc_fence_after();
+      uint32_t o[64];
+      tmem_ld_32x32b_x32(tmem + lane_off + 256, *reinterpret_cast<uint32_t(*)[32]>(o));
+      tmem_ld_32x32b_x32(tmem + lane_off + 256 + 32, *reinterpret_cast<uint32_t(*)[32]>(o + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty);
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      if (storer) tma_store_wait_read<0>();  // the previous item's store has read the staging
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 v;
+        v.x = pk2<kBf16>(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv);
+        v.y = pk2<kBf16>(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv);
+        v.z = pk2<kBf16>(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv);
+        v.w = pk2<kBf16>(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv);
+        *reinterpret_cast<uint4*>(sO + sw(r, c)) = v;
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (storer) {
+        tma_store_2d(&map_ctx, sO, h * 64, req * S + qb * 128);
+        tma_store_commit();
+      }
+    }
+    if (storer) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 }  // namespace
 
 void launch_attention_tc(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
@@ -316,6 +546,39 @@ void launch_attention_tc(const AttnPlan& p, const int* lens, int n_req, int head
   } else {
     launch_pdl(attention_tc_kernel<false>, dim3(grid), dim3(kTcThreads), kSmem, stream, p.map_qkv,
                p.map_ctx, lens, items, heads, p.d, causal, scale_log2);
+  }
+  HMI_CUDA(cudaGetLastError());
+}
+
+bool attention_long_tc_ok(int S) { return S % 128 == 0 && S >= 256 && S <= 128 * kLMaxBlocks; }
+
+void launch_attention_long_tc(const AttnPlan& p, const int* lens, int n_req, int S, int heads,
+                              int causal, cudaStream_t stream) {
+  if (n_req <= 0) return;
+  HMI_CHECK(attention_long_tc_ok(S) && p.d == heads * 64, HMI_CONFIG_ERROR,
+            "attention: tcgen05 long path needs 256 <= S <= 512, S % 128 == 0, 64-wide heads");
+  const float scale_log2 = 1.4426950408889634f / sqrtf(64.0f);
+  const int nb = S / 128;
+  const int items = n_req * heads * nb;
+  const int grid = items < device_sm_count() ? items : device_sm_count();
+  static bool configured[2] = {false, false};
+  const int bf = p.precision == 1 ? 1 : 0;
+  if (!configured[bf]) {
+    if (bf) {
+      HMI_CUDA(cudaFuncSetAttribute(attention_long_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
+    } else {
+      HMI_CUDA(cudaFuncSetAttribute(attention_long_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
+    }
+    configured[bf] = true;
+  }
+  if (bf) {
+    launch_pdl(attention_long_kernel<true>, dim3(grid), dim3(kLThreads), kLSmem, stream, p.map_qkv,
+               p.map_ctx, lens, items, heads, nb, p.d, causal, scale_log2);
+  } else {
+    launch_pdl(attention_long_kernel<false>, dim3(grid), dim3(kLThreads), kLSmem, stream,
+               p.map_qkv, p.map_ctx, lens, items, heads, nb, p.d, causal, scale_log2);
   }
   HMI_CUDA(cudaGetLastError());
 }

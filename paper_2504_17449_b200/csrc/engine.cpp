@@ -1171,7 +1171,9 @@ int Ctx::submit(uint32_t n_req, const uint32_t* inst, const uint32_t* tokens_hos
       const AttnPlan& ap = attn[kv ? l : 0];
       if (S == 128) {
         launch_attention_tc(ap, d_lens.p, static_cast<int>(n_req), heads, causal, s);
-      } else {
+      } else if (attention_long_tc_ok(S)) {
+        launch_attention_long_tc(ap, d_lens.p, static_cast<int>(n_req), S, heads, causal, s);
+      } else {  // padded lengths beyond 512 (TMEM holds the scores of 4 key blocks of 128)
         launch_attention(qkv_at(l), ctx16.p, d_lens.p, static_cast<int>(n_req), S, d, heads, causal,
                          prec, s);
       }

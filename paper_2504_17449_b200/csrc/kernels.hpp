@@ -85,6 +85,10 @@ AttnPlan make_attention_plan(const void* qkv, void* ctx, int max_rows, int d, in
 // Same, on tcgen05 (S and O in TMEM, softmax warps write P to smem): attention_tc.cu
 void launch_attention_tc(const AttnPlan& p, const int* lens, int n_req, int heads, int causal,
                          cudaStream_t stream);
+// Padded lengths 256..512 on tcgen05 (two-pass softmax over 128-key blocks): attention_tc.cu
+bool attention_long_tc_ok(int S);
+void launch_attention_long_tc(const AttnPlan& p, const int* lens, int n_req, int S, int heads,
+                              int causal, cudaStream_t stream);
 
 // K3: attention core.
 void launch_attention(const void* qkv, void* ctx, const int* lens, int n_req, int S, int d,
