@@ -739,7 +739,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
-  pdl_wait();  // inputs of the previous kernel are complete and visible from here on
+  // pdl_wait (the previous kernel complete and visible) per role: the producer first stages
+  // the shared weights of its first ring lap, which no kernel writes, then waits; the MMA
+  // thread touches no global memory; the epilogue waits before its first read
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -747,6 +749,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_a = policy_evict_first();
       const uint64_t pol_b = policy_evict_last();
       uint32_t stage = 0, phase = 0;
+      // first ring lap: B (shared weights) of the first unit's first stages before pdl_wait
+      int pre = 0;
+      if (cluster < total) {
+        const PairUnit pu = pair_unit<BN>(args, cluster);
+        const CUtensorMap* mb = !pu.tail ? &map_b : args.tail_r1 ? &maps.r1 : &maps.r0;
+        const uint32_t bytes = 2 * (L::kABytes + (pu.width / 2) * kBlockK * 2);
+        const int col = pu.col0 + static_cast<int>(rank) * (pu.width / 2);
+        pre = num_kb < kStages ? num_kb : kStages;
+        for (int kb = 0; kb < pre; ++kb) {
+          if (rank == 0) mbar_arrive_expect_tx(&full[kb], bytes);
+          tma_load_3d_2sm(sB + kb * L::kBBytes, mb, mapa_shared(smem_u32(&full[kb]), 0),
+                          kb * kBlockK, col, 0, pol_b);
+        }
+      }
+      pdl_wait();
       for (int v = cluster; v < total; v += n_clusters) {
         const PairUnit pu = pair_unit<BN>(args, v);
         const int mt = 2 * pu.mp + static_cast<int>(rank);
@@ -754,14 +771,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const CUtensorMap* mb = !pu.tail ? &map_b : args.tail_r1 ? &maps.r1 : &maps.r0;
         const uint32_t bytes = 2 * (L::kABytes + (pu.width / 2) * kBlockK * 2);
         for (int kb = 0; kb < all_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+          const bool staged_b = pre > 0;  // this stage's B went out before pdl_wait
+          if (!staged_b) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+          }
           const uint32_t leader_full = mapa_shared(smem_u32(&full[stage]), 0);
           const int col = pu.col0 + static_cast<int>(rank) * (pu.width / 2);
           if (!kExt || kb < num_kb) {
             tma_load_2d_2sm(sA + stage * L::kABytes, &map_a, leader_full, kb * kBlockK,
                             mt * kBlockM, pol_a);
-            tma_load_3d_2sm(sB + stage * L::kBBytes, mb, leader_full, kb * kBlockK, col, 0, pol_b);
+            if (!staged_b) {
+              tma_load_3d_2sm(sB + stage * L::kBBytes, mb, leader_full, kb * kBlockK, col, 0, pol_b);
+            } else {
+              --pre;
+            }
           } else {
             // tenant block: tile e's ext rows against tile e's slot; the other CTA's A half
             // is the zero rows, so rows of the other request gain nothing
@@ -806,6 +830,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
+    pdl_wait();
     const uint32_t q = warp & 3;
     const int half = static_cast<int>(warp - 2) >> 2;
     uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
