@@ -618,6 +618,17 @@ def bench_generate(args, wl):
                                "adapters": w_adapt, "kv_cache": kv, "logits": logits,
                                "total": step_bytes, "distinct_tenants": tenants,
                                "mean_context": ctx_mean}}
+    # ---- per-class device time (CUDA events around every launch: a separate profile pass; the
+    # events cost the programmatic-launch overlap, so the sum exceeds the timed batch)
+    eng.profile(True)
+    for k in range(K):
+        inst, toks, lens = batches[W + k]
+        eng.generate(inst, toks, lens, wl.gen_tokens)
+    torch.cuda.synchronize()
+    prof = eng.profile_read()
+    eng.profile(False)
+    kernels = {c: {"ms_per_batch": v[0] / K, "launches_per_batch": v[1] / K}
+               for c, v in prof.items() if v[1]}
     line = {
         "metric": f"{wl.name} mixed-tenant generated requests/s (prompt {wl.seq} + {wl.gen_tokens} tokens)",
         "value": value, "unit": "req/s", "n_gpus": world_size, "steps": K, "warmup": W,
@@ -629,6 +640,7 @@ def bench_generate(args, wl):
                 "d2h_bytes_per_step": wl.batch * wl.gen_tokens * 8},
         "gpu_launches": int(c1["launches"] - c0["launches"]),
         "roofline": roof,
+        "kernels": kernels,
         "tensor_frac": value / world_size * wl.generate_flops_per_request() / 1e12 / peak_burst,
         "flops_per_request": wl.generate_flops_per_request(),
         "note": "host API timed (hmi_gpu_generate, synchronous per batch); a side config, the "
