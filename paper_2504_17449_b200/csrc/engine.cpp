@@ -856,7 +856,11 @@ void Ctx::build_lm_plan(LmHead& h) {
   s.b = h.w16; s.N = h.V_pad; s.b_ld = d; s.b_group_stride_bytes = static_cast<size_t>(h.V_pad) * d * 2;
   s.bias = h.bias; s.c = lm_logits.p; s.c_ld = static_cast<int>(lm_logits.n / Bp);
   s.epi = kEpiOutF32;
-  s.bn = pick_bn(h.V_pad, Bp / 128, device_sm_count());
+  // the pair kernel: both 128-row halves of a 256-row batch share each streamed weight tile
+  // (the 1-CTA form read the 77 MB GPT-2 head once per 128-row tile, at BN = 64 re-reading
+  // the rows 786 times)
+  s.cta2 = true;
+  s.bn = pick_bn(h.V_pad, Bp / 128, device_sm_count(), true);
   h.plan = make_gemm_plan(s);
 }
 
