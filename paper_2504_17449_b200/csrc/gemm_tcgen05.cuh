@@ -298,8 +298,10 @@ __device__ __forceinline__ void epilogue_tile(uint32_t t_acc, int mt, int col_ba
       }
     }
     if constexpr (kStaged) {
-      mbar_wait(&rbar[kc], (*rph >> kc) & 1u);
-      *rph ^= 1u << kc;
+      if (row0 < args.M) {  // else nothing was staged: the rows are past the batch
+        mbar_wait(&rbar[kc], (*rph >> kc) & 1u);
+        *rph ^= 1u << kc;
+      }
       const uint8_t* rowp = stg + kc * 4096 + lane * 128;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {  // 16-byte chunks, consumed as they are read
@@ -851,6 +853,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       if (v >= total) return;
       const PairUnit pn = pair_unit<BN>(args, v);
       const int row0 = (2 * pn.mp + static_cast<int>(rank)) * kBlockM + static_cast<int>(q) * 32;
+      if (row0 >= args.M) return;  // rows past the batch (odd tile count): nothing to stage
       tma_store_wait_read<0>();
       int k = 0;
       for (int c = half * 64; c < pn.width; c += 128, ++k) {
