@@ -440,13 +440,15 @@ struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // 8 epilogue warps x (32 rows x 128 B), double-buffered except with staged residuals
-  static constexpr int kEpiBytes = RT ? 8 * 4096 : 8 * 2 * 4096;
+  // 8 epilogue warps x (32 rows x 128 B), double-buffered except with staged residuals and
+  // at BN = 64 (one store per warp and tile: the space goes to ring stages instead)
+  static constexpr bool kSingleStg = RT || BN == 64;
+  static constexpr int kEpiBytes = kSingleStg ? 8 * 4096 : 8 * 2 * 4096;
   // RT: two residual tiles of 128 rows x BN (BN/64 SWIZZLE_128B boxes of 16 KB each)
   static constexpr int kResBytes = RT ? 2 * (BN / 64) * 16384 : 0;
   static constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 256 /*barriers*/;
   static constexpr int kStagesRaw = (kBudget - kEpiBytes - kResBytes) / kStageBytes;
-  static constexpr int kStagesCap = RT ? 2 : 6;  // RT GEMMs have a single K block (K = r)
+  static constexpr int kStagesCap = RT ? 2 : 8;  // RT GEMMs have a single K block (K = r)
   static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
   static constexpr int kTotal =
       1024 + kStages * kStageBytes + kEpiBytes + kResBytes + 256;
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = static_cast<int>(warp - 2) >> 2;
-    uint8_t* stg = sEpi + (warp - 2) * (kRT ? 4096 : 2 * 4096);
+    uint8_t* stg = sEpi + (warp - 2) * (L::kSingleStg ? 4096 : 2 * 4096);
     uint32_t sbuf = 0;
     uint32_t acc = 0, acc_phase = 0, iter = 0;
     for (int t = t_first; t < num_tiles; t += t_step, ++iter) {
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if constexpr (kRT) mbar_wait(res_full, iter & 1);
-      epilogue_tile<BN, EPI>(tmem_base + acc * BN, mt, nt * BN, BN, grp, args, &map_c, stg, sbuf,
+      epilogue_tile<BN, EPI, false, false, L::kSingleStg ? 1 : 2>(tmem_base + acc * BN, mt, nt * BN, BN, grp, args, &map_c, stg, sbuf,
                              q, half, lane, a_st, r_st, sRes);
       if constexpr (kRT) {  // residual tiles consumed: the producer may stage the next tile's
         __syncwarp();

@@ -2,9 +2,10 @@
 """Summarise an `ncu --set full` capture of one C2 layer into profiles/ (text + json).
 
 The capture (tools/profile.sh) holds, in launch order: retrieve, then higher
-layers 0 and 1 (gemm_qkv, attention, gemm_oproj, adapter (fused down+up),
-gemm_ffn1, gemm_ffn2 each; layer 1's QKV is the LN-folded variant). Keys
-without a suffix are layer 1 (the steady-state layer).
+layers 0 and 1 (gemm_qkv, attention, adapter_down (tenant-grouped down
+projection from ctx), gemm_oproj (O projection + the tenants' up projections
++ residual + LN statistics), gemm_ffn1, gemm_ffn2 each; layer 1's QKV is the
+LN-folded variant). Keys without a suffix are layer 1 (the steady-state layer).
 """
 import csv
 import io
@@ -13,7 +14,7 @@ import subprocess
 import sys
 
 # LayerNorm folded (default engine mode): retrieval, then layer 0 and layer 1
-LAYER = ["gemm_qkv", "attention", "gemm_oproj", "adapter_up", "gemm_ffn1", "gemm_ffn2"]
+LAYER = ["gemm_qkv", "attention", "adapter_down", "gemm_oproj", "gemm_ffn1", "gemm_ffn2"]
 ORDER = ["retrieve"] + [f"{k}@L0" for k in LAYER] + LAYER
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
