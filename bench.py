@@ -504,7 +504,9 @@ def bench_ours(args, wl):
         "dtype": "fp16 operands, fp32 accumulate" if args.precision == 0 else "bf16 operands, fp32 accumulate",
         "data": "synthetic (seeded generate_model / adapters / heads, synthetic PLOT tables)",
         "config": config_dict(wl, args, world_size),
-        "e2e": {"value": e2e, "unit": "req/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e, "unit": "req/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "l2": "not flushed: back-to-back serving loop, two batches in flight (the device-"
+                      "timed value flushes L2 before every step)"},
         "gpu_launches": int(c1["launches"] - c0["launches"]),
         "roofline": {
             "bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak_sust,
