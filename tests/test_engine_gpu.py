@@ -387,13 +387,13 @@ def test_full_size_swapping_is_invisible(mode):
         b = small.eng.infer_batch(inst.astype(np.uint32), toks, lens)
         assert np.array_equal(a.scores, b.scores), k
     assert small.eng.pool_stats()["bytes_copied"] > ref.eng.pool_stats()["bytes_copied"]  # re-loads
-    # whole-task misses land in one block of consecutive slots: one transfer per missed tenant,
-    # not one per (tenant, layer)
+    # whole-task misses land in one block of consecutive slots: at most one transfer per missed
+    # tenant, not one per (tenant, layer) (tenants registered and placed side by side share one)
     loads = small.eng.pool_stats()["loads"]
     transfers = E.engine_counters(small.eng)["adapter_copies"]
     L = oracle.BASE.higher_layers
     print(f"{loads} (tenant, layer) loads in {transfers} transfers")
-    assert loads >= L * transfers * 0.9 and transfers >= loads // L
+    assert 1 <= transfers <= -(-loads // L)
     ref.eng.close()
     small.eng.close()
 
