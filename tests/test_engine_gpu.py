@@ -215,9 +215,9 @@ BASE_SMALL = dict(n_tasks=4, r=64, labels=8, max_batch=4, branches=tuple((0, 60)
 
 
 def test_grouped_adapter_gemms_wide_bottleneck():
-    """Bottleneck r = 96 (> 64, padded to 128): the adapter runs as the two tenant-grouped
-    tcgen05 GEMMs (down + ReLU, then up + skip + LN2-residual + row statistics) instead of
-    the fused kernel; parity against the oracle."""
+    """Bottleneck r = 96 (> 64, padded to 128): the adapter runs as the O projection followed by
+    the two tenant-grouped tcgen05 GEMMs (folded down + ReLU, then up + skip + LN2-residual + row
+    statistics) instead of the O projection's tenant K blocks; parity against the oracle."""
     w = World(oracle.TINY, n_tasks=8, r=96, labels=8, max_batch=16)
     inst, toks, lens = w.requests(29, 16, 128)
     res = w.eng.infer_batch(inst, toks, lens)
@@ -399,8 +399,9 @@ def test_full_size_swapping_is_invisible(mode):
 
 
 def test_large_parity_three_level_tree():
-    """C5 shapes (hBERT-large: d=1024, 16 heads, 12 higher layers, ffn 4096, r=64): the fused
-    adapter at d=1024 (16 row-statistics partials), a 3-level domain tree."""
+    """C5 shapes (hBERT-large: d=1024, 16 heads, 12 higher layers, ffn 4096, r=64): the folded
+    adapter and the O projection's tenant K blocks at d=1024 (16 row-statistics partials), a
+    3-level domain tree."""
     w = World(oracle.LARGE, n_tasks=6, r=64, labels=8, max_batch=6,
               branches=((0, 60), (0, 60), (1, 40), (2, 40)), n_hot=64, n_bi=300, n_tri=300)
     inst, toks, lens = w.requests(43, 6, 128, min_len=90)
