@@ -281,6 +281,13 @@ int hmi_pool_op(hmi_pool* pool, int op, uint32_t n, const uint32_t* tasks, uint3
                 hmi_load_record* trace, uint32_t trace_cap, uint32_t* evicted,
                 uint32_t evicted_cap, int32_t* n_trace);
 int hmi_pool_stats(hmi_pool* pool, uint64_t* out);
+/* The same policy with the engine's physical placement: `physical_slots` slots in blocks of
+ * `block_len` (a task's layer l goes to block * block_len + l of the block it claims; any free
+ * slot when no block is free). Residency decisions are the byte budget's alone.
+ * hmi_pool_slot: the slot of a resident (task, layer), else -1. */
+int hmi_pool_create_placed(uint64_t capacity_bytes, uint32_t physical_slots, uint32_t block_len,
+                           hmi_pool** out);
+int hmi_pool_slot(hmi_pool* pool, uint32_t task, uint32_t layer, int32_t* slot);
 
 /* ---- GPU PLOT builder --------------------------
  * The reference's offline table construction: build_root / derive_branch

@@ -187,6 +187,8 @@ def _sig(L):
     L.hmi_pool_op.argtypes = [vp, ctypes.c_int, u32, u32p, u32, P(LoadRecord), u32, u32p, u32,
                               P(i32)]
     L.hmi_pool_stats.argtypes = [vp, u64p]
+    L.hmi_pool_create_placed.argtypes = [u64, u32, u32, P(vp)]
+    L.hmi_pool_slot.argtypes = [vp, u32, u32, P(ctypes.c_int32)]
     L.hmi_generate_model.argtypes = [P(ModelConfig), f32p, f32p, f32p, f32p]
     L.hmi_generate_adapter.argtypes = [P(ModelConfig), u32, u64, f32p]
     L.hmi_generate_head.argtypes = [u32, u32, u64, f32p, f32p]

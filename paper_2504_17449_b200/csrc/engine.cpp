@@ -2904,6 +2904,23 @@ int hmi_pool_create(uint64_t capacity_bytes, hmi_pool** out) {
   });
 }
 
+int hmi_pool_create_placed(uint64_t capacity_bytes, uint32_t physical_slots, uint32_t block_len,
+                           hmi_pool** out) {
+  return guarded([&] {
+    HMI_CHECK(out != nullptr && physical_slots > 0, HMI_CONFIG_ERROR, "pool: physical slots");
+    auto* h = new hmi_pool;
+    h->p = std::make_unique<hmi_b200::SlotPool>(capacity_bytes, physical_slots, block_len);
+    *out = h;
+  });
+}
+
+int hmi_pool_slot(hmi_pool* pool, uint32_t task, uint32_t layer, int32_t* slot) {
+  return guarded([&] {
+    HMI_CHECK(pool != nullptr && slot != nullptr, HMI_CONFIG_ERROR, "null argument");
+    *slot = pool->p->slot_of(task, layer);
+  });
+}
+
 int hmi_pool_destroy(hmi_pool* pool) {
   delete pool;
   return HMI_OK;

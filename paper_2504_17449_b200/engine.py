@@ -369,10 +369,19 @@ class GpuEngine:
 class SlotPoolPolicy:
     """Standalone DeviceSlotPool policy (host only) for trace-parity tests."""
 
-    def __init__(self, capacity_bytes: int):
+    def __init__(self, capacity_bytes: int, physical_slots: int = 0, block_len: int = 1):
         h = ctypes.c_void_p()
-        check(_native.lib().hmi_pool_create(capacity_bytes, ctypes.byref(h)))
+        if physical_slots:  # with the engine's physical slot placement
+            check(_native.lib().hmi_pool_create_placed(capacity_bytes, physical_slots, block_len,
+                                                       ctypes.byref(h)))
+        else:
+            check(_native.lib().hmi_pool_create(capacity_bytes, ctypes.byref(h)))
         self.h = h
+
+    def slot(self, task: int, layer: int) -> int:
+        s = ctypes.c_int32(-1)
+        check(_native.lib().hmi_pool_slot(self.h, task, layer, ctypes.byref(s)))
+        return s.value
 
     def __del__(self):
         if getattr(self, "h", None):
