@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
   float* sc = reinterpret_cast<float*>(vtail + ((T * 128 + 1023) & ~1023));  // [S + T] scores
   __shared__ float qs[64];
   __shared__ float red[32];
-  __shared__ float part[4 * 64];
+  __shared__ __align__(16) float part[4 * 64];
   __shared__ uint64_t bar_k, bar_v;  // K lands first: scores and softmax overlap the V copy
   const int h = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -511,27 +511,32 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
   }
   sum = block_sum_t(sum, red);  // contains the barrier that publishes sc[]
   mbar_wait(&bar_v, 0);
-  // context: warp w takes keys j = w (mod 4); lane its dims 2 lane, 2 lane + 1 (4 bytes of the
-  // row's chunk lane / 4)
-  float a0 = 0.f, a1 = 0.f;
-  const int c = lane >> 2, cb = (lane & 3) * 4;
-  for (int j = warp; j < nk; j += 4) {
-    uint32_t u;
-    if (j == pos) {
-      u = reinterpret_cast<const uint32_t*>(qrow + 2 * d + h * 64)[lane];
-    } else {
-      const uint8_t* box = j < len0 ? vpre : vtail;
-      const int r = j < len0 ? j : j - len0;
-      u = *reinterpret_cast<const uint32_t*>(box + r * 128 + ((c ^ (r & 7)) << 4) + cb);
-    }
-    const float2 v = A.bf16 ? make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u))
-                            : __half22float2(*reinterpret_cast<const __half2*>(&u));
-    const float p = sc[j];
-    a0 += p * v.x;
-    a1 += p * v.y;
+  // context: 8 lanes per value row, lane c its 16-byte chunk c (dims 8c..8c+7); the CTA's 16 lane
+  // groups take rows g, g + 16, ... of the prompt box, then of the generated rows' box, then
+  // group 15 the new row from this step's projections
+  const int g = threadIdx.x >> 3, c = lane & 7;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  auto fma_row = [&](const uint4& u, float p) {
+    float f[8];
+    unpack8(u, f, A.bf16);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += p * f[e];
+  };
+  for (int r = g; r < len0; r += 16) fma_row(*srow(vpre, r, c), sc[r]);
+  for (int r = g; r < n_tail; r += 16) fma_row(*srow(vtail, r, c), sc[len0 + r]);
+  if (g == 15) fma_row(reinterpret_cast<const uint4*>(qrow + 2 * d + h * 64)[c], sc[pos]);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 8);
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
   }
-  part[warp * 64 + 2 * lane] = a0;
-  part[warp * 64 + 2 * lane + 1] = a1;
+  if (lane < 8) {
+    float4* pw = reinterpret_cast<float4*>(part + warp * 64 + c * 8);
+    pw[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    pw[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
   __syncthreads();
   if (threadIdx.x < 64) {
     const int cc = threadIdx.x;
