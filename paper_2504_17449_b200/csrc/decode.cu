@@ -573,15 +573,39 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   const uint16_t* arow = A.ctx16 + static_cast<long long>(b) * d;
   const uint16_t* skiprow = A.a16 + static_cast<long long>(b) * d;  // the adapter's skip input
   const uint16_t* hrow = A.h16 + static_cast<long long>(b) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) a[i] = ld16(arow, i, A.bf16);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(arow)[c], f, A.bf16);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[c * 8 + e] = f[e];
+  }
+  // the up phase's per-output inputs (bias, skip, residual), in flight with the down phase
+  // coalesced up phase (below): lane group g = tid / 8 reads rows g + 32 k of the up projection,
+  // lane c = tid % 8 chunk c of each, and owns the outputs of rows k = c, c + 8, c + 16
+  const bool fast_up = RP == 64 && blockDim.x == 256 && d % 256 == 0 && d <= 768;
+  const int ug = threadIdx.x >> 3, uc = threadIdx.x & 7;
+  float ub[3] = {0.f, 0.f, 0.f}, us[3] = {0.f, 0.f, 0.f}, uh[3] = {0.f, 0.f, 0.f};
+  if (fast_up) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int i = ug + 32 * (uc + 8 * k);
+      if (i < d) {
+        ub[k] = bu[i];
+        us[k] = ld16(skiprow, i, A.bf16);
+        uh[k] = ld16(hrow, i, A.bf16);
+      }
+    }
+  }
   __syncthreads();
   // down projection: warp per bottleneck unit, 16-byte weight vectors across the lanes
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (RP == 64 && nw == 8 && d <= 96 * 8) {
     // every weight load of this warp's 8 units in flight at once (the loop below waits one
-    // memory round trip per unit); same per-lane order of sums, so the same mid[]
+    // memory round trip per unit), their biases with them; same per-lane order of sums, so the
+    // same mid[]
     constexpr int U = RP > 0 ? RP / 8 : 1;
     const int nch = d / 8;
+    const float bdl = lane < U ? bd[warp + 8 * lane] : 0.f;
     uint4 w[U][3];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -606,7 +630,8 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
         }
       }
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) mid[warp + 8 * u] = fmaxf(acc + bd[warp + 8 * u], 0.f);
+      const float bias = __shfl_sync(0xffffffffu, bdl, u);
+      if (lane == 0) mid[warp + 8 * u] = fmaxf(acc + bias, 0.f);
     }
   } else {
     for (int j = warp; j < rp; j += nw) {
@@ -631,32 +656,41 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   __syncthreads();
   // up projection + bias + skip + residual
   float s1 = 0.f;
-  if (RP > 0 && d <= 3 * static_cast<int>(blockDim.x)) {
-    // this thread's (up to) three output rows: all their weight loads in flight at once
-    constexpr int C = RP > 0 ? RP / 8 : 1;
-    uint4 w[3][C];
+  if (fast_up) {
+    // each warp instruction reads four consecutive 128-byte rows (512 contiguous bytes); every
+    // weight load of the group's d / 32 rows in flight at once; row sums reduced over the 8 lanes
+    constexpr int KR = 24;
+    const int nr = d / 32;
+    const uint4* w4 = reinterpret_cast<const uint4*>(wu);
+    uint4 w[KR];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int i = threadIdx.x + k * blockDim.x;
-      const uint4* w4 = reinterpret_cast<const uint4*>(wu + static_cast<size_t>(i < d ? i : 0) * rp);
+    for (int k = 0; k < KR; ++k)
+      w[k] = k < nr ? __ldg(w4 + static_cast<size_t>(ug + 32 * k) * 8 + uc) : make_uint4(0, 0, 0, 0);
+    float m8[8];
 #pragma unroll
-      for (int c = 0; c < C; ++c) w[k][c] = i < d ? __ldg(w4 + c) : make_uint4(0, 0, 0, 0);
+    for (int e = 0; e < 8; ++e) m8[e] = mid[uc * 8 + e];
+    float mine[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      if (k >= nr) break;
+      float f[8];
+      unpack8(w[k], f, A.bf16);
+      float p = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) p += m8[e] * f[e];
+      p += __shfl_xor_sync(0xffffffffu, p, 1);
+      p += __shfl_xor_sync(0xffffffffu, p, 2);
+      p += __shfl_xor_sync(0xffffffffu, p, 4);
+      if ((k & 7) == uc) mine[k >> 3] = p;
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int i = threadIdx.x + k * blockDim.x;
-      if (i >= d) break;
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        float f[8];
-        unpack8(w[k][c], f, A.bf16);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc += mid[c * 8 + e] * f[e];
+    for (int j = 0; j < 3; ++j) {
+      const int i = ug + 32 * (uc + 8 * j);
+      if (uc + 8 * j < nr) {
+        const float v = mine[j] + ub[j] + us[j] + uh[j];
+        y[i] = v;
+        s1 += v;
       }
-      const float v = acc + bu[i] + ld16(skiprow, i, A.bf16) + ld16(hrow, i, A.bf16);
-      y[i] = v;
-      s1 += v;
     }
   } else
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
