@@ -161,16 +161,17 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
       }
     }
   };
-  // 16 logits in flight per thread: 4 x float4 per round (rows are 16-byte aligned, ld % 4 == 0)
+  // 32 logits in flight per thread: 8 x float4 per round (rows are 16-byte aligned, ld % 4 == 0)
+  constexpr int kRound = 8;
   const int V4 = A.V & ~3;
   int j0 = threadIdx.x * 4;
-  for (; j0 + 3 * 4 * kArgThreads < V4; j0 += 4 * 4 * kArgThreads) {
-    float4 x4[4];
+  for (; j0 + (kRound - 1) * 4 * kArgThreads < V4; j0 += kRound * 4 * kArgThreads) {
+    float4 x4[kRound];
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-      x4[t] = *reinterpret_cast<const float4*>(lg + j0 + t * 4 * kArgThreads);
+    for (int t = 0; t < kRound; ++t)
+      x4[t] = __ldcs(reinterpret_cast<const float4*>(lg + j0 + t * 4 * kArgThreads));
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < kRound; ++t) {
       const int jj = j0 + t * 4 * kArgThreads;
       consider(x4[t].x, jj);
       consider(x4[t].y, jj + 1);

@@ -6,7 +6,7 @@ import sys
 WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Cache Throughput", "L1/TEX Cache Throughput",
         "Compute (SM) Throughput", "Registers Per Thread", "Achieved Occupancy", "SM Frequency",
         "One or More Eligible", "No Eligible", "Issued Warp Per Scheduler", "Warp Cycles Per Issued Instruction",
-        "Executed Ipc Active", "Mem Busy", "Max Bandwidth", "Mem Pipes Busy"]
+        "Executed Ipc Active", "Grid Size", "Mem Busy", "Max Bandwidth", "Mem Pipes Busy"]
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[0]
 ix = {h: i for i, h in enumerate(hdr)}
