@@ -416,6 +416,9 @@ constexpr int kDecS = 256;     // max prompt rows staged (2 boxes of 128)
 constexpr int kDecTailBox = 8; // generated rows per tail box (one 1 KB swizzle atom)
 __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_constant__ AttnDecodeMaps M,
                                                              AttnDecodeArgs A) {
+  // the next decode GEMM (programmatic launch) may take free SM space during this grid's last
+  // wave and stream its weights before its griddepcontrol.wait
+  pdl_trigger();
   extern __shared__ uint8_t dsm[];
   uint8_t* base = dsm + ((1024 - (smem_u32(dsm) & 1023)) & 1023);
   const int S = A.S, T = A.tail_cap;
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
 // RP > 0: bottleneck fixed at compile time (all weight loads of a unit / an output in flight)
 template <int RP>
 __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A) {
+  pdl_trigger();  // as in attn_decode_tma_kernel: FFN1 may start streaming its weights
   extern __shared__ float sm[];  // ctx[d] (the down projection's input), y[d], mid[r_pad]
   __shared__ float red[32];
   const int b = blockIdx.x;

@@ -386,6 +386,7 @@ struct Ctx {
   int gen_stride = 0;
   struct DecPlans {
     GemmPlan qkv, oproj, ffn1, ffn2;
+    DecGemmPlan kqkv, koproj, kffn1, kffn2;  // K-split cluster GEMMs (dec_kgemm)
     std::vector<GemmPlan> ffn2_split;  // K slices of FFN2 (f32 partials, no bias / residual)
     AttnDecodeMaps attn;  // TMA maps over this layer's prompt q|k|v and generated k|v
   };
@@ -394,6 +395,9 @@ struct Ctx {
   // into slices run as concurrent branches (aux streams; graph branches when captured) and the
   // LayerNorm after it sums the partials
   int dec_splits = 1;
+  // decode GEMMs as K-split clusters reduced through DSMEM (gemm_dec.cu); HMI_DEC_GEMM=0
+  // keeps the persistent K1 kernel (with FFN2's K slices as graph branches)
+  bool dec_kgemm = true;
   DevBuf<float> dec_part, dec_zero;
   std::vector<cudaStream_t> dec_aux;
   std::vector<cudaEvent_t> dec_ev;  // [0] fork, [1..] joins
@@ -814,16 +818,20 @@ void Ctx::build_plans() {
       s.bias = w.bqkv; s.c = qkv_dec.p; s.c_ld = 3 * d; s.epi = 0;
       s.bn = pick_bn(3 * d, mt, sms);
       dp.qkv = make_gemm_plan(s);
+      if (dec_kgemm) dp.kqkv = make_dec_gemm_plan(s, mt);
       s.a = ctx16.p; s.b = w.wo; s.N = d; s.b_group_stride_bytes = size_t(d) * d * 2;
       s.bias = w.bo; s.c = a16.p; s.c_ld = d; s.bn = pick_bn(d, mt, sms);
       dp.oproj = make_gemm_plan(s);
+      if (dec_kgemm) dp.koproj = make_dec_gemm_plan(s, mt);
       s.a = x16.p; s.b = w.w1; s.N = f; s.b_group_stride_bytes = size_t(f) * d * 2;
       s.bias = w.b1; s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.bn = pick_bn(f, mt, sms);
       dp.ffn1 = make_gemm_plan(s);
+      if (dec_kgemm) dp.kffn1 = make_dec_gemm_plan(s, mt);
       s.a = ffn16.p; s.a_ld = f; s.K = f; s.b = w.w2; s.N = d; s.b_ld = f;
       s.b_group_stride_bytes = size_t(d) * f * 2; s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
       s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, mt, sms);
       dp.ffn2 = make_gemm_plan(s);
+      if (dec_kgemm) dp.kffn2 = make_dec_gemm_plan(s, mt);
       if (dec_splits > 1) {
         const int ks = f / dec_splits;
         for (int sp = 0; sp < dec_splits; ++sp) {
@@ -1350,7 +1358,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
       LayerDev& w = layers[l];
       DecPlans& dp = dec[l];
       const bool last = l == L - 1;
-      timed(P_QKV, s, [&] { launch_gemm(dp.qkv, Mp, s); });
+      timed(P_QKV, s, [&] { dec_kgemm ? launch_dec_gemm(dp.kqkv, Mp, s) : launch_gemm(dp.qkv, Mp, s); });
       timed(P_ATTN, s, [&] {
         AttnDecodeArgs a;
         a.qkv_new = qkv_dec.p;
@@ -1370,7 +1378,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
           launch_attn_decode(a, n, heads, S + static_cast<int>(n_new), s);
         }
       });
-      timed(P_OPROJ, s, [&] { launch_gemm(dp.oproj, Mp, s); });
+      timed(P_OPROJ, s, [&] { dec_kgemm ? launch_dec_gemm(dp.koproj, Mp, s) : launch_gemm(dp.oproj, Mp, s); });
       timed(P_AD_UP, s, [&] {
         AdapterRowsArgs a;
         a.ctx16 = ctx16.p;
@@ -1391,7 +1399,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
         a.bf16 = prec;
         launch_adapter_rows_ln(a, n, s);
       });
-      timed(P_FFN1, s, [&] { launch_gemm(dp.ffn1, Mp, s); });
+      timed(P_FFN1, s, [&] { dec_kgemm ? launch_dec_gemm(dp.kffn1, Mp, s) : launch_gemm(dp.ffn1, Mp, s); });
       if (!dp.ffn2_split.empty()) {
         // K slices as concurrent branches: fork from s, join before the LayerNorm that sums them
         timed(P_FFN2, s, [&] {
@@ -1411,7 +1419,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
                            static_cast<long long>(Bp) * d, w.b2, x16.p);
         });
       } else {
-        timed(P_FFN2, s, [&] { launch_gemm(dp.ffn2, Mp, s); });
+        timed(P_FFN2, s, [&] { dec_kgemm ? launch_dec_gemm(dp.kffn2, Mp, s) : launch_gemm(dp.ffn2, Mp, s); });
         timed(P_LN2, s, [&] {
           launch_layernorm(y32.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p, last ? hdec32.p : nullptr,
                            n, d, prec, s);
@@ -1674,7 +1682,9 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       c.gen_logit.alloc(Bm * T);
       // three slices measured best for GPT-2 small (10.45k vs 10.35k at two, 10.25k unsplit);
       // fall back to the largest count that divides f into 64-wide K blocks
-      c.dec_splits = 3;
+      const char* kg = std::getenv("HMI_DEC_GEMM");
+      c.dec_kgemm = !(kg && std::string(kg) == "0");
+      c.dec_splits = c.dec_kgemm ? 1 : 3;
       while (c.dec_splits > 1 && f % (64 * c.dec_splits) != 0) --c.dec_splits;
       if (c.dec_splits > 1) {
         c.dec_part.alloc(static_cast<size_t>(c.dec_splits) * c.Bp * d);

@@ -135,6 +135,36 @@ struct GemmPlan {
 };
 
 GemmPlan make_gemm_plan(const GemmSpec& s);
+
+// Decode-step GEMM (gemm_dec.cu): one 128 x bn tile per cluster of ks CTAs, each CTA one
+// K / ks slice, partials reduced through distributed shared memory. Epilogues: bias,
+// bias + ReLU, bias -> f32, bias + res0 -> f32.
+struct DecGemmArgs {
+  int num_n_tiles, ks, kb_per_cta;
+  const float* bias;
+  const void* res0;  // 16-bit [rows][res_ld]
+  int res_ld;
+  void* c;           // 16-bit or f32 [rows][c_ld]
+  int c_ld;
+  uint32_t idesc;
+};
+struct DecGemmMaps {
+  CUtensorMap a, b;
+};
+struct DecGemmCfg {
+  int bn, ks;
+};
+struct DecGemmPlan {
+  DecGemmMaps maps;
+  DecGemmArgs args;
+  DecGemmCfg cfg{0, 0};
+  void* fn = nullptr;
+  int smem_bytes = 0;
+  int max_rows = 0;
+};
+DecGemmCfg pick_dec_cfg(int N, int K, int m_tiles, int sms, int epi);
+DecGemmPlan make_dec_gemm_plan(const GemmSpec& s, int m_tiles);
+void launch_dec_gemm(const DecGemmPlan& p, int M, cudaStream_t stream);
 void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream, const uint32_t* ready = nullptr,
                  uint32_t ready_seq = 0, int32_t* err = nullptr);
 

@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
                                                         const float* __restrict__ bias,
                                                         const uint16_t* __restrict__ res16) {
   constexpr int d = 128 * V;
+  // a programmatically launched GEMM after this kernel may stream its weights during the
+  // last wave (it still waits for this grid before reading the rows)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
