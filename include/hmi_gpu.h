@@ -412,8 +412,11 @@ int hmi_gpu_release_export(hmi_gpu_ctx* src, uint32_t task_idx, int drop);
  *   bias     : groups*N f32
  *   tile_slot: M/128 ints selecting the group of each 128-row tile, or NULL
  *   res0/res1: optional M*N 16-bit residuals (epi flags 2/4)
- *   epi      : bit0 ReLU, bit1 +res0, bit2 +res0+res1, bit3 f32 output
- *   bn       : N-tile width (64, 128, 192 or 256)
+ *   epi      : bit0 ReLU, bit1 +res0, bit2 +res0+res1, bit3 f32 output; probe flags:
+ *              256 cta_group::2 pair kernel, 8192 no wave-tail split, 16384 the decode
+ *              K-split cluster kernel (gemm_dec.cu)
+ *   bn       : N-tile width (64, 128, 192 or 256); with 16384: (ks << 16) | width, or 0
+ *              for the decode plan's own choice
  *   out      : M*N, 16-bit or f32 per epi bit3
  *   elapsed_ms (nullable): device time of one launch (CUDA events)        */
 int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups, const uint16_t* a16,

@@ -305,7 +305,8 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
                                   void* out, float* elapsed_ms) {
   const bool cta2 = (epi & 256) != 0;  // probe flag: request the cta_group::2 kernel
   const bool no_tail = (epi & 8192) != 0;  // probe flag: no wave-tail sub-tiles
-  epi &= ~(256 | 8192);
+  const bool dec = (epi & 16384) != 0;     // probe flag: decode K-split cluster kernel
+  epi &= ~(256 | 8192 | 16384);
   using namespace hmi_b200;
   void *dA = nullptr, *dB = nullptr, *dBias = nullptr, *dC = nullptr, *dSlot = nullptr,
        *dR0 = nullptr, *dR1 = nullptr;
@@ -343,15 +344,25 @@ extern "C" int hmi_gpu_gemm_probe(int device, int M, int N, int K, int groups,
     s.tile_slot = static_cast<const int*>(dSlot);
     s.res0 = dR0; s.res1 = dR1; s.res_ld = N;
     s.c = dC; s.c_ld = N;
-    s.epi = epi; s.bn = bn; s.precision = precision; s.cta2 = cta2;
-    GemmPlan p = make_gemm_plan(s);
-    if (no_tail) p.tail_enabled = false;
+    s.epi = epi; s.precision = precision; s.cta2 = cta2;
     HMI_CUDA(cudaEventCreate(&e0));
     HMI_CUDA(cudaEventCreate(&e1));
-    launch_gemm(p, M, 0);  // warm-up / first launch
-    HMI_CUDA(cudaEventRecord(e0, 0));
-    launch_gemm(p, M, 0);
-    HMI_CUDA(cudaEventRecord(e1, 0));
+    if (dec) {  // bn = (ks << 16) | tile width, or 0: the plan's own choice
+      const DecGemmCfg force{bn & 0xffff, bn >> 16};
+      DecGemmPlan p = make_dec_gemm_plan(s, M / kBlockM, force);
+      launch_dec_gemm(p, M, 0);
+      HMI_CUDA(cudaEventRecord(e0, 0));
+      launch_dec_gemm(p, M, 0);
+      HMI_CUDA(cudaEventRecord(e1, 0));
+    } else {
+      s.bn = bn;
+      GemmPlan p = make_gemm_plan(s);
+      if (no_tail) p.tail_enabled = false;
+      launch_gemm(p, M, 0);  // warm-up / first launch
+      HMI_CUDA(cudaEventRecord(e0, 0));
+      launch_gemm(p, M, 0);
+      HMI_CUDA(cudaEventRecord(e1, 0));
+    }
     HMI_CUDA(cudaEventSynchronize(e1));
     if (elapsed_ms) HMI_CUDA(cudaEventElapsedTime(elapsed_ms, e0, e1));
     HMI_CUDA(cudaMemcpy(out, dC, size_t(M) * N * out_elem, cudaMemcpyDeviceToHost));

@@ -163,7 +163,7 @@ struct DecGemmPlan {
   int max_rows = 0;
 };
 DecGemmCfg pick_dec_cfg(int N, int K, int m_tiles, int sms, int epi);
-DecGemmPlan make_dec_gemm_plan(const GemmSpec& s, int m_tiles);
+DecGemmPlan make_dec_gemm_plan(const GemmSpec& s, int m_tiles, DecGemmCfg force = {0, 0});
 void launch_dec_gemm(const DecGemmPlan& p, int M, cudaStream_t stream);
 void launch_gemm(const GemmPlan& p, int M, cudaStream_t stream, const uint32_t* ready = nullptr,
                  uint32_t ready_seq = 0, int32_t* err = nullptr);

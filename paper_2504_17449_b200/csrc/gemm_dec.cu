@@ -298,16 +298,15 @@ DecGemmCfg pick_dec_cfg(int N, int K, int m_tiles, int sms, int epi) {
   return best;
 }
 
-DecGemmPlan make_dec_gemm_plan(const GemmSpec& s, int m_tiles) {
+DecGemmPlan make_dec_gemm_plan(const GemmSpec& s, int m_tiles, DecGemmCfg force) {
   HMI_CHECK(s.K % kBlockK == 0 && s.a_rows % kBlockM == 0 && s.groups == 1 && !s.tile_slot,
             HMI_CONFIG_ERROR, "decode gemm: K % 64, rows % 128, shared weights");
   HMI_CHECK((s.epi & ~(kEpiRelu | kEpiRes1 | kEpiOutF32)) == 0 &&
                 (!(s.epi & kEpiRes1) || (s.res0 && (s.epi & kEpiOutF32))),
             HMI_CONFIG_ERROR, "decode gemm: unsupported epilogue");
   DecGemmPlan p;
-  const char* force = std::getenv("HMI_DEC_CFG");  // "bn,ks" (probe / A-B only)
-  if (force) {
-    std::sscanf(force, "%d,%d", &p.cfg.bn, &p.cfg.ks);
+  if (force.bn > 0) {
+    p.cfg = force;
   } else {
     p.cfg = pick_dec_cfg(s.N, s.K, m_tiles, device_sm_count(), s.epi | (s.precision == 1 ? kEpiBf16 : 0));
   }

@@ -195,3 +195,51 @@ def test_gemm_cta_pair_wave_tail_split_bit_identical(M, N, K, bn, epi):
         if epi & 1:
             ref = np.maximum(ref, 0)
         assert np.abs(split[rows] - ref).max() / np.abs(ref).max() < 2e-3
+
+
+# decode-step GEMMs: K-split clusters reduced through DSMEM (gemm_dec.cu). `cfg` = (bn, ks)
+# forced, or None for the plan's own choice; ks = 3 / 6 split the tile's rows unevenly
+@pytest.mark.parametrize("M,N,K,epi,cfg", [
+    (256, 2304, 768, 0, None), (256, 768, 768, 0, None), (256, 3072, 768, 1, None),
+    (256, 768, 3072, 2 | 8, None), (128, 2304, 768, 0, None), (256, 768, 768, 8, (64, 2)),
+    (256, 2304, 768, 0, (128, 3)), (256, 3072, 768, 1, (256, 6)), (128, 768, 3072, 2 | 8, (64, 8)),
+    (384, 1024, 1024, 1, (128, 4))])
+def test_decode_gemm_ksplit(M, N, K, epi, cfg):
+    rng = np.random.default_rng(M + 3 * N + K)
+    a = rng.standard_normal((M, K)).astype(np.float16)
+    b = rng.uniform(-0.05, 0.05, (1, N, K)).astype(np.float16)
+    bias = rng.uniform(-0.05, 0.05, (1, N)).astype(np.float32)
+    r0 = rng.standard_normal((M, N)).astype(np.float16) if epi & 2 else None
+    bn = 0 if cfg is None else (cfg[1] << 16) | cfg[0]
+    out, _ = _probe(a, b, bias, res0=r0, epi=epi | 16384, bn=bn)
+    ref = _ref(a, b, bias, None, r0, relu=bool(epi & 1))
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err < 2e-3, err
+    again, _ = _probe(a, b, bias, res0=r0, epi=epi | 16384, bn=bn)
+    assert np.array_equal(out, again)  # fixed rank order: run-to-run identical
+
+
+def test_decode_gemm_bf16():
+    rng = np.random.default_rng(5)
+    M, N, K = 256, 2304, 768
+    a32 = rng.standard_normal((M, K)).astype(np.float32)
+    b32 = rng.uniform(-0.05, 0.05, (1, N, K)).astype(np.float32)
+
+    def bf16(x):  # round to nearest even on the top 16 bits
+        u = x.view(np.uint32).astype(np.uint64)
+        u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+        return u
+
+    a16, b16 = bf16(a32), bf16(b32)
+    bias = np.zeros((1, N), np.float32)
+    out = np.zeros((M, N), np.float32)
+    ms = ctypes.c_float(0)
+    st = _native.lib().hmi_gpu_gemm_probe(
+        0, M, N, K, 1, a16.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)),
+        b16.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)),
+        bias.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), None, None, None, 8 | 16384, 0, 1,
+        out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(ms))
+    assert st == 0, _native.last_error()
+    up = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    ref = up(a16) @ up(b16)[0].T
+    assert np.abs(out - ref).max() / np.abs(ref).max() < 2e-3
