@@ -146,47 +146,6 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
     v[k] = -INFINITY;
     ix[k] = 0x7fffffff;
   }
-  auto consider = [&](float x, int xi) {
-    if (x > v[kTopK - 1]) {  // insert, keeping the earlier index first among equals
-#pragma unroll
-      for (int k = 0; k < kTopK; ++k) {
-        if (x > v[k]) {
-          const float tv = v[k];
-          const int ti = ix[k];
-          v[k] = x;
-          ix[k] = xi;
-          x = tv;
-          xi = ti;
-        }
-      }
-    }
-  };
-  // 32 logits in flight per thread: 8 x float4 per round (rows are 16-byte aligned, ld % 4 == 0)
-  constexpr int kRound = 8;
-  const int V4 = A.V & ~3;
-  int j0 = threadIdx.x * 4;
-  for (; j0 + (kRound - 1) * 4 * kArgThreads < V4; j0 += kRound * 4 * kArgThreads) {
-    float4 x4[kRound];
-#pragma unroll
-    for (int t = 0; t < kRound; ++t)
-      x4[t] = __ldcs(reinterpret_cast<const float4*>(lg + j0 + t * 4 * kArgThreads));
-#pragma unroll
-    for (int t = 0; t < kRound; ++t) {
-      const int jj = j0 + t * 4 * kArgThreads;
-      consider(x4[t].x, jj);
-      consider(x4[t].y, jj + 1);
-      consider(x4[t].z, jj + 2);
-      consider(x4[t].w, jj + 3);
-    }
-  }
-  for (; j0 < V4; j0 += 4 * kArgThreads) {
-    const float4 x4 = *reinterpret_cast<const float4*>(lg + j0);
-    consider(x4.x, j0);
-    consider(x4.y, j0 + 1);
-    consider(x4.z, j0 + 2);
-    consider(x4.w, j0 + 3);
-  }
-  for (int j = V4 + static_cast<int>(threadIdx.x); j < A.V; j += kArgThreads) consider(lg[j], j);
   // merge the sorted per-thread lists in registers: each round the warp's best head (value,
   // then lower index) is taken and its owner lane shifts its list; warps' top-k go to shared
   // memory and warp 0 merges those the same way
@@ -222,6 +181,92 @@ __global__ void __launch_bounds__(kArgThreads) lm_argmax_kernel(LmArgmaxArgs A) 
       }
     }
   };
+  // Two passes over the row. Pass 1: each thread's maximum (one FMNMX per logit); the block's
+  // 8th-largest thread maximum tau is a lower bound of the row's 8th-largest logit (8 distinct
+  // logits >= tau exist), so no logit < tau can be a candidate. Pass 2 (the row is L2-resident
+  // from pass 1) offers only logits >= tau to the per-thread top-k, which keeps the insertion
+  // -- ~40 predicated instructions per logit when offered every one -- off the common path.
+  // The candidate set is the one an unfiltered scan selects (value, then lower index).
+  constexpr int kRound = 8;  // 32 logits in flight per thread: 8 x float4 per round
+  const int V4 = A.V & ~3;   // rows are 16-byte aligned (ld % 4 == 0)
+  __shared__ float tau_s;
+  {
+    float tmax = -INFINITY;
+    int j0 = threadIdx.x * 4;
+    for (; j0 + (kRound - 1) * 4 * kArgThreads < V4; j0 += kRound * 4 * kArgThreads) {
+      float4 x4[kRound];
+#pragma unroll
+      for (int t = 0; t < kRound; ++t)
+        x4[t] = *reinterpret_cast<const float4*>(lg + j0 + t * 4 * kArgThreads);
+#pragma unroll
+      for (int t = 0; t < kRound; ++t)
+        tmax = fmaxf(tmax, fmaxf(fmaxf(x4[t].x, x4[t].y), fmaxf(x4[t].z, x4[t].w)));
+    }
+    for (; j0 < V4; j0 += 4 * kArgThreads) {
+      const float4 x4 = *reinterpret_cast<const float4*>(lg + j0);
+      tmax = fmaxf(tmax, fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)));
+    }
+    for (int j = V4 + static_cast<int>(threadIdx.x); j < A.V; j += kArgThreads) tmax = fmaxf(tmax, lg[j]);
+    float hv[kTopK];
+    int hi[kTopK];
+#pragma unroll
+    for (int k = 0; k < kTopK; ++k) {
+      hv[k] = k == 0 ? tmax : -INFINITY;
+      hi[k] = k == 0 ? static_cast<int>(threadIdx.x) : 0x7fffffff;
+    }
+    warp_topk(hv, hi, cv + (threadIdx.x >> 5) * kTopK, ci + (threadIdx.x >> 5) * kTopK);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+#pragma unroll
+      for (int t = 0; t < kTopK; ++t) {
+        const bool own = static_cast<int>(threadIdx.x) < kArgThreads / 32;
+        hv[t] = own ? cv[threadIdx.x * kTopK + t] : -INFINITY;
+        hi[t] = own ? ci[threadIdx.x * kTopK + t] : 0x7fffffff;
+      }
+      float tv[kTopK];
+      int ti[kTopK];
+      warp_topk(hv, hi, tv, ti);
+      if (threadIdx.x == 0) tau_s = tv[kTopK - 1];
+    }
+    __syncthreads();
+  }
+  const float tau = tau_s;
+  auto consider = [&](float x, int xi) {
+    if (x > v[kTopK - 1]) {  // insert, keeping the earlier index first among equals
+#pragma unroll
+      for (int k = 0; k < kTopK; ++k) {
+        if (x > v[k]) {
+          const float tv = v[k];
+          const int ti = ix[k];
+          v[k] = x;
+          ix[k] = xi;
+          x = tv;
+          xi = ti;
+        }
+      }
+    }
+  };
+  auto consider4 = [&](const float4& x4, int jj) {
+    if (fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)) >= tau) {
+      consider(x4.x, jj);
+      consider(x4.y, jj + 1);
+      consider(x4.z, jj + 2);
+      consider(x4.w, jj + 3);
+    }
+  };
+  int j0 = threadIdx.x * 4;
+  for (; j0 + (kRound - 1) * 4 * kArgThreads < V4; j0 += kRound * 4 * kArgThreads) {
+    float4 x4[kRound];
+#pragma unroll
+    for (int t = 0; t < kRound; ++t)
+      x4[t] = __ldcs(reinterpret_cast<const float4*>(lg + j0 + t * 4 * kArgThreads));
+#pragma unroll
+    for (int t = 0; t < kRound; ++t) consider4(x4[t], j0 + t * 4 * kArgThreads);
+  }
+  for (; j0 < V4; j0 += 4 * kArgThreads) consider4(*reinterpret_cast<const float4*>(lg + j0), j0);
+  for (int j = V4 + static_cast<int>(threadIdx.x); j < A.V; j += kArgThreads) {
+    if (lg[j] >= tau) consider(lg[j], j);
+  }
   warp_topk(v, ix, cv + (threadIdx.x >> 5) * kTopK, ci + (threadIdx.x >> 5) * kTopK);
   __syncthreads();
   if (threadIdx.x < 32) {

@@ -386,21 +386,12 @@ struct Ctx {
   int gen_stride = 0;
   struct DecPlans {
     GemmPlan qkv, oproj, ffn1, ffn2;
-    DecGemmPlan kqkv, koproj, kffn1, kffn2;  // K-split cluster GEMMs (dec_kgemm)
-    std::vector<GemmPlan> ffn2_split;  // K slices of FFN2 (f32 partials, no bias / residual)
+    // K-split cluster GEMMs (gemm_dec.cu); fn == nullptr: no (tile, split) fits this shape and
+    // the persistent K1 plan above runs instead
+    DecGemmPlan kqkv, koproj, kffn1, kffn2;
     AttnDecodeMaps attn;  // TMA maps over this layer's prompt q|k|v and generated k|v
   };
   std::vector<DecPlans> dec;
-  // decode FFN2 split-K: the M = 256 GEMM has only d / 64 x 2 tiles, so its K = f loop is cut
-  // into slices run as concurrent branches (aux streams; graph branches when captured) and the
-  // LayerNorm after it sums the partials
-  int dec_splits = 1;
-  // decode GEMMs as K-split clusters reduced through DSMEM (gemm_dec.cu); HMI_DEC_GEMM=0
-  // keeps the persistent K1 kernel (with FFN2's K slices as graph branches)
-  bool dec_kgemm = true;
-  DevBuf<float> dec_part, dec_zero;
-  std::vector<cudaStream_t> dec_aux;
-  std::vector<cudaEvent_t> dec_ev;  // [0] fork, [1..] joins
   // wide lm heads (kind 2, labels > max_labels): 16-bit [V_pad][d] GEMM operand + padded bias
   struct LmHead {
     int V = 0, V_pad = 0;
@@ -553,10 +544,6 @@ Ctx::~Ctx() {
   for (auto& [p, n] : pinned_chunks) host_free_local(p, n);
   for (auto& [k, p] : ipc_open) cudaIpcCloseMemHandle(p);
   for (auto& [k, g] : dec_graphs) cudaGraphExecDestroy(g);
-  for (auto st : dec_aux) cudaStreamDestroy(st);
-  for (auto e : dec_ev) cudaEventDestroy(e);
-  dec_part.free();
-  dec_zero.free();
   for (auto e : ev_layer) cudaEventDestroy(e);
   if (copy2) cudaStreamDestroy(copy2);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -807,6 +794,14 @@ void Ctx::build_plans() {
   dec.clear();
   if (kv) {
     const int mt = Bp / 128;
+    auto dec_plan = [&](const GemmSpec& g) {
+      try {
+        return make_dec_gemm_plan(g, mt);
+      } catch (const HmiError& e) {
+        if (e.code != HMI_CONFIG_ERROR) throw;
+        return DecGemmPlan{};  // no (tile, K split) fits: the K1 plan serves this GEMM
+      }
+    };
     for (int l = 0; l < L; ++l) {
       LayerDev& w = layers[l];
       DecPlans dp;
@@ -818,34 +813,20 @@ void Ctx::build_plans() {
       s.bias = w.bqkv; s.c = qkv_dec.p; s.c_ld = 3 * d; s.epi = 0;
       s.bn = pick_bn(3 * d, mt, sms);
       dp.qkv = make_gemm_plan(s);
-      if (dec_kgemm) dp.kqkv = make_dec_gemm_plan(s, mt);
+      dp.kqkv = dec_plan(s);
       s.a = ctx16.p; s.b = w.wo; s.N = d; s.b_group_stride_bytes = size_t(d) * d * 2;
       s.bias = w.bo; s.c = a16.p; s.c_ld = d; s.bn = pick_bn(d, mt, sms);
       dp.oproj = make_gemm_plan(s);
-      if (dec_kgemm) dp.koproj = make_dec_gemm_plan(s, mt);
+      dp.koproj = dec_plan(s);
       s.a = x16.p; s.b = w.w1; s.N = f; s.b_group_stride_bytes = size_t(f) * d * 2;
       s.bias = w.b1; s.c = ffn16.p; s.c_ld = f; s.epi = kEpiRelu; s.bn = pick_bn(f, mt, sms);
       dp.ffn1 = make_gemm_plan(s);
-      if (dec_kgemm) dp.kffn1 = make_dec_gemm_plan(s, mt);
+      dp.kffn1 = dec_plan(s);
       s.a = ffn16.p; s.a_ld = f; s.K = f; s.b = w.w2; s.N = d; s.b_ld = f;
       s.b_group_stride_bytes = size_t(d) * f * 2; s.bias = w.b2; s.res0 = x16.p; s.res_ld = d;
       s.c = y32.p; s.c_ld = d; s.epi = kEpiRes1 | kEpiOutF32; s.bn = pick_bn(d, mt, sms);
       dp.ffn2 = make_gemm_plan(s);
-      if (dec_kgemm) dp.kffn2 = make_dec_gemm_plan(s, mt);
-      if (dec_splits > 1) {
-        const int ks = f / dec_splits;
-        for (int sp = 0; sp < dec_splits; ++sp) {
-          GemmSpec t = s;
-          t.a = ffn16.p + static_cast<size_t>(sp) * ks;  // columns [sp ks, (sp + 1) ks) of A
-          t.K = ks;
-          t.b = w.w2 + static_cast<size_t>(sp) * ks;
-          t.bias = dec_zero.p;
-          t.res0 = nullptr;
-          t.c = dec_part.p + static_cast<size_t>(sp) * Bp * d;
-          t.epi = kEpiOutF32;
-          dp.ffn2_split.push_back(make_gemm_plan(t));
-        }
-      }
+      dp.kffn2 = dec_plan(s);
       dp.attn = make_attn_decode_maps(qkv_at(l), max_rows,
                                       kv_tail.p + static_cast<size_t>(l) * opt.max_batch *
                                                       opt.max_new_tokens * 2 * d,
@@ -1349,6 +1330,13 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
   am.out_tokens = gen_out.p;
   am.out_logits = gen_logit.p;
   am.out_ld = T;
+  auto launch_dec = [&](const DecGemmPlan& kp, const GemmPlan& g) {
+    if (kp.fn) {
+      launch_dec_gemm(kp, Mp, s);
+    } else {
+      launch_gemm(g, Mp, s);
+    }
+  };
   auto step = [&](uint32_t k) {
     timed(P_RETRIEVE, s, [&] {
       launch_retrieve(P, gen_tokens.p, d_lens.p, d_req_version.p, n, S, 1, h16.p, prec, nullptr,
@@ -1358,7 +1346,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
       LayerDev& w = layers[l];
       DecPlans& dp = dec[l];
       const bool last = l == L - 1;
-      timed(P_QKV, s, [&] { dec_kgemm ? launch_dec_gemm(dp.kqkv, Mp, s) : launch_gemm(dp.qkv, Mp, s); });
+      timed(P_QKV, s, [&] { launch_dec(dp.kqkv, dp.qkv); });
       timed(P_ATTN, s, [&] {
         AttnDecodeArgs a;
         a.qkv_new = qkv_dec.p;
@@ -1378,7 +1366,7 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
           launch_attn_decode(a, n, heads, S + static_cast<int>(n_new), s);
         }
       });
-      timed(P_OPROJ, s, [&] { dec_kgemm ? launch_dec_gemm(dp.koproj, Mp, s) : launch_gemm(dp.oproj, Mp, s); });
+      timed(P_OPROJ, s, [&] { launch_dec(dp.koproj, dp.oproj); });
       timed(P_AD_UP, s, [&] {
         AdapterRowsArgs a;
         a.ctx16 = ctx16.p;
@@ -1399,32 +1387,12 @@ void Ctx::decode_steps(uint32_t n_req, uint32_t n_new, int S, const LmHead& lm, 
         a.bf16 = prec;
         launch_adapter_rows_ln(a, n, s);
       });
-      timed(P_FFN1, s, [&] { dec_kgemm ? launch_dec_gemm(dp.kffn1, Mp, s) : launch_gemm(dp.ffn1, Mp, s); });
-      if (!dp.ffn2_split.empty()) {
-        // K slices as concurrent branches: fork from s, join before the LayerNorm that sums them
-        timed(P_FFN2, s, [&] {
-          HMI_CUDA(cudaEventRecord(dec_ev[0], s));
-          for (size_t i = 1; i < dp.ffn2_split.size(); ++i) {
-            cudaStream_t a = dec_aux[i - 1];
-            HMI_CUDA(cudaStreamWaitEvent(a, dec_ev[0], 0));
-            launch_gemm(dp.ffn2_split[i], Mp, a);
-            HMI_CUDA(cudaEventRecord(dec_ev[i], a));
-          }
-          launch_gemm(dp.ffn2_split[0], Mp, s);
-          for (size_t i = 1; i < dp.ffn2_split.size(); ++i) HMI_CUDA(cudaStreamWaitEvent(s, dec_ev[i], 0));
-        });
-        timed(P_LN2, s, [&] {
-          launch_layernorm(dec_part.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p,
-                           last ? hdec32.p : nullptr, n, d, prec, s, dec_splits,
-                           static_cast<long long>(Bp) * d, w.b2, x16.p);
-        });
-      } else {
-        timed(P_FFN2, s, [&] { dec_kgemm ? launch_dec_gemm(dp.kffn2, Mp, s) : launch_gemm(dp.ffn2, Mp, s); });
-        timed(P_LN2, s, [&] {
-          launch_layernorm(y32.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p, last ? hdec32.p : nullptr,
-                           n, d, prec, s);
-        });
-      }
+      timed(P_FFN1, s, [&] { launch_dec(dp.kffn1, dp.ffn1); });
+      timed(P_FFN2, s, [&] { launch_dec(dp.kffn2, dp.ffn2); });
+      timed(P_LN2, s, [&] {
+        launch_layernorm(y32.p, w.ln2g, w.ln2b, last ? hdec16.p : h16.p, last ? hdec32.p : nullptr,
+                         n, d, prec, s);
+      });
     }
     timed(P_HEAD, s, [&] {
       launch_gemm(lm.plan, Mp, s);
@@ -1680,21 +1648,6 @@ int hmi_gpu_create(int device, const hmi_model_config* cfg, const hmi_gpu_option
       c.gen_pos.alloc(Bm);
       c.gen_out.alloc(Bm * T);
       c.gen_logit.alloc(Bm * T);
-      // three slices measured best for GPT-2 small (10.45k vs 10.35k at two, 10.25k unsplit);
-      // fall back to the largest count that divides f into 64-wide K blocks
-      const char* kg = std::getenv("HMI_DEC_GEMM");
-      c.dec_kgemm = !(kg && std::string(kg) == "0");
-      c.dec_splits = c.dec_kgemm ? 1 : 3;
-      while (c.dec_splits > 1 && f % (64 * c.dec_splits) != 0) --c.dec_splits;
-      if (c.dec_splits > 1) {
-        c.dec_part.alloc(static_cast<size_t>(c.dec_splits) * c.Bp * d);
-        c.dec_zero.alloc(static_cast<size_t>(d));
-        HMI_CUDA(cudaMemset(c.dec_zero.p, 0, static_cast<size_t>(d) * 4));
-        c.dec_aux.resize(c.dec_splits - 1);
-        for (auto& st : c.dec_aux) HMI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        c.dec_ev.resize(c.dec_splits);
-        for (auto& e : c.dec_ev) HMI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      }
     }
     // + 128 zero rows: the other CTA's half of the O projection's tenant K blocks
     c.mid16.alloc((R + 128) * c.r_pad);
