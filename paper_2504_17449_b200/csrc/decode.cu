@@ -505,6 +505,9 @@ __global__ void __launch_bounds__(128) attn_decode_tma_kernel(const __grid_const
     for (int x = 0; x < ntail; ++x)
       tma_load_2d(vtail + x * kDecTailBox * 128, &M.tail, &bar_v, d + h * 64, b * T + kDecTailBox * x);
   }
+  // launched as a programmatic dependent of the QKV GEMM: everything above reads only the prompt
+  // and earlier steps' cache rows; this step's q, k, v are read from here on
+  pdl_wait();
   if (threadIdx.x < 64) qs[threadIdx.x] = ld16(qrow, h * 64 + threadIdx.x, A.bf16);
   __syncthreads();
   // append this row's k, v (head slice) to the generated-rows cache (global; the staged copy of
@@ -623,6 +626,29 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
   const uint16_t* arow = A.ctx16 + static_cast<long long>(b) * d;
   const uint16_t* skiprow = A.a16 + static_cast<long long>(b) * d;  // the adapter's skip input
   const uint16_t* hrow = A.h16 + static_cast<long long>(b) * d;
+  // down projection (fast form): warp per bottleneck unit, 16-byte weight vectors across the
+  // lanes; every weight load of this warp's 8 units in flight at once. The tenant slot is
+  // resident for the whole generate call, so these loads go out before griddepcontrol.wait
+  // (this kernel is a programmatic dependent of the O projection, which triggers at entry)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int U = RP > 0 ? RP / 8 : 1;
+  const bool fast_down = RP == 64 && nw == 8 && d <= 96 * 8;
+  const int nch = d / 8;
+  uint4 w[U][3];
+  float bdl = 0.f;
+  if (fast_down) {
+    bdl = lane < U ? bd[warp + 8 * lane] : 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4* w4 = reinterpret_cast<const uint4*>(wd + static_cast<size_t>(warp + 8 * u) * d);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int c = lane + 32 * m;
+        w[u][m] = c < nch ? __ldg(w4 + c) : make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+  pdl_wait();  // ctx (attention), a (O projection), h (LayerNorm) from here on
   for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
     float f[8];
     unpack8(reinterpret_cast<const uint4*>(arow)[c], f, A.bf16);
@@ -647,25 +673,8 @@ __global__ void __launch_bounds__(256) adapter_rows_ln_kernel(AdapterRowsArgs A)
     }
   }
   __syncthreads();
-  // down projection: warp per bottleneck unit, 16-byte weight vectors across the lanes
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (RP == 64 && nw == 8 && d <= 96 * 8) {
-    // every weight load of this warp's 8 units in flight at once (the loop below waits one
-    // memory round trip per unit), their biases with them; same per-lane order of sums, so the
-    // same mid[]
-    constexpr int U = RP > 0 ? RP / 8 : 1;
-    const int nch = d / 8;
-    const float bdl = lane < U ? bd[warp + 8 * lane] : 0.f;
-    uint4 w[U][3];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint4* w4 = reinterpret_cast<const uint4*>(wd + static_cast<size_t>(warp + 8 * u) * d);
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int c = lane + 32 * m;
-        w[u][m] = c < nch ? __ldg(w4 + c) : make_uint4(0, 0, 0, 0);
-      }
-    }
+  if (fast_down) {
+    // same per-lane order of sums as the general loop below, so the same mid[]
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float acc = 0.f;
@@ -841,8 +850,9 @@ void launch_attn_decode_tma(const AttnDecodeArgs& a, const AttnDecodeMaps& m, in
                                   static_cast<int>(smem)));
     configured = smem;
   }
-  attn_decode_tma_kernel<<<dim3(heads, n_req), 128, smem, stream>>>(m, a);
-  HMI_CUDA(cudaGetLastError());
+  // programmatic dependent of the QKV GEMM (which triggers at entry): the cached K / V copies are
+  // issued before griddepcontrol.wait, under the GEMM
+  launch_pdl(attn_decode_tma_kernel, dim3(heads, n_req), dim3(128), smem, stream, m, a);
 }
 
 void launch_adapter_rows_ln(const AdapterRowsArgs& a, int n_req, cudaStream_t stream) {
@@ -850,9 +860,9 @@ void launch_adapter_rows_ln(const AdapterRowsArgs& a, int n_req, cudaStream_t st
   HMI_CHECK(a.d % 8 == 0 && a.r_pad % 8 == 0, HMI_CONFIG_ERROR, "adapter rows: d, r_pad % 8");
   const size_t smem = static_cast<size_t>(2 * a.d + a.r_pad) * sizeof(float);
   if (a.r_pad == 64) {
-    adapter_rows_ln_kernel<64><<<n_req, 256, smem, stream>>>(a);
+    launch_pdl(adapter_rows_ln_kernel<64>, dim3(n_req), dim3(256), smem, stream, a);
   } else {
-    adapter_rows_ln_kernel<0><<<n_req, 256, smem, stream>>>(a);
+    launch_pdl(adapter_rows_ln_kernel<0>, dim3(n_req), dim3(256), smem, stream, a);
   }
   HMI_CUDA(cudaGetLastError());
 }
