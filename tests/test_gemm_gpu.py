@@ -243,3 +243,24 @@ def test_decode_gemm_bf16():
     up = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
     ref = up(a16) @ up(b16)[0].T
     assert np.abs(out - ref).max() / np.abs(ref).max() < 2e-3
+
+
+def test_decode_gemm_no_fit_is_config_error():
+    """K / 64 = 17 has no split with at most 16 K blocks per CTA: the decode plan refuses with a
+    configuration error (the engine then serves that GEMM with the persistent K1 plan)."""
+    rng = np.random.default_rng(9)
+    M, N, K = 128, 256, 64 * 17
+    a = rng.standard_normal((M, K)).astype(np.float16)
+    b = rng.uniform(-0.05, 0.05, (1, N, K)).astype(np.float16)
+    bias = np.zeros((1, N), np.float32)
+    out = np.zeros((M, N), np.uint16)
+    ms = ctypes.c_float(0)
+    st = _native.lib().hmi_gpu_gemm_probe(
+        0, M, N, K, 1, a.view(np.uint16).ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)),
+        b.view(np.uint16).ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)),
+        bias.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), None, None, None, 16384, 0, 0,
+        out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(ms))
+    assert st == _native.ConfigError.code, (st, _native.last_error())
+    out2, _ = _probe(a, b, bias, bn=64)  # the K1 kernel serves the same shape
+    ref = _ref(a, b, bias, None)
+    assert np.abs(out2 - ref).max() / np.abs(ref).max() < 2e-3
