@@ -24,8 +24,6 @@
 //                 16-bit or f32 rows with coalesced 8- / 16-byte stores.
 #include <cstdio>
 #include <cstdlib>
-#include <mutex>
-#include <vector>
 
 #include "gemm_tcgen05.cuh"
 
